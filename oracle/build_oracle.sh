@@ -1,0 +1,8 @@
+#!/usr/bin/env bash
+# Builds the CPU oracle (test infrastructure only) into oracle/liboracle.so.
+# -ffp-contract=off mirrors the reference's default x86-64 Release build,
+# which emits no fused multiply-adds (proj/CMakeLists.txt:8-10,36).
+set -euo pipefail
+here="$(cd "$(dirname "${BASH_SOURCE[0]}")" && pwd)"
+g++ -std=c++20 -O3 -ffp-contract=off -fPIC -shared -Wall -Wextra \
+    -o "$here/liboracle.so" "$here/fgs_oracle.cpp"
