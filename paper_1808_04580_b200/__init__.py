@@ -1,0 +1,494 @@
+"""paper_1808_04580_b200 -- B200-native NFFT fast-summation graph operator.
+
+Python mirror of the reference's hot-path interface (/root/reference/proj,
+namespace ``fgs``) over the C ABI in ``include/fgs_b200.h``:
+
+=======================  ==========================  ===========================
+reference                this module                 C ABI
+=======================  ==========================  ===========================
+fgs::NfftPlan            NfftPlan                    fgs_nfft_*
+fgs::FastsumParams       FastsumParams               fgs_fastsum_params
+fgs::KernelSpec          KernelSpec                  fgs_kernel + shape
+fgs::FastsumPlan         FastsumPlan                 fgs_fastsum_*
+fgs::AdjacencyOperator   AdjacencyOperator           fgs_adjacency_*
+fgs::lanczos_largest     lanczos_largest             fgs_lanczos_largest
+fgs::make_eigenpairs,    EigenPairs,                 (host)
+adjacency_to_laplacian   adjacency_to_laplacian
+errors.hpp exceptions    ParameterError, ...         fgs_status codes
+=======================  ==========================  ===========================
+
+All compute runs in ``libfgs_b200.so`` (hand-written sm_100a CUDA + cuFFT);
+there is no CPU fallback: importing works anywhere, but constructing a plan
+without a CUDA device raises ``CudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfgs_b200.so")
+
+
+# ---- errors (errors.hpp:8-49) -------------------------------------------
+class FgsError(Exception):
+    """Base of the reference's exception hierarchy mirror."""
+
+
+class ParameterError(FgsError, ValueError):
+    pass
+
+
+class RangeError(FgsError, ValueError):
+    pass
+
+
+class ShapeError(FgsError, ValueError):
+    pass
+
+
+class NumericalError(FgsError, RuntimeError):
+    def __init__(self, msg, bad_node=-1):
+        super().__init__(msg)
+        self.bad_node = bad_node
+
+
+class ResourceError(FgsError, RuntimeError):
+    pass
+
+
+class CudaError(FgsError, RuntimeError):
+    pass
+
+
+class NcclError(FgsError, RuntimeError):
+    pass
+
+
+_ERRORS = {1: ParameterError, 2: RangeError, 3: ShapeError, 4: NumericalError, 5: ResourceError,
+           6: CudaError, 7: NcclError}
+
+GAUSSIAN, LAPLACIAN_RBF, MULTIQUADRIC, INV_MULTIQUADRIC = 0, 1, 2, 3
+OP_KERNEL, OP_WEIGHT, OP_NORMALIZED, OP_SYM_LAPLACIAN = 0, 1, 2, 3
+
+_lib = None
+
+
+class _Params(C.Structure):
+    _fields_ = [("bandwidth", C.c_int), ("cutoff", C.c_int), ("smoothness", C.c_int),
+                ("eps_b", C.c_double), ("oversampling", C.c_double)]
+
+
+def lib():
+    """Load libfgs_b200.so (fails loudly if the extension is not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1808_04580_b200.build` "
+                              "(or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        L.fgs_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(status, bad_node=-1):
+    if status != 0:
+        msg = lib().fgs_last_error().decode()
+        cls = _ERRORS.get(status, FgsError)
+        if cls is NumericalError:
+            raise NumericalError(msg, bad_node)
+        raise cls(msg)
+
+
+_D = C.POINTER(C.c_double)
+
+
+def _dp(a):
+    return a.ctypes.data_as(_D)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _nodes(nodes):
+    a = np.asarray(nodes, dtype=np.float64)
+    if a.ndim == 1:
+        a = a[:, None]
+    n, d = a.shape
+    return np.asfortranarray(a).ravel(order="F").copy(), n, d
+
+
+# ---- parameters (fastsum.hpp:13-23, kernels.hpp:27-35) ------------------
+@dataclass
+class FastsumParams:
+    bandwidth: int = 32
+    cutoff: int = 4
+    smoothness: int = 4
+    eps_b: float = 0.0
+    oversampling: float = 2.0
+
+    @staticmethod
+    def preset(level: int, eps_b: float = 0.0) -> "FastsumParams":
+        p = _Params()
+        _check(lib().fgs_fastsum_preset(int(level), C.c_double(eps_b), C.byref(p)))
+        return FastsumParams(p.bandwidth, p.cutoff, p.smoothness, p.eps_b, p.oversampling)
+
+    def _c(self):
+        return _Params(self.bandwidth, self.cutoff, self.smoothness, self.eps_b, self.oversampling)
+
+
+@dataclass
+class KernelSpec:
+    family: int = GAUSSIAN
+    shape: float = 1.0
+
+    @staticmethod
+    def gaussian(sigma):
+        return KernelSpec(GAUSSIAN, sigma)
+
+    @staticmethod
+    def laplacian_rbf(sigma):
+        return KernelSpec(LAPLACIAN_RBF, sigma)
+
+    @staticmethod
+    def multiquadric(c):
+        return KernelSpec(MULTIQUADRIC, c)
+
+    @staticmethod
+    def inverse_multiquadric(c):
+        return KernelSpec(INV_MULTIQUADRIC, c)
+
+
+def bessel_i0(x: float) -> float:
+    out = C.c_double()
+    _check(lib().fgs_bessel_i0(C.c_double(x), C.byref(out)))
+    return out.value
+
+
+# ---- NfftPlan (nfft.hpp:59-94) ------------------------------------------
+class NfftPlan:
+    def __init__(self, dims, bandwidth, cutoff, nodes, oversampling=2.0, device=0):
+        nd, n, d = _nodes(nodes)
+        h = C.c_void_p()
+        _check(lib().fgs_nfft_create(int(dims), int(bandwidth), int(cutoff), _dp(nd), C.c_int64(n),
+                                     C.c_double(oversampling), int(device), C.byref(h)))
+        self._h = h
+        self._n = n
+        M = C.c_int()
+        F = C.c_int64()
+        _check(lib().fgs_nfft_info(h, C.byref(M), C.byref(F)))
+        self._M, self._F = M.value, F.value
+        self._d, self._N, self._m = dims, bandwidth, cutoff
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().fgs_nfft_destroy(self._h)
+            self._h = None
+
+    def dims(self):
+        return self._d
+
+    def bandwidth(self):
+        return self._N
+
+    def cutoff(self):
+        return self._m
+
+    def node_count(self):
+        return self._n
+
+    def coefficient_count(self):
+        return self._F
+
+    def grid_size(self):
+        return self._M
+
+    def forward(self, fhat) -> np.ndarray:
+        f = np.ascontiguousarray(fhat, dtype=np.complex128)
+        out = np.zeros(self._n, np.complex128)
+        _check(lib().fgs_nfft_forward(self._h, _dp(f.view(np.float64)), C.c_int64(f.size),
+                                      _dp(out.view(np.float64))))
+        return out
+
+    def adjoint(self, x) -> np.ndarray:
+        xv = np.ascontiguousarray(x, dtype=np.complex128)
+        out = np.zeros(self._F, np.complex128)
+        _check(lib().fgs_nfft_adjoint(self._h, _dp(xv.view(np.float64)), C.c_int64(xv.size),
+                                      _dp(out.view(np.float64))))
+        return out
+
+    def forward_real(self, fhat) -> np.ndarray:
+        f = np.ascontiguousarray(fhat, dtype=np.complex128)
+        out = np.zeros(self._n)
+        _check(lib().fgs_nfft_forward_real(self._h, _dp(f.view(np.float64)), C.c_int64(f.size), _dp(out)))
+        return out
+
+
+# ---- FastsumPlan (fastsum.hpp:34-67) ------------------------------------
+class FastsumPlan:
+    def __init__(self, nodes, kernel: KernelSpec, params: FastsumParams = None, device=0):
+        params = params or FastsumParams()
+        nd, n, d = _nodes(nodes)
+        h = C.c_void_p()
+        cp = params._c()
+        _check(lib().fgs_fastsum_create(_dp(nd), C.c_int64(n), int(d), int(kernel.family),
+                                        C.c_double(kernel.shape), C.byref(cp), int(device), C.byref(h)))
+        self._h = h
+        self._n, self._d = n, d
+        self._params = params
+        self._kernel = kernel
+        rho, of, k0, ss = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        _check(lib().fgs_fastsum_info(h, C.byref(rho), C.byref(of), C.byref(k0), C.byref(ss)))
+        self._rho, self._of, self._k0, self._ss = rho.value, of.value, k0.value, ss.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().fgs_fastsum_destroy(self._h)
+            self._h = None
+
+    def size(self):
+        return self._n
+
+    def dims(self):
+        return self._d
+
+    def params(self):
+        return self._params
+
+    def kernel(self):
+        return self._kernel
+
+    def scaled_kernel(self):
+        return KernelSpec(self._kernel.family, self._ss)
+
+    def scaling(self):
+        return self._rho
+
+    def output_factor(self):
+        return self._of
+
+    def kernel_zero(self):
+        return self._k0
+
+    def coefficients(self) -> np.ndarray:
+        out = np.zeros(self._params.bandwidth ** self._d, np.complex128)
+        _check(lib().fgs_fastsum_coefficients(self._h, _dp(out.view(np.float64))))
+        return out
+
+    def apply(self, x) -> np.ndarray:
+        xv = _f64(x)
+        y = np.zeros(xv.size)
+        _check(lib().fgs_fastsum_apply(self._h, _dp(xv), C.c_int64(xv.size), _dp(y)))
+        return y
+
+    def kernel_error_estimate(self, sample_count, seed) -> float:
+        out = C.c_double()
+        _check(lib().fgs_fastsum_error_estimate(self._h, int(sample_count), C.c_uint64(seed), C.byref(out)))
+        return out.value
+
+
+# ---- AdjacencyOperator (graphop.hpp:45-97) ------------------------------
+class AdjacencyOperator:
+    def __init__(self, nodes, kernel: KernelSpec, params: FastsumParams = None, device=0,
+                 rank=0, world=1, nccl_id: bytes = None):
+        params = params or FastsumParams()
+        nd, n, d = _nodes(nodes)
+        h = C.c_void_p()
+        bad = C.c_int64(-1)
+        cp = params._c()
+        if world > 1:
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+            st = lib().fgs_adjacency_create_sharded(_dp(nd), C.c_int64(n), int(d), int(kernel.family),
+                                                    C.c_double(kernel.shape), C.byref(cp), int(device),
+                                                    int(rank), int(world), idbuf, C.byref(h), C.byref(bad))
+        else:
+            st = lib().fgs_adjacency_create(_dp(nd), C.c_int64(n), int(d), int(kernel.family),
+                                            C.c_double(kernel.shape), C.byref(cp), int(device), C.byref(h),
+                                            C.byref(bad))
+        _check(st, bad.value)
+        self._h = h
+        self._n, self._d = n, d
+        self._kernel, self._params = kernel, params
+        rho, of, k0 = C.c_double(), C.c_double(), C.c_double()
+        nl, off = C.c_int64(), C.c_int64()
+        _check(lib().fgs_adjacency_info(h, C.byref(rho), C.byref(of), C.byref(k0), C.byref(nl), C.byref(off)))
+        self._k0 = k0.value
+        self.n_local, self.offset = nl.value, off.value
+        self.world = world
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().fgs_adjacency_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def size(self):
+        return self._n
+
+    def dims(self):
+        return self._d
+
+    def kernel(self):
+        return self._kernel
+
+    def kernel_zero(self):
+        return self._k0
+
+    def degrees(self) -> np.ndarray:
+        out = np.zeros(self._n)
+        _check(lib().fgs_adjacency_degrees(self._h, _dp(out)))
+        return out
+
+    def _apply(self, op, x):
+        xv = np.asarray(x, dtype=np.float64)
+        block = xv.ndim == 2
+        xm = np.asfortranarray(xv if block else xv[:, None])
+        if xm.shape[0] != self._n:
+            raise ShapeError("input length does not match operator dimension")
+        ym = np.zeros_like(xm, order="F")
+        _check(lib().fgs_adjacency_apply(self._h, int(op), _dp(xm), _dp(ym), int(xm.shape[1]),
+                                         C.c_int64(self._n)))
+        return ym if block else ym[:, 0].copy()
+
+    def apply_kernel(self, x):
+        return self._apply(OP_KERNEL, x)
+
+    def apply_weight(self, x):
+        return self._apply(OP_WEIGHT, x)
+
+    def apply_normalized(self, x):
+        return self._apply(OP_NORMALIZED, x)
+
+    def apply_sym_laplacian(self, x):
+        return self._apply(OP_SYM_LAPLACIAN, x)
+
+    def apply_device(self, op, dx_ptr: int, dy_ptr: int, nvec=1, ld=None, internal_order=True):
+        ld = ld if ld is not None else (self.n_local if internal_order else self._n)
+        _check(lib().fgs_adjacency_apply_device(self._h, int(op), C.c_void_p(dx_ptr), C.c_void_p(dy_ptr),
+                                                int(nvec), C.c_int64(ld), int(bool(internal_order))))
+
+    def permute_device(self, dx_ptr: int, dy_ptr: int, nvec=1, ld=None, direction=0):
+        ld = ld if ld is not None else self._n
+        _check(lib().fgs_adjacency_permute_device(self._h, C.c_void_p(dx_ptr), C.c_void_p(dy_ptr), int(nvec),
+                                                  C.c_int64(ld), int(direction)))
+
+    def set_stream(self, stream_ptr: int):
+        _check(lib().fgs_adjacency_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    def profile(self, enable: bool):
+        _check(lib().fgs_adjacency_profile(self._h, int(bool(enable))))
+
+    def profile_read(self):
+        """(ms per stage summed since last read, applies covered); stages =
+        spread, assemble, r2c, multiply, c2r, interp."""
+        ms = np.zeros(6)
+        n = C.c_int64()
+        _check(lib().fgs_adjacency_profile_read(self._h, _dp(ms), C.byref(n)))
+        return ms, n.value
+
+    def geometry(self) -> dict:
+        d, N, M, T, items = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        bs = C.c_int64()
+        _check(lib().fgs_adjacency_geometry(self._h, C.byref(d), C.byref(N), C.byref(M), C.byref(T),
+                                            C.byref(items), C.byref(bs)))
+        return dict(d=d.value, N=N.value, M=M.value, taps=T.value, items=items.value, box_stride=bs.value)
+
+    def launch_count(self) -> int:
+        out = C.c_int64()
+        _check(lib().fgs_adjacency_launch_count(self._h, C.byref(out)))
+        return out.value
+
+
+STAGES = ("spread", "assemble", "fft_r2c", "multiply", "fft_c2r", "interp")
+
+
+def measure_fp64_peak(device=0) -> float:
+    out = C.c_double()
+    _check(lib().fgs_measure_fp64_peak(int(device), C.byref(out)))
+    return out.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().fgs_nccl_unique_id(buf))
+    return buf.raw
+
+
+# ---- spectral (spectral.hpp:33-70) --------------------------------------
+@dataclass
+class LanczosOptions:
+    max_iter: int = 1000
+    tol: float = 1e-12
+    seed: int = 1
+
+
+@dataclass
+class LanczosInfo:
+    iterations: int = 0
+    converged: bool = False
+
+
+@dataclass
+class EigenPairs:
+    values: np.ndarray
+    vectors: np.ndarray
+
+    def count(self):
+        return self.values.size
+
+
+def lanczos_largest(op: AdjacencyOperator, k: int, opts: LanczosOptions = None, info: LanczosInfo = None,
+                    which: int = 0, want_vectors: bool = True) -> EigenPairs:
+    """k largest Ritz pairs of A = D^-1/2 W D^-1/2 (which=0, adjacency_handle)
+    or of L_s (which=1, laplacian_handle), device-resident Lanczos."""
+    opts = opts or LanczosOptions()
+    n = op.size()
+    values = np.zeros(max(k, 1))
+    vectors = np.zeros((n, max(k, 1)), order="F") if want_vectors else None
+    cnt, it, conv = C.c_int(), C.c_int(), C.c_int()
+    _check(lib().fgs_lanczos_largest(op.handle, int(which), int(k), int(opts.max_iter), C.c_double(opts.tol),
+                                     C.c_uint64(opts.seed), _dp(values),
+                                     _dp(vectors) if want_vectors else None,
+                                     C.byref(cnt), C.byref(it), C.byref(conv)))
+    if info is not None:
+        info.iterations, info.converged = it.value, bool(conv.value)
+    c = cnt.value
+    return EigenPairs(values[:c].copy(), vectors[:, :c].copy() if want_vectors else None)
+
+
+def adjacency_to_laplacian(pairs: EigenPairs) -> EigenPairs:
+    """spectral.cpp:129-139: lambda_L = 1 - lambda_A, ascending."""
+    k = pairs.count()
+    vals = np.array([1.0 - pairs.values[k - 1 - i] for i in range(k)])
+    vecs = None if pairs.vectors is None else pairs.vectors[:, ::-1].copy()
+    return EigenPairs(vals, vecs)
+
+
+# ---- synthetic BASELINE workloads ----------------------------------------
+def workload_info(config: int) -> dict:
+    n, d, N, m, p, k = C.c_int64(), C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    sigma = C.c_double()
+    _check(lib().fgs_workload_info(int(config), C.byref(n), C.byref(d), C.byref(sigma), C.byref(N), C.byref(m),
+                                   C.byref(p), C.byref(k)))
+    return dict(n=n.value, d=d.value, sigma=sigma.value, N=N.value, m=m.value, p=p.value, k=k.value)
+
+
+def workload_nodes(config: int, seed: int = 2024) -> np.ndarray:
+    info = workload_info(config)
+    out = np.zeros(info["n"] * info["d"])
+    _check(lib().fgs_workload_generate(int(config), C.c_uint64(seed), _dp(out)))
+    return out.reshape(info["d"], info["n"]).T.copy()
+
+
+def workload_vectors(n: int, nvec: int, seed: int) -> np.ndarray:
+    out = np.zeros(n * nvec)
+    _check(lib().fgs_workload_vectors(C.c_int64(n), int(nvec), C.c_uint64(seed), _dp(out)))
+    return out.reshape(nvec, n).T.copy() if nvec > 1 else out

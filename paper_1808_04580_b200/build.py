@@ -1,0 +1,64 @@
+"""Builds the B200 extension in-tree: paper_1808_04580_b200/libfgs_b200.so.
+
+nvcc -gencode arch=compute_100a,code=sm_100a (sm_100a only), -lineinfo so
+ncu's source page maps to csrc/, objects compiled in parallel, linked against
+cuFFT and NCCL from the CUDA toolkit / system.  Usage: python -m
+paper_1808_04580_b200.build [--force] [--verbose]
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libfgs_b200.so")
+OBJ = os.path.join(ROOT, "build", "obj")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+
+SOURCES = ["core.cu", "lanczos.cu", "capi.cu", "peak.cu", "workload.cpp"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+NVFLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-O3"]
+
+
+def _deps():
+    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "fgs_b200.h")]
+    return max(os.path.getmtime(f) for f in files)
+
+
+def _compile(src: str, verbose: bool) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+    path = os.path.join(CSRC, src)
+    if src.endswith(".cu"):
+        cmd = [NVCC] + COMMON + NVFLAGS + ["-c", path, "-o", obj]
+    else:
+        cmd = ["g++", "-O3", "-std=c++20", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+               "-I", os.path.join(CUDA, "include"), "-c", path, "-o", obj]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return obj
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _deps():
+        return OUT
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+    link = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs + [
+        "-L", os.path.join(CUDA, "lib64"), "-lcufft", "-lcudart", "-ldl",
+        "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64")]
+    if verbose:
+        print(" ".join(link), flush=True)
+    subprocess.run(link, check=True)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))

@@ -1,0 +1,98 @@
+// common.cuh -- error plumbing, plan geometry and device-side PODs shared by
+// the B200 fast-summation kernels (paper_1808_04580_b200/csrc).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "fgs_b200.h"
+
+namespace fgsb {
+
+// Typed failure carrying an fgs_status; the C ABI converts it to a return
+// code + fgs_last_error() message, the C++ drop-in layer rethrows the
+// matching reference exception class (errors.hpp:8-49).
+struct Error : std::runtime_error {
+  fgs_status code;
+  Error(fgs_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(fgs_status code, const std::string& msg) { throw Error(code, msg); }
+
+#define FGS_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      ::fgsb::fail(e_ == cudaErrorMemoryAllocation ? FGS_ERESOURCE : FGS_ECUDA,            \
+                   std::string(#call) + ": " + cudaGetErrorString(e_) + " (" + __FILE__ +  \
+                       ":" + std::to_string(__LINE__) + ")");                             \
+  } while (0)
+
+#define FGS_CUFFT(call)                                                              \
+  do {                                                                               \
+    cufftResult r_ = (call);                                                         \
+    if (r_ != CUFFT_SUCCESS)                                                         \
+      ::fgsb::fail(FGS_ECUDA, std::string(#call) + ": cufft error " +               \
+                                  std::to_string(static_cast<int>(r_)) + " (" + __FILE__ + \
+                                  ":" + std::to_string(__LINE__) + ")");             \
+  } while (0)
+
+// One work item = one CTA of the spread / interp kernels: a run list of
+// point cells inside one spatial tile, with the bounding box of the union of
+// their (2m)^d window footprints.  `a` is the wrapped grid origin of that
+// box, `ext` its extent per dimension (<= B + 2m - 1).
+struct DItem {
+  int run_begin, run_end;
+  int a0, a1, a2;
+  int e0, e1, e2;
+};
+
+// A run = consecutive points (in the internal order) that share the same
+// first window tap u0 = ceil(v M - m) in every dimension, i.e. the same
+// footprint.  `off` packs the footprint origin relative to the item box,
+// 10 bits per dimension.
+struct DRun {
+  int pstart, pcount, off;
+};
+
+// Epilogue selector of the interpolation kernel (graphop.cpp:87-103).
+enum Epilogue : int {
+  EPI_KERNEL = 0,     // y = W~ x                                  apply_kernel
+  EPI_WEIGHT = 1,     // y = W~ x - K0 x                           apply_weight
+  EPI_NORMALIZED = 2, // y = s (W~ (s x) - K0 s x)                 apply_normalized
+  EPI_LAPLACIAN = 3,  // y = x - s (W~ (s x) - K0 s x)             apply_sym_laplacian
+  EPI_DEGREE = 4      // d = W~ 1 - K0;  s = d^-1/2; flag d <= 0    AdjacencyOperator ctor
+};
+
+// Arguments shared by spread and interp launches.
+struct PassArgs {
+  const DItem* items;
+  const DRun* runs;
+  const double* taps;    // [n_local][D][T] internal order
+  const int* perm;       // internal -> caller index (nullable: vectors already internal)
+  int64_t point_base;    // first internal index owned by this shard (perm offset)
+  const double* x;       // input vectors, column j at x + j*ldx
+  int64_t ldx;
+  const double* s;       // D^-1/2 in internal order (nullable)
+  int scale_input;       // multiply x by s before spreading
+  int nvec;
+  int M;
+  double* priv;          // spread: per-item private boxes, item k at priv + k*box_stride
+  int64_t box_stride;    // doubles per item box per vector
+  const double* grid;    // interp: real grid(s), vector j at grid + j*grid_stride
+  int64_t grid_stride;
+  double* y;             // interp output
+  int64_t ldy;
+  int epilogue;
+  double k0;
+  double* degrees;       // EPI_DEGREE outputs (internal order)
+  double* inv_sqrt;
+  unsigned long long* bad_flag;  // EPI_DEGREE: min caller index with d <= 0
+  const int* caller;   // internal -> caller index of this shard's slice (always set)
+};
+
+}  // namespace fgsb

@@ -1,0 +1,983 @@
+// core.cu -- plan construction and apply orchestration of the B200 fast
+// summation (reference: nfft.cpp:328-438, kernels.cpp:266-335,
+// fastsum.cpp:69-118, graphop.cpp:36-103).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <numeric>
+
+#include "core.cuh"
+#include "kernels.cuh"
+#include "nccl_shim.hpp"
+
+namespace fgsb {
+
+void validate_params(const Params& p) {  // fastsum.cpp:25-36
+  if (p.N < 2 || p.N % 2 != 0) fail(FGS_EPARAM, "bandwidth must be even and >= 2");
+  if (p.m < 1 || p.m > 32) fail(FGS_EPARAM, "cutoff must lie in [1, 32]");
+  if (p.p < 1 || p.p > 8) fail(FGS_EPARAM, "smoothness order must lie in [1, 8]");
+  if (!(p.eps_b >= 0.0) || !(p.eps_b < 0.5)) fail(FGS_EPARAM, "blend width must lie in [0, 1/2)");
+  if (!(p.oversampling >= 1.0)) fail(FGS_EPARAM, "oversampling factor must be >= 1");
+}
+
+namespace {
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+inline int round32(int x) { return (x + 31) / 32 * 32; }
+
+// ---- small device kernels of the complex NfftPlan path -------------------
+__global__ void merge_complex_kernel(const double* re, const double* im, cufftDoubleComplex* out, int64_t n) {
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = make_cuDoubleComplex(re[i], im[i]);
+}
+__global__ void split_complex_kernel(const cufftDoubleComplex* in, double* re, double* im, int64_t n) {
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) {
+    re[i] = in[i].x;
+    im[i] = in[i].y;
+  }
+}
+
+// grid offset of frequency multi-index f in FrequencyIndexSet order
+__device__ __forceinline__ int64_t freq_to_grid(int64_t f, int D, int N, int M, double* dec,
+                                                const double* deconv) {
+  int64_t g = 0, stride = 1;
+  double prod = 1.0;
+  double fac[3];
+  int64_t rest = f;
+  for (int t = D - 1; t >= 0; --t) {
+    int a = static_cast<int>(rest % N);
+    rest /= N;
+    int l = a - N / 2;
+    int k = (l + M) % M;
+    g += k * stride;
+    stride *= M;
+    fac[t] = deconv[a];
+  }
+  // (deconv[a] * deconv[c]) * deconv[e] as nfft.cpp:200-201
+  prod = fac[0];
+  for (int t = 1; t < D; ++t) prod = prod * fac[t];
+  *dec = prod;
+  return g;
+}
+
+// place_coefficients (nfft.cpp:174-213) into a zeroed complex grid
+__global__ void place_kernel(const cufftDoubleComplex* fhat, cufftDoubleComplex* grid, int64_t F, int D, int N,
+                             int M, const double* deconv) {
+  int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= F) return;
+  double dec;
+  int64_t g = freq_to_grid(f, D, N, M, &dec, deconv);
+  cufftDoubleComplex v = fhat[f];
+  grid[g] = make_cuDoubleComplex(v.x * dec, v.y * dec);
+}
+
+// extract_coefficients (nfft.cpp:216-250)
+__global__ void extract_kernel(const cufftDoubleComplex* grid, cufftDoubleComplex* fhat, int64_t F, int D, int N,
+                               int M, const double* deconv) {
+  int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= F) return;
+  double dec;
+  int64_t g = freq_to_grid(f, D, N, M, &dec, deconv);
+  cufftDoubleComplex v = grid[g];
+  fhat[f] = make_cuDoubleComplex(v.x * dec, v.y * dec);
+}
+
+// ---- sharded spectrum exchange: window <-> half spectrum ------------------
+struct WindowArgs {
+  cufftDoubleComplex* spec;
+  cufftDoubleComplex* window;
+  const cufftDoubleComplex* mult;
+  int64_t spec_stride, window_stride, total;
+  int nvec, D, M, N;
+};
+
+__device__ __forceinline__ bool window_to_spec(int64_t w, int D, int M, int N, int64_t* sidx) {
+  const int hN = N / 2, W = N + 1, H = M / 2 + 1;
+  int l2 = static_cast<int>(w % (hN + 1));
+  int64_t rest = w / (hN + 1);
+  int l1 = 0, l0 = 0;
+  if (D >= 2) {
+    l1 = static_cast<int>(rest % W) - hN;
+    rest /= W;
+  }
+  if (D == 3) l0 = static_cast<int>(rest) - hN;
+  if (l2 > M / 2) return false;
+  if (M == N && ((D >= 2 && l1 == hN) || (D == 3 && l0 == hN))) return false;  // aliases -N/2
+  int64_t s = l2;
+  if (D >= 2) s += static_cast<int64_t>((l1 + M) % M) * H;
+  if (D == 3) s += static_cast<int64_t>((l0 + M) % M) * H * M;
+  *sidx = s;
+  return true;
+}
+
+__global__ void pack_window_kernel(WindowArgs a) {
+  int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (w >= a.total) return;
+  int64_t s;
+  bool ok = window_to_spec(w, a.D, a.M, a.N, &s);
+  for (int v = 0; v < a.nvec; ++v)
+    a.window[v * a.window_stride + w] = ok ? a.spec[v * a.spec_stride + s] : make_cuDoubleComplex(0.0, 0.0);
+}
+
+__global__ void unpack_multiply_kernel(WindowArgs a) {
+  int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (w >= a.total) return;
+  int64_t s;
+  if (!window_to_spec(w, a.D, a.M, a.N, &s)) return;
+  cufftDoubleComplex m = a.mult[w];
+  for (int v = 0; v < a.nvec; ++v) {
+    cufftDoubleComplex z = a.window[v * a.window_stride + w];
+    a.spec[v * a.spec_stride + s] = make_cuDoubleComplex(z.x * m.x - z.y * m.y, z.x * m.y + z.y * m.x);
+  }
+}
+
+__global__ void fill_kernel(double* x, int64_t n, double v) {
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+
+__global__ void permute_kernel(const double* x, int64_t ldx, double* y, int64_t ldy, const int* perm, int64_t n,
+                               int nvec, int direction) {
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int64_t c = perm[i];
+  for (int v = 0; v < nvec; ++v) {
+    if (direction == 0)
+      y[v * ldy + i] = x[v * ldx + c];  // caller -> internal
+    else
+      y[v * ldy + c] = x[v * ldx + i];  // internal -> caller
+  }
+}
+
+// ---- launch policy of the templated cell-contraction kernels --------------
+struct Policy {
+  int nt;  // threads per CTA
+  bool templated;
+};
+
+Policy policy(int D, int T) {
+  if (T > 16) return {256, false};
+  if (D == 3) return {std::min(256, round32(T * T)), true};
+  return {32, true};
+}
+
+template <int D, int T>
+constexpr int e_of() {
+  return D == 3 ? T : (D == 2 ? (T >= 2 ? T / 2 : 1) : (T >= 2 ? 2 : 1));
+}
+template <int D, int T>
+constexpr int nt_of() {
+  return D == 3 ? ((T * T + 31) / 32 * 32 > 256 ? 256 : (T * T + 31) / 32 * 32) : 32;
+}
+
+template <int D, int T>
+void launch_spread_t(const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
+  constexpr int E = e_of<D, T>();
+  constexpr int NT = nt_of<D, T>();
+  auto k = spread_kernel<D, T, E, NT>;
+  FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k<<<nitems, NT, smem, s>>>(a, T, box_stride);
+}
+
+template <int D, int T>
+void launch_interp_t(const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
+  constexpr int E = e_of<D, T>();
+  constexpr int NT = nt_of<D, T>();
+  auto k = interp_kernel<D, T, E, NT>;
+  FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k<<<nitems, NT, smem, s>>>(a, T, box_stride);
+}
+
+template <int D>
+void dispatch(bool interp, int T, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
+#define FGS_CASE(TT)                                              \
+  case TT:                                                        \
+    if (interp)                                                   \
+      launch_interp_t<D, TT>(a, nitems, smem, box_stride, s);     \
+    else                                                          \
+      launch_spread_t<D, TT>(a, nitems, smem, box_stride, s);     \
+    return;
+  switch (T) {
+    FGS_CASE(2)
+    FGS_CASE(4)
+    FGS_CASE(6)
+    FGS_CASE(8)
+    FGS_CASE(10)
+    FGS_CASE(12)
+    FGS_CASE(14)
+    FGS_CASE(16)
+    default: break;
+  }
+#undef FGS_CASE
+  // runtime-T fallback (m > 8): E = 1, 256 threads
+  if (interp) {
+    auto k = interp_kernel<D, 0, 1, 256>;
+    FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k<<<nitems, 256, smem, s>>>(a, T, box_stride);
+  } else {
+    auto k = spread_kernel<D, 0, 1, 256>;
+    FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k<<<nitems, 256, smem, s>>>(a, T, box_stride);
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+Core::Core(const double* nodes_colmajor, int64_t n_, int d_, Kind kind_, const KernelSpec& kernel_,
+           const Params& params_, int device_, int rank_, int world_, const void* nccl_id)
+    : kind(kind_), d(d_), n(n_), rank(rank_), world(world_), kernel(kernel_), params(params_), device(device_) {
+  if (kind == FASTSUM) {
+    validate_params(params);
+    if (n == 0) fail(FGS_ESHAPE, "node set is empty");
+    if (d < 1 || d > 3) fail(FGS_ESHAPE, "nodes must have 1, 2, or 3 columns");
+    check_spec(kernel);
+  } else {
+    if (d < 1 || d > 3) fail(FGS_EPARAM, "dims must be 1, 2, or 3, got " + std::to_string(d));
+    if (params.N < 2 || params.N % 2 != 0)
+      fail(FGS_EPARAM, "bandwidth must be even and >= 2, got " + std::to_string(params.N));
+    if (n == 0) fail(FGS_ESHAPE, "node set is empty");
+    if (params.m < 1 || params.m > 32)
+      fail(FGS_EPARAM, "cutoff must lie in [1, 32], got " + std::to_string(params.m));
+    if (!(params.oversampling >= 1.0)) fail(FGS_EPARAM, "oversampling factor must be >= 1");
+  }
+  if (world < 1 || rank < 0 || rank >= world) fail(FGS_EPARAM, "invalid shard rank/world");
+  if (n > INT_MAX) fail(FGS_ERESOURCE, "more than 2^31-1 nodes are not supported");
+  N = params.N;
+  m = params.m;
+  T = 2 * m;
+  FGS_CUDA(cudaSetDevice(device));
+  FGS_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+
+  if (kind == FASTSUM) {
+    // common rescaling into the ball of radius 1/4 - eps_b/2 (fastsum.cpp:79-88)
+    const double radius = 0.25 - 0.5 * params.eps_b;
+    if (!(radius > 0.0)) fail(FGS_EPARAM, "blend width leaves no node radius");
+    double maxnorm = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int t = 0; t < d; ++t) {
+        const double v = nodes_colmajor[t * n + j];
+        s += v * v;
+      }
+      const double nr = std::sqrt(s);
+      if (j == 0 || nr > maxnorm) maxnorm = nr;
+    }
+    rho = (maxnorm > radius) ? radius / maxnorm : 1.0;
+    scaled = kernel;
+    scaled.shape = kernel.shape * rho;
+    out_factor = 1.0;
+    if (kernel.family == FGS_MULTIQUADRIC) out_factor = 1.0 / rho;
+    if (kernel.family == FGS_INV_MULTIQUADRIC) out_factor = rho;
+    k0 = kernel_value(kernel, 0.0);
+    reg = RegKernel(scaled, params.eps_b, params.p);
+  }
+
+  // NFFT geometry (nfft.cpp:343-354)
+  M = 2 * static_cast<int>(std::ceil(params.oversampling * N / 2.0));
+  b_kb = kPi * (2.0 - static_cast<double>(N) / M);
+  deconv.resize(static_cast<size_t>(N));
+  for (int a = 0; a < N; ++a) {
+    const double l = a - N / 2;
+    const double arg = b_kb * b_kb - std::pow(2.0 * kPi * l / M, 2);
+    deconv[static_cast<size_t>(a)] = 1.0 / i0_series(m * std::sqrt(std::max(arg, 0.0)));
+  }
+  double gsz = 1.0;
+  for (int t = 0; t < d; ++t) gsz *= M;
+  if (gsz > 2.0e9) fail(FGS_ERESOURCE, "oversampled grid exceeds 2^31 points");
+  B = d == 3 ? 4 : (d == 2 ? 8 : 32);
+  if (B > M) B = M;
+  nt = ceil_div(M, B);
+  ntiles = 1;
+  for (int t = 0; t < d; ++t) ntiles *= nt;
+  grid_elems = 1;
+  for (int t = 0; t < d; ++t) grid_elems *= M;
+  spec_elems = grid_elems / M * (M / 2 + 1);
+  window_elems = (N / 2 + 1);
+  for (int t = 0; t + 1 < d; ++t) window_elems *= (N + 1);
+  deconv_d.upload(deconv.data(), deconv.size(), stream);
+
+  build_plan(nodes_colmajor);
+  if (kind == FASTSUM) build_coefficients();
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    nccl_check(nccl().comm_init_rank(&comm, world, id, rank), "ncclCommInitRank");
+  }
+  FGS_CUDA(cudaStreamSynchronize(stream));
+}
+
+Core::~Core() {
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto& kv : ws_) {
+    if (kv.second->has_plans) {
+      cufftDestroy(kv.second->r2c);
+      cufftDestroy(kv.second->c2r);
+    }
+    if (kv.second->has_z2z) cufftDestroy(kv.second->z2z);
+  }
+  ws_.clear();
+  for (auto& evs : ev_pending_)
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  if (comm) nccl().comm_destroy(comm);
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+void Core::set_stream(cudaStream_t s) {
+  FGS_CUDA(cudaStreamSynchronize(stream));
+  if (own_stream) cudaStreamDestroy(stream);
+  stream = s;
+  own_stream = false;
+  for (auto& kv : ws_) {
+    if (kv.second->has_plans) {
+      FGS_CUFFT(cufftSetStream(kv.second->r2c, stream));
+      FGS_CUFFT(cufftSetStream(kv.second->c2r, stream));
+    }
+    if (kv.second->has_z2z) FGS_CUFFT(cufftSetStream(kv.second->z2z, stream));
+  }
+}
+
+void Core::build_plan(const double* nodes_colmajor) {
+  DBuf<double> dnodes;
+  dnodes.upload(nodes_colmajor, static_cast<size_t>(n) * d, stream);
+  DBuf<unsigned long long> keys, keys_sorted, bad;
+  DBuf<int> idx;
+  keys.alloc(n);
+  keys_sorted.alloc(n);
+  idx.alloc(n);
+  perm.alloc(n);
+  bad.alloc(1);
+  unsigned long long init = ULLONG_MAX;
+  FGS_CUDA(cudaMemcpyAsync(bad.p, &init, sizeof(init), cudaMemcpyHostToDevice, stream));
+
+  PointArgs pa{dnodes.p, n, d, M, m, B, nt, rho, kind == FASTSUM ? 1 : 0, keys.p, idx.p, bad.p};
+  point_keys_kernel<<<ceil_div(n, 256), 256, 0, stream>>>(pa);
+  ++launches;
+  FGS_CUDA(cudaGetLastError());
+  unsigned long long badj = 0;
+  FGS_CUDA(cudaMemcpyAsync(&badj, bad.p, sizeof(badj), cudaMemcpyDeviceToHost, stream));
+  FGS_CUDA(cudaStreamSynchronize(stream));
+  if (badj != ULLONG_MAX) {
+    // validate_common (nfft.cpp:42-49): name the first offending node
+    const int64_t j = static_cast<int64_t>(badj);
+    for (int t = 0; t < d; ++t) {
+      double v = nodes_colmajor[t * n + j];
+      if (kind == FASTSUM) v = rho * v;
+      if (!(v >= -0.5 && v < 0.5))
+        fail(FGS_ERANGE, "node " + std::to_string(j) + " component " + std::to_string(t) + " = " +
+                             std::to_string(v) + " outside [-1/2, 1/2)");
+    }
+  }
+
+  // stable radix sort by (tile, cell): the internal order
+  int end_bit = 1;
+  {
+    double total = 1.0;
+    for (int t = 0; t < d; ++t) total *= static_cast<double>(nt) * B;
+    while (end_bit < 64 && std::ldexp(1.0, end_bit) < total) ++end_bit;
+  }
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys_sorted.p, idx.p, perm.p, static_cast<int>(n), 0,
+                                  end_bit, stream);
+  DBuf<char> tmp;
+  tmp.alloc(tmp_bytes);
+  FGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys_sorted.p, idx.p, perm.p,
+                                           static_cast<int>(n), 0, end_bit, stream));
+  // run-length encode the sorted keys: one entry per nonempty cell
+  DBuf<unsigned long long> uniq;
+  DBuf<int> counts, nruns;
+  uniq.alloc(n);
+  counts.alloc(n);
+  nruns.alloc(1);
+  size_t tmp2 = 0;
+  cub::DeviceRunLengthEncode::Encode(nullptr, tmp2, keys_sorted.p, uniq.p, counts.p, nruns.p, static_cast<int>(n),
+                                     stream);
+  DBuf<char> tmpb;
+  tmpb.alloc(tmp2);
+  FGS_CUDA(cub::DeviceRunLengthEncode::Encode(tmpb.p, tmp2, keys_sorted.p, uniq.p, counts.p, nruns.p,
+                                              static_cast<int>(n), stream));
+  int ncells = 0;
+  FGS_CUDA(cudaMemcpyAsync(&ncells, nruns.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  FGS_CUDA(cudaStreamSynchronize(stream));
+  std::vector<unsigned long long> hkeys(static_cast<size_t>(ncells));
+  std::vector<int> hcounts(static_cast<size_t>(ncells));
+  FGS_CUDA(cudaMemcpyAsync(hkeys.data(), uniq.p, sizeof(unsigned long long) * ncells, cudaMemcpyDeviceToHost, stream));
+  FGS_CUDA(cudaMemcpyAsync(hcounts.data(), counts.p, sizeof(int) * ncells, cudaMemcpyDeviceToHost, stream));
+  host_perm.resize(static_cast<size_t>(n));
+  FGS_CUDA(cudaMemcpyAsync(host_perm.data(), perm.p, sizeof(int) * n, cudaMemcpyDeviceToHost, stream));
+  FGS_CUDA(cudaStreamSynchronize(stream));
+
+  // shard slice of the internal order
+  offset = n * rank / world;
+  n_local = n * (rank + 1) / world - offset;
+
+  // ---- work items: runs of cells inside one tile, <= chunk points ---------
+  int64_t target_items = 4 * 148;
+  int chunk = static_cast<int>(std::max<int64_t>(64, std::min<int64_t>(4096, (n_local + target_items - 1) / target_items)));
+  chunk = (chunk + 31) / 32 * 32;
+  int BD = 1;
+  for (int t = 0; t < d; ++t) BD *= B;
+
+  struct HRun {
+    int pstart, pcount;
+    int c[3];
+  };
+  struct HItem {
+    int tile;
+    std::vector<HRun> runs;
+    int npts = 0;
+  };
+  std::vector<HItem> hitems;
+  auto decode_cell = [&](unsigned long long key, int* tcoord, int* cc) {
+    unsigned long long tile = key / BD, cell = key % BD;
+    for (int t = 2; t >= 0; --t) {
+      if (t >= 3 - d) {
+        cc[t] = static_cast<int>(cell % B);
+        cell /= B;
+        tcoord[t] = static_cast<int>(tile % nt);
+        tile /= nt;
+      } else {
+        cc[t] = 0;
+        tcoord[t] = 0;
+      }
+    }
+  };
+  {
+    int64_t start = 0;
+    HItem cur;
+    cur.tile = -1;
+    auto flush = [&]() {
+      if (!cur.runs.empty()) hitems.push_back(std::move(cur));
+      cur = HItem();
+      cur.tile = -1;
+    };
+    for (int c = 0; c < ncells; ++c) {
+      const int64_t cs = start, ce = start + hcounts[static_cast<size_t>(c)];
+      start = ce;
+      const int64_t lo = std::max(cs, offset), hi = std::min(ce, offset + n_local);
+      if (lo >= hi) continue;
+      const int tile = static_cast<int>(hkeys[static_cast<size_t>(c)] / BD);
+      if (tile != cur.tile) flush();
+      cur.tile = tile;
+      int tc[3], cc[3];
+      decode_cell(hkeys[static_cast<size_t>(c)], tc, cc);
+      int64_t p = lo;
+      while (p < hi) {
+        int take = static_cast<int>(std::min<int64_t>(hi - p, chunk - cur.npts));
+        if (take <= 0) {
+          flush();
+          cur.tile = tile;
+          continue;
+        }
+        HRun r;
+        r.pstart = static_cast<int>(p - offset);
+        r.pcount = take;
+        r.c[0] = cc[0];
+        r.c[1] = cc[1];
+        r.c[2] = cc[2];
+        cur.runs.push_back(r);
+        cur.npts += take;
+        p += take;
+        if (cur.npts >= chunk) {
+          flush();
+          cur.tile = tile;
+        }
+      }
+    }
+    flush();
+  }
+  // heaviest items first (LPT order for the block scheduler)
+  std::stable_sort(hitems.begin(), hitems.end(), [](const HItem& x, const HItem& y) { return x.npts > y.npts; });
+
+  nitems = static_cast<int>(hitems.size());
+  std::vector<DItem> ditems;
+  std::vector<DRun> druns;
+  std::vector<std::vector<int>> tile_lists(static_cast<size_t>(ntiles));
+  const int Md[3] = {d == 3 ? M : 1, d >= 2 ? M : 1, M};
+  box_stride = 1;
+  for (int k = 0; k < nitems; ++k) {
+    const HItem& h = hitems[static_cast<size_t>(k)];
+    int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+    for (const HRun& r : h.runs)
+      for (int t = 0; t < 3; ++t) {
+        lo[t] = std::min(lo[t], r.c[t]);
+        hi[t] = std::max(hi[t], r.c[t]);
+      }
+    int tc[3], cc[3];
+    decode_cell(static_cast<unsigned long long>(h.tile) * BD, tc, cc);
+    DItem it;
+    it.run_begin = static_cast<int>(druns.size());
+    for (const HRun& r : h.runs) {
+      DRun dr;
+      dr.pstart = r.pstart;
+      dr.pcount = r.pcount;
+      dr.off = (r.c[0] - lo[0]) | ((r.c[1] - lo[1]) << 10) | ((r.c[2] - lo[2]) << 20);
+      druns.push_back(dr);
+    }
+    it.run_end = static_cast<int>(druns.size());
+    int ext[3], org[3];
+    for (int t = 0; t < 3; ++t) {
+      const bool used = t >= 3 - d;
+      ext[t] = used ? (hi[t] - lo[t] + T) : 1;
+      org[t] = used ? ((tc[t] * B + lo[t]) % M) : 0;
+    }
+    it.a0 = org[0];
+    it.a1 = org[1];
+    it.a2 = org[2];
+    it.e0 = ext[0];
+    it.e1 = ext[1];
+    it.e2 = ext[2];
+    box_stride = std::max<int64_t>(box_stride, static_cast<int64_t>(ext[0]) * ext[1] * ext[2]);
+    ditems.push_back(it);
+    // covered tiles (with periodic wrap) -> assembly lists
+    std::vector<int> cov[3];
+    for (int t = 0; t < 3; ++t) {
+      if (t < 3 - d) {
+        cov[t].push_back(0);
+        continue;
+      }
+      for (int i = 0; i < ext[t]; ++i) {
+        const int tt = ((org[t] + i) % Md[t]) / B;
+        if (std::find(cov[t].begin(), cov[t].end(), tt) == cov[t].end()) cov[t].push_back(tt);
+      }
+    }
+    for (int t0 : cov[0])
+      for (int t1 : cov[1])
+        for (int t2 : cov[2]) {
+          int lin = 0;
+          if (d == 3) lin = (t0 * nt + t1) * nt + t2;
+          if (d == 2) lin = t1 * nt + t2;
+          if (d == 1) lin = t2;
+          tile_lists[static_cast<size_t>(lin)].push_back(k);
+        }
+  }
+  box_stride = (box_stride + 1) / 2 * 2;  // keep the staging area 16-byte aligned
+  std::vector<int> tptr(static_cast<size_t>(ntiles) + 1, 0), titems;
+  for (int t = 0; t < ntiles; ++t) {
+    tptr[static_cast<size_t>(t) + 1] = tptr[static_cast<size_t>(t)] + static_cast<int>(tile_lists[static_cast<size_t>(t)].size());
+    titems.insert(titems.end(), tile_lists[static_cast<size_t>(t)].begin(), tile_lists[static_cast<size_t>(t)].end());
+  }
+  if (ditems.empty()) {
+    ditems.push_back(DItem{0, 0, 0, 0, 0, 1, 1, 1});
+    nitems = 0;
+  }
+  if (titems.empty()) titems.push_back(0);
+  items.upload(ditems.data(), ditems.size(), stream);
+  if (druns.empty()) druns.push_back(DRun{0, 0, 0});
+  runs.upload(druns.data(), druns.size(), stream);
+  tile_ptr.upload(tptr.data(), tptr.size(), stream);
+  tile_items.upload(titems.data(), titems.size(), stream);
+
+  // window taps of the local slice in internal order
+  taps.alloc(static_cast<size_t>(std::max<int64_t>(n_local, 1)) * d * T);
+  if (n_local > 0) {
+    TapArgs ta{dnodes.p, n, n_local, perm.p + offset, d, M, m, rho, b_kb, kind == FASTSUM ? 1 : 0, taps.p};
+    taps_kernel<<<ceil_div(n_local, 128), 128, 0, stream>>>(ta);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+  }
+  FGS_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Core::build_coefficients() {
+  // bhat_l = (-1)^{sum l} N^-d FFT[K_R(j/N)] (kernels.cpp:266-335); the N^d
+  // transform runs on the device (cuFFT Z2Z, FFTW_FORWARD sign)
+  size_t total = 1;
+  for (int t = 0; t < d; ++t) total *= static_cast<size_t>(N);
+  const int half = N / 2;
+  std::vector<cufftDoubleComplex> samples(total);
+  int idx[3] = {0, 0, 0};
+  for (size_t flat = 0; flat < total; ++flat) {
+    size_t rest = flat;
+    for (int t = d - 1; t >= 0; --t) {
+      idx[t] = static_cast<int>(rest % N);
+      rest /= N;
+    }
+    double s2 = 0.0;
+    for (int t = 0; t < d; ++t) {
+      const double y = static_cast<double>(idx[t] - half) / N;
+      s2 += y * y;
+    }
+    samples[flat] = make_cuDoubleComplex(reg(std::sqrt(s2)), 0.0);
+  }
+  DBuf<cufftDoubleComplex> buf;
+  buf.upload(samples.data(), total, stream);
+  cufftHandle plan;
+  int dims[3] = {N, N, N};
+  FGS_CUFFT(cufftPlanMany(&plan, d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2Z, 1));
+  FGS_CUFFT(cufftSetStream(plan, stream));
+  FGS_CUFFT(cufftExecZ2Z(plan, buf.p, buf.p, CUFFT_FORWARD));
+  FGS_CUDA(cudaMemcpyAsync(samples.data(), buf.p, total * sizeof(cufftDoubleComplex), cudaMemcpyDeviceToHost, stream));
+  FGS_CUDA(cudaStreamSynchronize(stream));
+  cufftDestroy(plan);
+  bhat.resize(total);
+  const double norm = 1.0 / static_cast<double>(total);
+  for (size_t flat = 0; flat < total; ++flat) {
+    size_t rest = flat, bin = 0, stride = 1;
+    int lsum = 0;
+    for (int t = d - 1; t >= 0; --t) {
+      const int a = static_cast<int>(rest % N);
+      rest /= N;
+      const int l = a - half;
+      lsum += l;
+      bin += static_cast<size_t>((l + N) % N) * stride;
+      stride *= static_cast<size_t>(N);
+    }
+    const double sign = (lsum % 2 == 0) ? 1.0 : -1.0;
+    bhat[flat] = std::complex<double>(samples[bin].x, samples[bin].y) * (sign * norm);
+  }
+
+  // compact Hermitian-symmetrised multiplier (see multiply_kernel)
+  auto mval = [&](const int* k) -> std::complex<double> {  // m_k on wrap(I_N)
+    size_t flat = 0;
+    double dec = 1.0;
+    for (int t = 0; t < d; ++t) {
+      int l;
+      if (k[t] < half)
+        l = k[t];
+      else if (k[t] >= M - half)
+        l = k[t] - M;
+      else
+        return 0.0;
+      flat = flat * N + static_cast<size_t>(l + half);
+      dec = (t == 0) ? deconv[static_cast<size_t>(l + half)] : dec * deconv[static_cast<size_t>(l + half)];
+    }
+    return out_factor * (bhat[flat] * (dec * dec));
+  };
+  std::vector<cufftDoubleComplex> hm(static_cast<size_t>(window_elems));
+  const int W = N + 1, hN = N / 2;
+  for (int64_t w = 0; w < window_elems; ++w) {
+    int l[3] = {0, 0, 0};
+    l[d - 1] = static_cast<int>(w % (hN + 1));
+    int64_t rest = w / (hN + 1);
+    for (int t = d - 2; t >= 0; --t) {
+      l[t] = static_cast<int>(rest % W) - hN;
+      rest /= W;
+    }
+    int k[3], km[3];
+    for (int t = 0; t < d; ++t) {
+      k[t] = ((l[t] % M) + M) % M;
+      km[t] = ((-l[t] % M) + M) % M;
+    }
+    std::complex<double> v = 0.5 * (mval(k) + std::conj(mval(km)));
+    hm[static_cast<size_t>(w)] = make_cuDoubleComplex(v.real(), v.imag());
+  }
+  mult.upload(hm.data(), hm.size(), stream);
+  FGS_CUDA(cudaStreamSynchronize(stream));
+}
+
+Workspace& Core::workspace(int nvec) {
+  auto itw = ws_.find(nvec);
+  if (itw != ws_.end()) return *itw->second;
+  auto w = std::make_unique<Workspace>();
+  w->nvec = nvec;
+  w->priv.alloc(static_cast<size_t>(std::max(nitems, 1)) * box_stride * nvec);
+  w->grid.alloc(static_cast<size_t>(grid_elems) * nvec);
+  w->spec.alloc(static_cast<size_t>(spec_elems) * nvec);
+  if (world > 1) w->window.alloc(static_cast<size_t>(window_elems) * nvec);
+  int dims[3] = {M, M, M};
+  FGS_CUFFT(cufftPlanMany(&w->r2c, d, dims, nullptr, 1, static_cast<int>(grid_elems), nullptr, 1,
+                          static_cast<int>(spec_elems), CUFFT_D2Z, nvec));
+  FGS_CUFFT(cufftPlanMany(&w->c2r, d, dims, nullptr, 1, static_cast<int>(spec_elems), nullptr, 1,
+                          static_cast<int>(grid_elems), CUFFT_Z2D, nvec));
+  FGS_CUFFT(cufftSetStream(w->r2c, stream));
+  FGS_CUFFT(cufftSetStream(w->c2r, stream));
+  w->has_plans = true;
+  auto& ref = *w;
+  ws_[nvec] = std::move(w);
+  return ref;
+}
+
+size_t Core::smem_bytes(bool interp) const {
+  const Policy pol = policy(d, T);
+  size_t dbl = static_cast<size_t>(box_stride) + static_cast<size_t>(kQ) * d * T + kQ + (interp ? pol.nt : 0);
+  return dbl * sizeof(double);
+}
+
+void Core::launch_spread(const PassArgs& a) {
+  if (nitems == 0) return;
+  const size_t smem = smem_bytes(false);
+  if (smem > 227 * 1024) fail(FGS_ERESOURCE, "tile box exceeds shared memory (cutoff too large for d = 3)");
+  if (d == 3) dispatch<3>(false, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  if (d == 2) dispatch<2>(false, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  if (d == 1) dispatch<1>(false, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  ++launches;
+  FGS_CUDA(cudaGetLastError());
+}
+
+void Core::launch_interp(const PassArgs& a) {
+  if (nitems == 0) return;
+  const size_t smem = smem_bytes(true);
+  if (smem > 227 * 1024) fail(FGS_ERESOURCE, "tile box exceeds shared memory (cutoff too large for d = 3)");
+  if (d == 3) dispatch<3>(true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  if (d == 2) dispatch<2>(true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  if (d == 1) dispatch<1>(true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  ++launches;
+  FGS_CUDA(cudaGetLastError());
+}
+
+void Core::launch_assemble(Workspace& w, int nvec) {
+  AssembleArgs aa{items.p, tile_ptr.p, tile_items.p, w.priv.p, box_stride, nitems, w.grid.p, grid_elems, nvec,
+                  d, M, B, nt};
+  int cells = 1;
+  for (int t = 0; t < d; ++t) cells *= B;
+  assemble_kernel<<<ntiles, std::min(256, round32(cells)), 0, stream>>>(aa);
+  ++launches;
+  FGS_CUDA(cudaGetLastError());
+}
+
+void Core::apply(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec, bool caller_order,
+                 bool scale_input) {
+  Workspace& w = workspace(nvec);
+  PassArgs a{};
+  a.items = items.p;
+  a.runs = runs.p;
+  a.taps = taps.p;
+  a.perm = caller_order ? perm.p + offset : nullptr;
+  a.point_base = offset;
+  a.x = x;
+  a.ldx = ldx;
+  a.s = inv_sqrt.p;
+  a.scale_input = scale_input ? 1 : 0;
+  a.nvec = nvec;
+  a.M = M;
+  a.priv = w.priv.p;
+  a.box_stride = box_stride;
+  a.grid = w.grid.p;
+  a.grid_stride = grid_elems;
+  a.y = y;
+  a.ldy = ldy;
+  a.epilogue = epilogue;
+  a.k0 = k0;
+  a.degrees = degrees.p;
+  a.inv_sqrt = inv_sqrt.p;
+  a.bad_flag = flag.p;
+  a.caller = perm.p + offset;
+
+  std::vector<cudaEvent_t> evs;
+  if (profile_) mark(evs);
+  launch_spread(a);
+  if (profile_) mark(evs);
+  launch_assemble(w, nvec);
+  if (profile_) mark(evs);
+  FGS_CUFFT(cufftExecD2Z(w.r2c, w.grid.p, w.spec.p));
+  if (profile_) mark(evs);
+  if (world == 1) {
+    MultiplyArgs ma{w.spec.p, mult.p, spec_elems, spec_elems, nvec, d, M, N};
+    multiply_kernel<<<ceil_div(spec_elems, 256), 256, 0, stream>>>(ma);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+  } else {
+    WindowArgs wa{w.spec.p, w.window.p, mult.p, spec_elems, window_elems, window_elems, nvec, d, M, N};
+    pack_window_kernel<<<ceil_div(window_elems, 256), 256, 0, stream>>>(wa);
+    ++launches;
+    nccl_check(nccl().all_reduce(w.window.p, w.window.p, static_cast<size_t>(window_elems) * nvec * 2, ncclDouble,
+                                 ncclSum, comm, stream),
+               "ncclAllReduce of the truncated spectrum");
+    FGS_CUDA(cudaMemsetAsync(w.spec.p, 0, sizeof(cufftDoubleComplex) * spec_elems * nvec, stream));
+    unpack_multiply_kernel<<<ceil_div(window_elems, 256), 256, 0, stream>>>(wa);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+  }
+  if (profile_) mark(evs);
+  FGS_CUFFT(cufftExecZ2D(w.c2r, w.spec.p, w.grid.p));
+  if (profile_) mark(evs);
+  launch_interp(a);
+  if (profile_) {
+    mark(evs);
+    ev_pending_.push_back(std::move(evs));
+  }
+}
+
+cudaEvent_t Core::stage_event() {
+  if (!ev_pool_.empty()) {
+    cudaEvent_t e = ev_pool_.back();
+    ev_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  FGS_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Core::mark(std::vector<cudaEvent_t>& evs) {
+  cudaEvent_t e = stage_event();
+  FGS_CUDA(cudaEventRecord(e, stream));
+  evs.push_back(e);
+}
+
+void Core::enable_profile(bool on) { profile_ = on; }
+
+void Core::read_profile(double* ms, int64_t* applies) {
+  for (int s = 0; s < ST_COUNT; ++s) ms[s] = 0.0;
+  FGS_CUDA(cudaStreamSynchronize(stream));
+  for (auto& evs : ev_pending_) {
+    for (int s = 0; s < ST_COUNT && s + 1 < static_cast<int>(evs.size()); ++s) {
+      float t = 0.f;
+      FGS_CUDA(cudaEventElapsedTime(&t, evs[static_cast<size_t>(s)], evs[static_cast<size_t>(s) + 1]));
+      ms[s] += t;
+    }
+    for (cudaEvent_t e : evs) ev_pool_.push_back(e);
+  }
+  if (applies) *applies = static_cast<int64_t>(ev_pending_.size());
+  ev_pending_.clear();
+}
+
+void Core::compute_degrees(int64_t* bad_node) {
+  degrees.alloc(static_cast<size_t>(std::max<int64_t>(n_local, 1)));
+  inv_sqrt.alloc(static_cast<size_t>(std::max<int64_t>(n_local, 1)));
+  flag.alloc(1);
+  DBuf<double> ones;
+  ones.alloc(static_cast<size_t>(std::max<int64_t>(n_local, 1)));
+  fill_kernel<<<ceil_div(std::max<int64_t>(n_local, 1), 256), 256, 0, stream>>>(ones.p, n_local, 1.0);
+  ++launches;
+  unsigned long long init = ULLONG_MAX;
+  FGS_CUDA(cudaMemcpyAsync(flag.p, &init, sizeof(init), cudaMemcpyHostToDevice, stream));
+  apply(EPI_DEGREE, ones.p, n_local, nullptr, 0, 1, false, false);
+  if (world > 1) {
+    nccl_check(nccl().all_reduce(flag.p, flag.p, 1, ncclUint64, ncclMin, comm, stream),
+               "ncclAllReduce of the degree flag");
+  }
+  unsigned long long bad = 0;
+  FGS_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(bad), cudaMemcpyDeviceToHost, stream));
+  FGS_CUDA(cudaStreamSynchronize(stream));
+  if (bad != ULLONG_MAX) {
+    const int64_t j = static_cast<int64_t>(bad);
+    if (bad_node) *bad_node = j;
+    double val = std::nan("");
+    // locate the value when this shard owns the node
+    std::vector<double> hdeg(static_cast<size_t>(n_local));
+    FGS_CUDA(cudaMemcpy(hdeg.data(), degrees.p, sizeof(double) * n_local, cudaMemcpyDeviceToHost));
+    for (int64_t p = 0; p < n_local; ++p)
+      if (host_perm[static_cast<size_t>(offset + p)] == j) val = hdeg[static_cast<size_t>(p)];
+    fail(FGS_ENUMERIC, "computed degree of node " + std::to_string(j) + " is not positive (" + std::to_string(val) +
+                           "); increase the fast-summation bandwidth/cutoff or widen the kernel");
+  }
+}
+
+void Core::nfft_adjoint(const double* x_planar, double* fhat_out) {
+  // x_planar: device [2][n] (re, im) in caller order; fhat_out: device interleaved N^d
+  Workspace& w = workspace(2);
+  PassArgs a{};
+  a.items = items.p;
+  a.runs = runs.p;
+  a.taps = taps.p;
+  a.perm = perm.p + offset;
+  a.x = x_planar;
+  a.ldx = n;
+  a.nvec = 2;
+  a.M = M;
+  a.priv = w.priv.p;
+  a.box_stride = box_stride;
+  launch_spread(a);
+  launch_assemble(w, 2);
+  w.cgrid.alloc(static_cast<size_t>(grid_elems));
+  merge_complex_kernel<<<ceil_div(grid_elems, 256), 256, 0, stream>>>(w.grid.p, w.grid.p + grid_elems, w.cgrid.p,
+                                                                      grid_elems);
+  ++launches;
+  if (!w.has_z2z) {
+    int dims[3] = {M, M, M};
+    FGS_CUFFT(cufftPlanMany(&w.z2z, d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2Z, 1));
+    FGS_CUFFT(cufftSetStream(w.z2z, stream));
+    w.has_z2z = true;
+  }
+  FGS_CUFFT(cufftExecZ2Z(w.z2z, w.cgrid.p, w.cgrid.p, CUFFT_FORWARD));
+  int64_t F = 1;
+  for (int t = 0; t < d; ++t) F *= N;
+  extract_kernel<<<ceil_div(F, 256), 256, 0, stream>>>(w.cgrid.p, reinterpret_cast<cufftDoubleComplex*>(fhat_out), F,
+                                                        d, N, M, deconv_d.p);
+  ++launches;
+  FGS_CUDA(cudaGetLastError());
+}
+
+void Core::nfft_forward(const double* fhat_in, double* y_planar) {
+  Workspace& w = workspace(2);
+  w.cgrid.alloc(static_cast<size_t>(grid_elems));
+  FGS_CUDA(cudaMemsetAsync(w.cgrid.p, 0, sizeof(cufftDoubleComplex) * grid_elems, stream));
+  int64_t F = 1;
+  for (int t = 0; t < d; ++t) F *= N;
+  place_kernel<<<ceil_div(F, 256), 256, 0, stream>>>(reinterpret_cast<const cufftDoubleComplex*>(fhat_in), w.cgrid.p,
+                                                      F, d, N, M, deconv_d.p);
+  ++launches;
+  if (!w.has_z2z) {
+    int dims[3] = {M, M, M};
+    FGS_CUFFT(cufftPlanMany(&w.z2z, d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2Z, 1));
+    FGS_CUFFT(cufftSetStream(w.z2z, stream));
+    w.has_z2z = true;
+  }
+  FGS_CUFFT(cufftExecZ2Z(w.z2z, w.cgrid.p, w.cgrid.p, CUFFT_INVERSE));
+  split_complex_kernel<<<ceil_div(grid_elems, 256), 256, 0, stream>>>(w.cgrid.p, w.grid.p, w.grid.p + grid_elems,
+                                                                      grid_elems);
+  ++launches;
+  PassArgs a{};
+  a.items = items.p;
+  a.runs = runs.p;
+  a.taps = taps.p;
+  a.perm = perm.p + offset;
+  a.x = nullptr;
+  a.nvec = 2;
+  a.M = M;
+  a.grid = w.grid.p;
+  a.grid_stride = grid_elems;
+  a.y = y_planar;
+  a.ldy = n;
+  a.epilogue = EPI_KERNEL;
+  launch_interp(a);
+}
+
+void Core::permute(const double* x, int64_t ldx, double* y, int64_t ldy, int nvec, int direction) {
+  permute_kernel<<<ceil_div(std::max<int64_t>(n_local, 1), 256), 256, 0, stream>>>(x, ldx, y, ldy, perm.p + offset,
+                                                                                  n_local, nvec, direction);
+  ++launches;
+  FGS_CUDA(cudaGetLastError());
+}
+
+double Core::error_estimate(int samples, uint64_t seed) const {
+  // kernel_error_estimate (fastsum.cpp:120-124) = |out_factor| *
+  // kernel_approx_error (kernels.cpp:369-396): sampled sup over the ball
+  if (samples < 1) fail(FGS_EPARAM, "sample count must be positive");
+  const double radius = 0.5 - params.eps_b;
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss;
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  double worst = 0.0;
+  std::vector<std::complex<double>> ph(static_cast<size_t>(d) * N);
+  for (int s = 0; s < samples; ++s) {
+    double y[3] = {0, 0, 0}, n2 = 0.0;
+    for (int t = 0; t < d; ++t) {
+      y[t] = gauss(rng);
+      n2 += y[t] * y[t];
+    }
+    const double len = std::sqrt(n2);
+    const double r = radius * std::pow(unif(rng), 1.0 / d);
+    for (int t = 0; t < d; ++t) y[t] = len > 0.0 ? y[t] * (r / len) : 0.0;
+    double yn = 0.0;
+    for (int t = 0; t < d; ++t) yn += y[t] * y[t];
+    for (int t = 0; t < d; ++t)
+      for (int a = 0; a < N; ++a)
+        ph[static_cast<size_t>(t) * N + a] = std::polar(1.0, 2.0 * kPi * (a - N / 2) * y[t]);
+    std::complex<double> acc = 0.0;
+    size_t flat = 0;
+    if (d == 1) {
+      for (int a = 0; a < N; ++a, ++flat) acc += bhat[flat] * ph[static_cast<size_t>(a)];
+    } else if (d == 2) {
+      for (int a = 0; a < N; ++a)
+        for (int c = 0; c < N; ++c, ++flat) acc += bhat[flat] * (ph[static_cast<size_t>(a)] * ph[static_cast<size_t>(N + c)]);
+    } else {
+      for (int a = 0; a < N; ++a)
+        for (int c = 0; c < N; ++c) {
+          const std::complex<double> pac = ph[static_cast<size_t>(a)] * ph[static_cast<size_t>(N + c)];
+          for (int e = 0; e < N; ++e, ++flat) acc += bhat[flat] * (pac * ph[static_cast<size_t>(2 * N + e)]);
+        }
+    }
+    worst = std::max(worst, std::abs(kernel_value(scaled, std::sqrt(yn)) - acc.real()));
+  }
+  return std::abs(out_factor) * worst;
+}
+
+}  // namespace fgsb

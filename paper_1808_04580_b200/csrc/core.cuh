@@ -1,0 +1,153 @@
+// core.cuh -- device-resident plan of the fast summation (the state behind
+// fgs::NfftPlan / FastsumPlan / AdjacencyOperator on one GPU or one shard).
+#pragma once
+
+#include <nccl.h>
+
+#include <complex>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "hostmath.hpp"
+
+namespace fgsb {
+
+struct Params {
+  int N = 32, m = 4, p = 4;
+  double eps_b = 0.0, oversampling = 2.0;
+};
+
+// RAII device buffer
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    reset();
+    if (count == 0) return;
+    FGS_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) FGS_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+struct Workspace {
+  int nvec = 0;
+  DBuf<double> priv, grid;
+  DBuf<cufftDoubleComplex> spec, cgrid, window;
+  cufftHandle r2c = 0, c2r = 0, z2z = 0;
+  bool has_plans = false, has_z2z = false;
+};
+
+class Core {
+ public:
+  enum Kind { NFFT = 0, FASTSUM = 1 };
+
+  Core(const double* nodes_colmajor, int64_t n, int d, Kind kind, const KernelSpec& kernel,
+       const Params& params, int device, int rank = 0, int world = 1, const void* nccl_id = nullptr);
+  ~Core();
+  Core(const Core&) = delete;
+  Core& operator=(const Core&) = delete;
+
+  // geometry / plan scalars
+  Kind kind;
+  int d = 0, N = 0, m = 0, T = 0, M = 0, B = 0, nt = 0, ntiles = 0;
+  int64_t n = 0, n_local = 0, offset = 0;
+  int rank = 0, world = 1;
+  double b_kb = 0.0;
+  KernelSpec kernel, scaled;
+  Params params;
+  double rho = 1.0, out_factor = 1.0, k0 = 0.0;
+  RegKernel reg;
+  std::vector<std::complex<double>> bhat;  // N^d, FrequencyIndexSet order
+  std::vector<double> deconv;              // N
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  ncclComm_t comm = nullptr;
+  int64_t launches = 0;
+
+  // device plan
+  DBuf<int> perm;  // internal -> caller, all n points (identical on every rank)
+  DBuf<double> taps;  // [n_local][d][T]
+  DBuf<DItem> items;
+  DBuf<DRun> runs;
+  DBuf<int> tile_ptr, tile_items;
+  DBuf<cufftDoubleComplex> mult;  // compact Hermitian multiplier (FASTSUM)
+  DBuf<double> deconv_d;
+  int nitems = 0;
+  int64_t box_stride = 0;
+  int64_t grid_elems = 0, spec_elems = 0, window_elems = 0;
+  std::vector<int> host_perm;
+
+  // graph-operator state (AdjacencyOperator)
+  DBuf<double> degrees, inv_sqrt;  // internal order, local slice
+  DBuf<unsigned long long> flag;
+
+  // staging buffers for host-vector calls
+  DBuf<double> xbuf, ybuf;
+
+  void set_stream(cudaStream_t s);
+  Workspace& workspace(int nvec);
+
+  // y = op(x) for the fast-summation pipeline.  x, y device pointers; when
+  // `caller_order` the vectors are full-length in caller order (perm
+  // indexing), else local-slice internal order.
+  void apply(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
+             bool caller_order, bool scale_input);
+  void compute_degrees(int64_t* bad_node);
+
+  // complex NFFT transforms (NfftPlan), interleaved complex on device
+  void nfft_adjoint(const double* x_re_im_planar, double* fhat_interleaved);
+  void nfft_forward(const double* fhat_interleaved, double* y_planar);
+
+  // permutation helpers (caller <-> internal), full length
+  void permute(const double* x, int64_t ldx, double* y, int64_t ldy, int nvec, int direction);
+
+  double error_estimate(int samples, uint64_t seed) const;
+
+  // stage profiling: when enabled, apply() records CUDA events on the
+  // handle's stream at every stage boundary; read_profile() syncs and
+  // returns the summed milliseconds per stage since the last read.
+  enum Stage { ST_SPREAD = 0, ST_ASSEMBLE, ST_R2C, ST_MULTIPLY, ST_C2R, ST_INTERP, ST_COUNT };
+  void enable_profile(bool on);
+  void read_profile(double* ms, int64_t* applies);
+
+ private:
+  std::map<int, std::unique_ptr<Workspace>> ws_;
+  bool profile_ = false;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<std::vector<cudaEvent_t>> ev_pending_;
+  cudaEvent_t stage_event();
+  void mark(std::vector<cudaEvent_t>& evs);
+  void build_plan(const double* nodes_colmajor);
+  void build_coefficients();
+  void launch_spread(const PassArgs& a);
+  void launch_interp(const PassArgs& a);
+  void launch_assemble(Workspace& w, int nvec);
+  size_t smem_bytes(bool interp) const;
+  int threads() const;
+};
+
+// FastsumParams validation (fastsum.cpp:25-36)
+void validate_params(const Params& p);
+
+// fp64 FMA peak of a device in TFLOP/s (peak.cu)
+double measure_fp64_peak(int device);
+
+}  // namespace fgsb

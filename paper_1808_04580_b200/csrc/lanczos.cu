@@ -1,0 +1,408 @@
+// lanczos.cu -- device-resident Lanczos with full two-pass classical
+// Gram-Schmidt reorthogonalisation over the fast graph operator
+// (reference: spectral.cpp:141-256, lanczos_largest).
+//
+// The Krylov basis lives in HBM in the operator's internal point order (rows
+// = this shard's slice), column-major with leading dimension n_local, and
+// grows geometrically like the reference's conservativeResize
+// (spectral.cpp:159,222-224).  Every reduction is a fixed-order two-stage
+// tree (block partials -> ordered final sum), so a run is bitwise
+// reproducible.  Sharded runs add one NCCL allreduce per reduction.
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <numeric>
+#include <random>
+
+#include "core.cuh"
+#include "lanczos.cuh"
+#include "nccl_shim.hpp"
+
+namespace fgsb {
+
+namespace {
+
+constexpr int kRedThreads = 256;
+constexpr int kRowsPerThread = 8;
+constexpr int kRowsPerBlock = kRedThreads * kRowsPerThread;
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// partial[b][j] = sum over block b's rows of Q[r, j] * z[r], j < m
+// (32 columns at a time per warp, transposed through a warp butterfly).
+__global__ void __launch_bounds__(kRedThreads) multidot_kernel(const double* __restrict__ Q, int64_t ldq, int m,
+                                                               const double* __restrict__ z, int64_t n,
+                                                               double* __restrict__ partial) {
+  __shared__ double red[kRedThreads / 32][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
+  double zr[kRowsPerThread];
+#pragma unroll
+  for (int i = 0; i < kRowsPerThread; ++i) {
+    const int64_t r = row0 + threadIdx.x + static_cast<int64_t>(i) * kRedThreads;
+    zr[i] = r < n ? z[r] : 0.0;
+  }
+  for (int j0 = 0; j0 < m; j0 += 32) {
+    double p[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      double acc = 0.0;
+      if (j0 + c < m) {
+        const double* col = Q + static_cast<int64_t>(j0 + c) * ldq;
+#pragma unroll
+        for (int i = 0; i < kRowsPerThread; ++i) {
+          const int64_t r = row0 + threadIdx.x + static_cast<int64_t>(i) * kRedThreads;
+          if (r < n) acc = fma(col[r], zr[i], acc);
+        }
+      }
+      p[c] = acc;
+    }
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+      const bool upper = (lane & sft) != 0;
+#pragma unroll
+      for (int k = 0; k < sft; ++k) {
+        const double send = upper ? p[k] : p[k + sft];
+        const double keep = upper ? p[k + sft] : p[k];
+        p[k] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+      }
+    }
+    red[warp][lane] = p[0];
+    __syncthreads();
+    if (warp == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kRedThreads / 32; ++w) s += red[w][lane];
+      if (j0 + lane < m) partial[static_cast<int64_t>(blockIdx.x) * m + j0 + lane] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// out[j] = scale_sign * sum_b partial[b][j]  (ordered); optional sqrt
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, int nblocks, int m,
+                                       double* __restrict__ out, int take_sqrt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double s = 0.0;
+  for (int b = 0; b < nblocks; ++b) s += partial[static_cast<int64_t>(b) * m + j];
+  out[j] = take_sqrt ? sqrt(s) : s;
+}
+
+
+// z[r] -= sum_j Q[r, j] * h[j]   (the GEMV of one CGS pass, spectral.cpp:195)
+__global__ void update_kernel(const double* __restrict__ Q, int64_t ldq, int m, const double* __restrict__ h,
+                              double* __restrict__ z, int64_t n) {
+  extern __shared__ double hs[];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) hs[j] = h[j];
+  __syncthreads();
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  double acc = 0.0;
+  int j = 0;
+  for (; j + 4 <= m; j += 4) {
+    const double q0 = Q[static_cast<int64_t>(j) * ldq + r];
+    const double q1 = Q[static_cast<int64_t>(j + 1) * ldq + r];
+    const double q2 = Q[static_cast<int64_t>(j + 2) * ldq + r];
+    const double q3 = Q[static_cast<int64_t>(j + 3) * ldq + r];
+    acc = fma(q0, hs[j], acc);
+    acc = fma(q1, hs[j + 1], acc);
+    acc = fma(q2, hs[j + 2], acc);
+    acc = fma(q3, hs[j + 3], acc);
+  }
+  for (; j < m; ++j) acc = fma(Q[static_cast<int64_t>(j) * ldq + r], hs[j], acc);
+  z[r] -= acc;
+}
+
+// z -= alpha q_{m-1} + beta q_{m-2}  (spectral.cpp:186-191)
+__global__ void three_term_kernel(double* __restrict__ z, const double* __restrict__ qcur,
+                                  const double* __restrict__ qprev, const double* __restrict__ alpha, double beta,
+                                  int64_t n) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  double v = z[r] - alpha[0] * qcur[r];
+  if (qprev) v -= beta * qprev[r];
+  z[r] = v;
+}
+
+__global__ void scale_kernel(const double* __restrict__ z, double inv, double* __restrict__ out, int64_t n) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r < n) out[r] = z[r] * inv;
+}
+
+// V[:, i] = Q_m S[:, i]   (Ritz vectors, spectral.cpp:250); S row-major m x k
+template <int KC>
+__global__ void ritz_kernel(const double* __restrict__ Q, int64_t ldq, int m, const double* __restrict__ S, int k,
+                            int c0, double* __restrict__ V, int64_t ldv, int64_t n) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  double acc[KC];
+#pragma unroll
+  for (int i = 0; i < KC; ++i) acc[i] = 0.0;
+  for (int j = 0; j < m; ++j) {
+    const double q = Q[static_cast<int64_t>(j) * ldq + r];
+#pragma unroll
+    for (int i = 0; i < KC; ++i)
+      if (c0 + i < k) acc[i] = fma(q, __ldg(S + static_cast<int64_t>(j) * k + c0 + i), acc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < KC; ++i)
+    if (c0 + i < k) V[static_cast<int64_t>(c0 + i) * ldv + r] = acc[i];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Symmetric tridiagonal eigensolver (the role of Eigen's
+// SelfAdjointEigenSolver::computeFromTridiagonal, spectral.cpp:174-179):
+// implicit QL with Wilkinson shifts; eigenvalues ascending, eigenvectors
+// as columns of z (column-major m x m).
+// ---------------------------------------------------------------------------
+void tridiagonal_eigen(int m, std::vector<double>& dg, const std::vector<double>& offd, std::vector<double>& z) {
+  const double eps = std::numeric_limits<double>::epsilon();
+  z.assign(static_cast<size_t>(m) * m, 0.0);
+  for (int i = 0; i < m; ++i) z[static_cast<size_t>(i) * m + i] = 1.0;
+  std::vector<double> e(static_cast<size_t>(m), 0.0);
+  for (int i = 0; i + 1 < m; ++i) e[static_cast<size_t>(i)] = offd[static_cast<size_t>(i)];
+  for (int l = 0; l < m; ++l) {
+    for (int iter = 0;; ++iter) {
+      int mm = l;
+      while (mm < m - 1 && std::abs(e[mm]) > eps * (std::abs(dg[mm]) + std::abs(dg[mm + 1]))) ++mm;
+      if (mm == l) break;
+      if (iter > 64) fail(FGS_ENUMERIC, "tridiagonal eigensolver did not converge");
+      double g = (dg[l + 1] - dg[l]) / (2.0 * e[l]);
+      double r = std::hypot(g, 1.0);
+      g = dg[mm] - dg[l] + e[l] / (g + std::copysign(r, g));
+      double s = 1.0, c = 1.0, p = 0.0;
+      bool deflated = false;
+      for (int i = mm - 1; i >= l; --i) {
+        double f = s * e[i], bb = c * e[i];
+        r = std::hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {
+          dg[i + 1] -= p;
+          e[mm] = 0.0;
+          deflated = true;
+          break;
+        }
+        s = f / r;
+        c = g / r;
+        g = dg[i + 1] - p;
+        r = (dg[i] - g) * s + 2.0 * c * bb;
+        p = s * r;
+        dg[i + 1] = g + p;
+        g = c * r - bb;
+        double* zi = &z[static_cast<size_t>(i) * m];
+        double* zi1 = &z[static_cast<size_t>(i + 1) * m];
+        for (int k = 0; k < m; ++k) {
+          const double t = zi1[k];
+          zi1[k] = s * zi[k] + c * t;
+          zi[k] = c * zi[k] - s * t;
+        }
+      }
+      if (deflated) continue;
+      dg[l] -= p;
+      e[l] = g;
+      e[mm] = 0.0;
+    }
+  }
+  std::vector<int> order(static_cast<size_t>(m));
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return dg[a] < dg[b]; });
+  std::vector<double> d2(static_cast<size_t>(m)), z2(z.size());
+  for (int i = 0; i < m; ++i) {
+    d2[static_cast<size_t>(i)] = dg[static_cast<size_t>(order[i])];
+    std::copy(&z[static_cast<size_t>(order[i]) * m], &z[static_cast<size_t>(order[i]) * m] + m,
+              &z2[static_cast<size_t>(i) * m]);
+  }
+  dg.swap(d2);
+  z.swap(z2);
+}
+
+// ---------------------------------------------------------------------------
+LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol, uint64_t seed, bool want_vectors) {
+  const int64_t n = c.n, nl = c.n_local;
+  if (k < 1) fail(FGS_EPARAM, "at least one eigenpair must be requested");
+  if (k > n) fail(FGS_EPARAM, "requested pairs must not exceed the operator dimension");
+  if (max_iter < 1) fail(FGS_EPARAM, "max_iter must be positive");
+  if (!(tol > 0.0)) fail(FGS_EPARAM, "tolerance must be positive");
+  const double kEps = std::numeric_limits<double>::epsilon();
+  cudaStream_t st = c.stream;
+  const int epi = which == 0 ? EPI_NORMALIZED : EPI_LAPLACIAN;
+
+  // start vector: mt19937_64(seed) uniform(-1, 1) over the caller order,
+  // normalised (spectral.cpp:152-156); moved to the internal order
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unif(-1.0, 1.0);
+  std::vector<double> start(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) start[static_cast<size_t>(i)] = unif(rng);
+  double sn = 0.0;
+  for (double v : start) sn += v * v;
+  sn = std::sqrt(sn);
+  std::vector<double> local(static_cast<size_t>(std::max<int64_t>(nl, 1)));
+  for (int64_t p = 0; p < nl; ++p) local[static_cast<size_t>(p)] = start[static_cast<size_t>(c.host_perm[static_cast<size_t>(c.offset + p)])] / sn;
+
+  int64_t cap = std::min<int64_t>(n, 64);
+  DBuf<double> basis, z, partial, hbuf, scal;
+  basis.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)) * cap);
+  z.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)));
+  const int nblk = std::max(1, ceil_div(nl, kRowsPerBlock));
+  hbuf.alloc(static_cast<size_t>(std::min<int64_t>(n, max_iter) + 2));
+  partial.alloc(static_cast<size_t>(nblk) * (std::min<int64_t>(n, max_iter) + 2));
+  scal.alloc(4);
+  FGS_CUDA(cudaMemcpyAsync(basis.p, local.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, st));
+
+  auto allreduce = [&](double* v, int count) {
+    if (c.world > 1)
+      nccl_check(nccl().all_reduce(v, v, static_cast<size_t>(count), ncclDouble, ncclSum, c.comm, st),
+                 "ncclAllReduce in Lanczos");
+  };
+  // out[0..m) = Q[:, 0..m)^T v  (global, fixed order)
+  auto multidot = [&](const double* Q, int m, const double* v, double* out) {
+    multidot_kernel<<<nblk, kRedThreads, 0, st>>>(Q, nl, m, v, nl, partial.p);
+    reduce_partials_kernel<<<ceil_div(m, 128), 128, 0, st>>>(partial.p, nblk, m, out, 0);
+    c.launches += 2;
+    allreduce(out, m);
+  };
+  auto update = [&](const double* Q, int m, const double* h, double* v) {
+    update_kernel<<<ceil_div(std::max<int64_t>(nl, 1), 256), 256, sizeof(double) * m, st>>>(Q, nl, m, h, v, nl);
+    ++c.launches;
+  };
+  auto cgs_pass = [&](int m, double* v) {  // v -= Q(Q^T v)
+    multidot(basis.p, m, v, hbuf.p);
+    update(basis.p, m, hbuf.p, v);
+  };
+  auto norm_of = [&](const double* v) -> double {
+    multidot(v, 1, v, scal.p + 1);
+    double h = 0.0;
+    FGS_CUDA(cudaMemcpyAsync(&h, scal.p + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+    FGS_CUDA(cudaStreamSynchronize(st));
+    return std::sqrt(h);
+  };
+
+  std::vector<double> alphas, betas, tvals, tvecs;
+  int tri_size = 0, iterations = 0, next_check = k;
+  double scale = 0.0;
+  bool converged = false;
+  auto solve_tri = [&](int m) {
+    tvals.assign(alphas.begin(), alphas.begin() + m);
+    std::vector<double> sub(betas.begin(), betas.begin() + (m - 1));
+    tridiagonal_eigen(m, tvals, sub, tvecs);
+    tri_size = m;
+  };
+
+  while (true) {
+    const int m = static_cast<int>(alphas.size()) + 1;
+    const double* qcur = basis.p + static_cast<int64_t>(m - 1) * nl;
+    c.apply(epi, qcur, nl, z.p, nl, 1, false, true);
+    ++iterations;
+    // alpha = q . z
+    multidot(qcur, 1, z.p, scal.p);
+    const double beta_prev = m >= 2 ? betas[static_cast<size_t>(m - 2)] : 0.0;
+    three_term_kernel<<<ceil_div(std::max<int64_t>(nl, 1), 256), 256, 0, st>>>(
+        z.p, qcur, m >= 2 ? basis.p + static_cast<int64_t>(m - 2) * nl : nullptr, scal.p, beta_prev, nl);
+    ++c.launches;
+    cgs_pass(m, z.p);
+    cgs_pass(m, z.p);
+    multidot(z.p, 1, z.p, scal.p + 1);
+    double ab[2];
+    FGS_CUDA(cudaMemcpyAsync(ab, scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    FGS_CUDA(cudaStreamSynchronize(st));
+    const double alpha = ab[0], beta = std::sqrt(ab[1]);
+    alphas.push_back(alpha);
+    scale = std::max(scale, std::abs(alpha) + beta + beta_prev);
+
+    const bool last = iterations >= max_iter || m == static_cast<int>(n);
+    if (m >= k && (m >= next_check || last)) {  // spectral.cpp:200-215
+      solve_tri(m);
+      bool all_small = true;
+      for (int i = 0; i < k && all_small; ++i) {
+        const double theta = tvals[static_cast<size_t>(m - 1 - i)];
+        const double est = beta * std::abs(tvecs[static_cast<size_t>(m - 1 - i) * m + (m - 1)]);
+        if (est > tol * std::max(std::abs(theta), kEps * std::max(scale, 1.0))) all_small = false;
+      }
+      if (all_small) {
+        converged = true;
+        break;
+      }
+      next_check = m + std::max(8, m / 8);
+    }
+    if (iterations >= max_iter) break;
+    if (m == static_cast<int>(n)) {
+      converged = true;
+      break;
+    }
+    if (m == cap) {  // geometric growth (conservativeResize)
+      const int64_t ncap = std::min<int64_t>(n, cap * 2);
+      DBuf<double> nb;
+      nb.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)) * ncap);
+      FGS_CUDA(cudaMemcpyAsync(nb.p, basis.p, sizeof(double) * nl * cap, cudaMemcpyDeviceToDevice, st));
+      FGS_CUDA(cudaStreamSynchronize(st));
+      std::swap(basis.p, nb.p);
+      std::swap(basis.n, nb.n);
+      cap = ncap;
+    }
+    double* qnext = basis.p + static_cast<int64_t>(m) * nl;
+    if (beta > 1e-14 * std::max(scale, 1.0)) {
+      betas.push_back(beta);
+      scale_kernel<<<ceil_div(std::max<int64_t>(nl, 1), 256), 256, 0, st>>>(z.p, 1.0 / beta, qnext, nl);
+      ++c.launches;
+      // reference divides z / beta; multiplying by the reciprocal differs by
+      // one rounding (<= 1 ulp per entry)
+    } else {
+      // breakdown: fresh random direction orthogonal to the basis
+      // (spectral.cpp:59-75, 225-238), same RNG stream as the start vector
+      bool found = false;
+      for (int attempt = 0; attempt < 8 && !found; ++attempt) {
+        std::vector<double> v(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) v[static_cast<size_t>(i)] = unif(rng);
+        for (int64_t p = 0; p < nl; ++p) local[static_cast<size_t>(p)] = v[static_cast<size_t>(c.host_perm[static_cast<size_t>(c.offset + p)])];
+        FGS_CUDA(cudaMemcpyAsync(z.p, local.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, st));
+        cgs_pass(m, z.p);
+        cgs_pass(m, z.p);
+        const double nv = norm_of(z.p);
+        if (nv > 1e-8) {
+          scale_kernel<<<ceil_div(std::max<int64_t>(nl, 1), 256), 256, 0, st>>>(z.p, 1.0 / nv, qnext, nl);
+          ++c.launches;
+          found = true;
+        }
+      }
+      if (!found) {
+        converged = true;
+        break;
+      }
+      betas.push_back(0.0);
+    }
+  }
+
+  const int m = static_cast<int>(alphas.size());
+  if (tri_size != m) solve_tri(m);
+  const int wanted = std::min(k, m);
+  LanczosResult res;
+  res.iterations = iterations;
+  res.converged = converged;
+  res.values.resize(static_cast<size_t>(wanted));
+  std::vector<double> S(static_cast<size_t>(m) * wanted);  // row-major m x wanted
+  for (int i = 0; i < wanted; ++i) {
+    res.values[static_cast<size_t>(i)] = tvals[static_cast<size_t>(m - 1 - i)];
+    for (int j = 0; j < m; ++j)
+      S[static_cast<size_t>(j) * wanted + i] = tvecs[static_cast<size_t>(m - 1 - i) * m + j];
+  }
+  if (want_vectors) {
+    DBuf<double> dS, V;
+    dS.upload(S.data(), S.size(), st);
+    V.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)) * wanted);
+    for (int c0 = 0; c0 < wanted; c0 += 8) {
+      ritz_kernel<8><<<ceil_div(std::max<int64_t>(nl, 1), 128), 128, 0, st>>>(basis.p, nl, m, dS.p, wanted, c0, V.p,
+                                                                             nl, nl);
+      ++c.launches;
+    }
+    res.local_vectors.resize(static_cast<size_t>(nl) * wanted);
+    FGS_CUDA(cudaMemcpyAsync(res.local_vectors.data(), V.p, sizeof(double) * nl * wanted, cudaMemcpyDeviceToHost, st));
+  }
+  FGS_CUDA(cudaStreamSynchronize(st));
+  FGS_CUDA(cudaGetLastError());
+  return res;
+}
+
+}  // namespace fgsb
