@@ -332,7 +332,7 @@ def run_b200(args, rank, world, local_rank):
         torch.cuda.synchronize()
         solve = time.perf_counter() - t0
         lanczos = {"k": info["k"], "tol": 1e-8, "setup_s": setup_s, "solve_s": solve, "total_s": setup_s + solve,
-                   "iterations": li.iterations, "converged": li.converged,
+                   "iterations": li.iterations, "converged": li.converged, "phases": op.lanczos_stats(),
                    "smallest_laplacian_eigs": [1.0 - v for v in pairs.values[:4].tolist()]}
 
     # ---- CPU baseline (rank 0, N=1) ----------------------------------------

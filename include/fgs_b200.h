@@ -153,6 +153,8 @@ fgs_status fgs_adjacency_geometry(fgs_adjacency_t h, int* d, int* N, int* M, int
 /* fp64 FMA-pipe peak of `device` in TFLOP/s (independent DFMA chains, CUDA
  * events), the denominator of the spread/interp roofline. */
 fgs_status fgs_measure_fp64_peak(int device, double* tflops);
+/* fp64 tensor-core (DMMA m8n8k4) peak in TFLOP/s, same method. */
+fgs_status fgs_measure_dmma_peak(int device, double* tflops);
 /* Kernel launches issued by this handle since creation (instrumentation). */
 fgs_status fgs_adjacency_launch_count(fgs_adjacency_t h, int64_t* out);
 void fgs_adjacency_destroy(fgs_adjacency_t h);
@@ -167,6 +169,11 @@ void fgs_adjacency_destroy(fgs_adjacency_t h);
 fgs_status fgs_lanczos_largest(fgs_adjacency_t h, int which, int k, int max_iter, double tol,
                                uint64_t seed, double* values, double* vectors, int* count,
                                int* iterations, int* converged);
+
+/* Device milliseconds of the last fgs_lanczos_largest on this handle spent in
+ * operator applies and in reorthogonalisation, the host wall time of its
+ * iteration loop, and its iteration count (instrumentation). */
+fgs_status fgs_lanczos_stats(fgs_adjacency_t h, double* out4);
 
 /* ---- synthetic workloads of BASELINE.json (seeded mt19937_64) ----------- */
 /* config 1..5: writes n x d column-major nodes; returns n, d, sigma, N, m, p, k */

@@ -401,6 +401,11 @@ class AdjacencyOperator:
                                             C.byref(items), C.byref(bs)))
         return dict(d=d.value, N=N.value, M=M.value, taps=T.value, items=items.value, box_stride=bs.value)
 
+    def lanczos_stats(self) -> dict:
+        out = np.zeros(4)
+        _check(lib().fgs_lanczos_stats(self._h, _dp(out)))
+        return dict(apply_ms=out[0], reorth_ms=out[1], loop_ms=out[2], iterations=int(out[3]))
+
     def launch_count(self) -> int:
         out = C.c_int64()
         _check(lib().fgs_adjacency_launch_count(self._h, C.byref(out)))

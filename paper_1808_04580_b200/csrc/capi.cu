@@ -448,6 +448,21 @@ fgs_status fgs_measure_fp64_peak(int device, double* tflops) {
   });
 }
 
+fgs_status fgs_measure_dmma_peak(int device, double* tflops) {
+  return guard([&] {
+    need(tflops, "tflops");
+    *tflops = fgsb::measure_dmma_peak(device);
+  });
+}
+
+fgs_status fgs_lanczos_stats(fgs_adjacency_t h, double* out4) {
+  return guard([&] {
+    need(h, "handle");
+    need(out4, "out4");
+    for (int i = 0; i < 4; ++i) out4[i] = h->core->lanczos_stats[i];
+  });
+}
+
 void fgs_adjacency_destroy(fgs_adjacency_t h) { delete h; }
 
 // ---- lanczos_largest -------------------------------------------------------
@@ -461,6 +476,10 @@ fgs_status fgs_lanczos_largest(fgs_adjacency_t h, int which, int k, int max_iter
     if (vectors && c.world > 1) fail(FGS_EPARAM, "Ritz vectors in caller order need an unsharded handle");
     FGS_CUDA(cudaSetDevice(c.device));
     fgsb::LanczosResult r = fgsb::lanczos_device(c, which, k, max_iter, tol, seed, vectors != nullptr);
+    c.lanczos_stats[0] = r.apply_ms;
+    c.lanczos_stats[1] = r.reorth_ms;
+    c.lanczos_stats[2] = r.loop_ms;
+    c.lanczos_stats[3] = r.iterations;
     const int cnt = static_cast<int>(r.values.size());
     // make_eigenpairs (spectral.cpp:105-127): stable descending sort, then
     // flip each column so its first largest-magnitude entry is positive

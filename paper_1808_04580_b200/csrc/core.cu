@@ -5,11 +5,15 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
 #include "core.cuh"
 #include "kernels.cuh"
+#include "kernels_v2.cuh"
+#include "kernels_v3.cuh"
+#include "kernels_v4.cuh"
 #include "nccl_shim.hpp"
 
 namespace fgsb {
@@ -152,16 +156,31 @@ __global__ void permute_kernel(const double* x, int64_t ldx, double* y, int64_t 
   }
 }
 
-// ---- launch policy of the templated cell-contraction kernels --------------
-struct Policy {
-  int nt;  // threads per CTA
-  bool templated;
-};
-
-Policy policy(int D, int T) {
-  if (T > 16) return {256, false};
-  if (D == 3) return {std::min(256, round32(T * T)), true};
-  return {32, true};
+// ---- launch policy ----------------------------------------------------------
+// 2m <= 16: register-blocked cp.async kernels (kernels_v2.cuh); FGS_KERNEL=v1
+// selects the first-generation single-row kernels (kept for A/B timing);
+// 2m > 16: runtime-2m single-value kernels (kernels.cuh).
+bool kernel_env(const char* v) {
+  const char* e = std::getenv("FGS_KERNEL");
+  return e && std::string(e) == v;
+}
+bool use_v1() {
+  static const bool v1 = kernel_env("v1");
+  return v1;
+}
+// warp-resident-footprint interpolation (kernels_v3.cuh) for d = 3, 2m in {8,12,16}
+template <int D, int T>
+constexpr bool has_v3() {
+  return D == 3 && (T == 8 || T == 12 || T == 16);
+}
+bool use_v3() {
+  static const bool v3 = kernel_env("v3");
+  return v3;
+}
+// fp64 tensor-core kernels (kernels_v4.cuh): the default for d = 3, 2m in {8,12,16}
+bool use_v4() {
+  static const bool v4 = !kernel_env("v1") && !kernel_env("v2") && !kernel_env("v3");
+  return v4;
 }
 
 template <int D, int T>
@@ -173,46 +192,114 @@ constexpr int nt_of() {
   return D == 3 ? ((T * T + 31) / 32 * 32 > 256 ? 256 : (T * T + 31) / 32 * 32) : 32;
 }
 
+// shared-memory doubles beyond the box, and threads, of the kernel that
+// dispatch() will launch for (D, T)
+struct LaunchShape {
+  int nt;
+  size_t extra_spread, extra_interp;
+};
+
 template <int D, int T>
-void launch_spread_t(const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
-  constexpr int E = e_of<D, T>();
-  constexpr int NT = nt_of<D, T>();
-  auto k = spread_kernel<D, T, E, NT>;
-  FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  k<<<nitems, NT, smem, s>>>(a, T, box_stride);
+LaunchShape shape_t() {
+  if (use_v1()) {
+    const size_t base = static_cast<size_t>(kQ) * D * T + kQ;
+    return {nt_of<D, T>(), base, base + nt_of<D, T>()};
+  }
+  using B = Blk<D, T>;
+  const size_t base = 2 * static_cast<size_t>(B::QS) * B::TAPS + 2 * B::QS;
+  size_t interp = base + 2 * static_cast<size_t>(B::NT / 32) * B::QB;
+  size_t spread = base;
+  if constexpr (has_v3<D, T>()) {
+    using B3 = Blk3<T>;
+    if (use_v3()) interp = 2 * static_cast<size_t>(B3::QS) * B3::TAPS + static_cast<size_t>(B3::P) * B3::G * B3::QB;
+    using B4 = Blk4<T>;
+    if (use_v4()) {
+      interp = 2 * static_cast<size_t>(B4::QS) * B4::TAPS + static_cast<size_t>(B4::P) * B4::G * 8;
+      spread = 2 * static_cast<size_t>(B4::QS) * B4::TAPS + 2 * B4::QS;
+    }
+  }
+  return {B::NT, spread, interp};
+}
+
+template <int D>
+LaunchShape shape_of(int T) {
+  switch (T) {
+    case 2: return shape_t<D, 2>();
+    case 4: return shape_t<D, 4>();
+    case 6: return shape_t<D, 6>();
+    case 8: return shape_t<D, 8>();
+    case 10: return shape_t<D, 10>();
+    case 12: return shape_t<D, 12>();
+    case 14: return shape_t<D, 14>();
+    case 16: return shape_t<D, 16>();
+    default: break;
+  }
+  const size_t base = static_cast<size_t>(kQ) * D * T + kQ;
+  return {256, base, base + 256};
 }
 
 template <int D, int T>
-void launch_interp_t(const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
-  constexpr int E = e_of<D, T>();
-  constexpr int NT = nt_of<D, T>();
-  auto k = interp_kernel<D, T, E, NT>;
-  FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  k<<<nitems, NT, smem, s>>>(a, T, box_stride);
+void launch_t(bool interp, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
+  if (use_v1()) {
+    constexpr int E = e_of<D, T>();
+    constexpr int NT = nt_of<D, T>();
+    if (interp) {
+      auto k = interp_kernel<D, T, E, NT>;
+      FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k<<<nitems, NT, smem, s>>>(a, T, box_stride);
+    } else {
+      auto k = spread_kernel<D, T, E, NT>;
+      FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k<<<nitems, NT, smem, s>>>(a, T, box_stride);
+    }
+    return;
+  }
+  constexpr int NT = Blk<D, T>::NT;
+  if constexpr (has_v3<D, T>()) {
+    if (use_v4()) {
+      if (interp) {
+        auto k = interp_v4_kernel<T>;
+        FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        k<<<nitems, Blk4<T>::NT, smem, s>>>(a, box_stride);
+      } else {
+        auto k = spread_v4_kernel<T>;
+        FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        k<<<nitems, Blk4<T>::NT, smem, s>>>(a, box_stride);
+      }
+      return;
+    }
+    if (interp && use_v3()) {
+      auto k = interp_v3_kernel<T>;
+      FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k<<<nitems, Blk3<T>::NT, smem, s>>>(a, box_stride);
+      return;
+    }
+  }
+  if (interp) {
+    auto k = interp_v2_kernel<D, T>;
+    FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k<<<nitems, NT, smem, s>>>(a, box_stride);
+  } else {
+    auto k = spread_v2_kernel<D, T>;
+    FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k<<<nitems, NT, smem, s>>>(a, box_stride);
+  }
 }
 
 template <int D>
 void dispatch(bool interp, int T, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
-#define FGS_CASE(TT)                                              \
-  case TT:                                                        \
-    if (interp)                                                   \
-      launch_interp_t<D, TT>(a, nitems, smem, box_stride, s);     \
-    else                                                          \
-      launch_spread_t<D, TT>(a, nitems, smem, box_stride, s);     \
-    return;
   switch (T) {
-    FGS_CASE(2)
-    FGS_CASE(4)
-    FGS_CASE(6)
-    FGS_CASE(8)
-    FGS_CASE(10)
-    FGS_CASE(12)
-    FGS_CASE(14)
-    FGS_CASE(16)
+    case 2: return launch_t<D, 2>(interp, a, nitems, smem, box_stride, s);
+    case 4: return launch_t<D, 4>(interp, a, nitems, smem, box_stride, s);
+    case 6: return launch_t<D, 6>(interp, a, nitems, smem, box_stride, s);
+    case 8: return launch_t<D, 8>(interp, a, nitems, smem, box_stride, s);
+    case 10: return launch_t<D, 10>(interp, a, nitems, smem, box_stride, s);
+    case 12: return launch_t<D, 12>(interp, a, nitems, smem, box_stride, s);
+    case 14: return launch_t<D, 14>(interp, a, nitems, smem, box_stride, s);
+    case 16: return launch_t<D, 16>(interp, a, nitems, smem, box_stride, s);
     default: break;
   }
-#undef FGS_CASE
-  // runtime-T fallback (m > 8): E = 1, 256 threads
+  // runtime-2m fallback (m > 8): one value per unit, 256 threads
   if (interp) {
     auto k = interp_kernel<D, 0, 1, 256>;
     FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -497,7 +584,6 @@ void Core::build_plan(const double* nodes_colmajor) {
   nitems = static_cast<int>(hitems.size());
   std::vector<DItem> ditems;
   std::vector<DRun> druns;
-  std::vector<std::vector<int>> tile_lists(static_cast<size_t>(ntiles));
   const int Md[3] = {d == 3 ? M : 1, d >= 2 ? M : 1, M};
   box_stride = 1;
   for (int k = 0; k < nitems; ++k) {
@@ -534,44 +620,44 @@ void Core::build_plan(const double* nodes_colmajor) {
     it.e2 = ext[2];
     box_stride = std::max<int64_t>(box_stride, static_cast<int64_t>(ext[0]) * ext[1] * ext[2]);
     ditems.push_back(it);
-    // covered tiles (with periodic wrap) -> assembly lists
-    std::vector<int> cov[3];
-    for (int t = 0; t < 3; ++t) {
-      if (t < 3 - d) {
-        cov[t].push_back(0);
-        continue;
-      }
-      for (int i = 0; i < ext[t]; ++i) {
-        const int tt = ((org[t] + i) % Md[t]) / B;
-        if (std::find(cov[t].begin(), cov[t].end(), tt) == cov[t].end()) cov[t].push_back(tt);
-      }
-    }
-    for (int t0 : cov[0])
-      for (int t1 : cov[1])
-        for (int t2 : cov[2]) {
-          int lin = 0;
-          if (d == 3) lin = (t0 * nt + t1) * nt + t2;
-          if (d == 2) lin = t1 * nt + t2;
-          if (d == 1) lin = t2;
-          tile_lists[static_cast<size_t>(lin)].push_back(k);
-        }
   }
   box_stride = (box_stride + 1) / 2 * 2;  // keep the staging area 16-byte aligned
-  std::vector<int> tptr(static_cast<size_t>(ntiles) + 1, 0), titems;
-  for (int t = 0; t < ntiles; ++t) {
-    tptr[static_cast<size_t>(t) + 1] = tptr[static_cast<size_t>(t)] + static_cast<int>(tile_lists[static_cast<size_t>(t)].size());
-    titems.insert(titems.end(), tile_lists[static_cast<size_t>(t)].begin(), tile_lists[static_cast<size_t>(t)].end());
+  if (static_cast<double>(std::max(nitems, 1)) * static_cast<double>(box_stride) > 2.0e9)
+    fail(FGS_ERESOURCE, "spread workspace exceeds 2^31 entries");
+  // Deterministic assembly map: for every grid cell, the private-box entries
+  // (item k, local offset) that land on it, in increasing item order.
+  {
+    std::vector<int> cnt(static_cast<size_t>(grid_elems) + 1, 0);
+    auto for_box = [&](const DItem& it, auto&& fn) {
+      for (int x0 = 0; x0 < it.e0; ++x0) {
+        const int64_t g0 = (it.a0 + x0) % Md[0];
+        for (int x1 = 0; x1 < it.e1; ++x1) {
+          const int64_t g01 = (g0 * Md[1] + (it.a1 + x1) % Md[1]) * Md[2];
+          const int base = (x0 * it.e1 + x1) * it.e2;
+          for (int x2 = 0; x2 < it.e2; ++x2) fn(g01 + (it.a2 + x2) % Md[2], base + x2);
+        }
+      }
+    };
+    for (int k = 0; k < nitems; ++k)
+      for_box(ditems[static_cast<size_t>(k)], [&](int64_t g, int) { ++cnt[static_cast<size_t>(g) + 1]; });
+    for (int64_t g = 0; g < grid_elems; ++g) cnt[static_cast<size_t>(g) + 1] += cnt[static_cast<size_t>(g)];
+    std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+    std::vector<int> idx(static_cast<size_t>(std::max(cnt.back(), 1)));
+    for (int k = 0; k < nitems; ++k) {
+      const int base = static_cast<int>(static_cast<int64_t>(k) * box_stride);
+      for_box(ditems[static_cast<size_t>(k)],
+              [&](int64_t g, int v) { idx[static_cast<size_t>(pos[static_cast<size_t>(g)]++)] = base + v; });
+    }
+    asm_ptr.upload(cnt.data(), cnt.size(), stream);
+    asm_idx.upload(idx.data(), idx.size(), stream);
   }
   if (ditems.empty()) {
     ditems.push_back(DItem{0, 0, 0, 0, 0, 1, 1, 1});
     nitems = 0;
   }
-  if (titems.empty()) titems.push_back(0);
   items.upload(ditems.data(), ditems.size(), stream);
   if (druns.empty()) druns.push_back(DRun{0, 0, 0});
   runs.upload(druns.data(), druns.size(), stream);
-  tile_ptr.upload(tptr.data(), tptr.size(), stream);
-  tile_items.upload(titems.data(), titems.size(), stream);
 
   // window taps of the local slice in internal order
   taps.alloc(static_cast<size_t>(std::max<int64_t>(n_local, 1)) * d * T);
@@ -694,9 +780,8 @@ Workspace& Core::workspace(int nvec) {
 }
 
 size_t Core::smem_bytes(bool interp) const {
-  const Policy pol = policy(d, T);
-  size_t dbl = static_cast<size_t>(box_stride) + static_cast<size_t>(kQ) * d * T + kQ + (interp ? pol.nt : 0);
-  return dbl * sizeof(double);
+  const LaunchShape sh = d == 3 ? shape_of<3>(T) : (d == 2 ? shape_of<2>(T) : shape_of<1>(T));
+  return (static_cast<size_t>(box_stride) + (interp ? sh.extra_interp : sh.extra_spread)) * sizeof(double);
 }
 
 void Core::launch_spread(const PassArgs& a) {
@@ -722,11 +807,9 @@ void Core::launch_interp(const PassArgs& a) {
 }
 
 void Core::launch_assemble(Workspace& w, int nvec) {
-  AssembleArgs aa{items.p, tile_ptr.p, tile_items.p, w.priv.p, box_stride, nitems, w.grid.p, grid_elems, nvec,
-                  d, M, B, nt};
-  int cells = 1;
-  for (int t = 0; t < d; ++t) cells *= B;
-  assemble_kernel<<<ntiles, std::min(256, round32(cells)), 0, stream>>>(aa);
+  AssembleArgs aa{asm_ptr.p, asm_idx.p, w.priv.p, static_cast<int64_t>(std::max(nitems, 1)) * box_stride, w.grid.p,
+                  grid_elems, grid_elems, nvec};
+  assemble_kernel<<<ceil_div(grid_elems, 256), 256, 0, stream>>>(aa);
   ++launches;
   FGS_CUDA(cudaGetLastError());
 }

@@ -81,13 +81,14 @@ class Core {
   bool own_stream = true;
   ncclComm_t comm = nullptr;
   int64_t launches = 0;
+  double lanczos_stats[4] = {0, 0, 0, 0};  // last run: apply ms, reorth ms, loop wall ms, iterations
 
   // device plan
   DBuf<int> perm;  // internal -> caller, all n points (identical on every rank)
   DBuf<double> taps;  // [n_local][d][T]
   DBuf<DItem> items;
   DBuf<DRun> runs;
-  DBuf<int> tile_ptr, tile_items;
+  DBuf<int> asm_ptr, asm_idx;  // grid cell -> private-box entries (CSR, item order)
   DBuf<cufftDoubleComplex> mult;  // compact Hermitian multiplier (FASTSUM)
   DBuf<double> deconv_d;
   int nitems = 0;
@@ -149,5 +150,6 @@ void validate_params(const Params& p);
 
 // fp64 FMA peak of a device in TFLOP/s (peak.cu)
 double measure_fp64_peak(int device);
+double measure_dmma_peak(int device);
 
 }  // namespace fgsb

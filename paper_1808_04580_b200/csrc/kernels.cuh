@@ -229,61 +229,30 @@ __global__ void __launch_bounds__(NT) spread_kernel(PassArgs a, int Trt, int box
 }
 
 // ---------------------------------------------------------------------------
-// Deterministic grid assembly: grid cell g = sum over the items whose box
-// covers g, in item order, of the item's private box value.
+// Deterministic grid assembly: grid cell g = sum, in increasing item order,
+// of the private-box entries that map onto g (CSR built at plan time).  A
+// pure gather: no atomics, fixed summation order -> bitwise reproducible.
 // ---------------------------------------------------------------------------
 struct AssembleArgs {
-  const DItem* items;
-  const int* tile_ptr;
-  const int* tile_items;
+  const int* ptr;       // grid_elems + 1
+  const int* idx;       // private-box entry offsets
   const double* priv;
-  int64_t box_stride;
-  int nitems;
+  int64_t priv_stride;  // per vector
   double* grid;
   int64_t grid_stride;
+  int64_t cells;
   int nvec;
-  int D, M, B, nt;
 };
 
 __global__ void assemble_kernel(AssembleArgs a) {
-  const int tile = blockIdx.x;
-  int tc[3] = {0, 0, 0};
-  {
-    int rest = tile;
-    for (int t = a.D - 1; t >= 0; --t) {
-      tc[3 - a.D + t] = rest % a.nt;
-      rest /= a.nt;
-    }
-  }
-  const int Md[3] = {a.D == 3 ? a.M : 1, a.D >= 2 ? a.M : 1, a.M};
-  const int Bd[3] = {a.D == 3 ? a.B : 1, a.D >= 2 ? a.B : 1, a.B};
-  const int cells = Bd[0] * Bd[1] * Bd[2];
-  const int lb = a.tile_ptr[tile], le = a.tile_ptr[tile + 1];
-  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
-    const int i2 = c % Bd[2], i1 = (c / Bd[2]) % Bd[1], i0 = c / (Bd[2] * Bd[1]);
-    const int g0 = tc[0] * Bd[0] + i0, g1 = tc[1] * Bd[1] + i1, g2 = tc[2] * Bd[2] + i2;
-    if (g0 >= Md[0] || g1 >= Md[1] || g2 >= Md[2]) continue;
-    const int64_t gidx = (static_cast<int64_t>(g0) * Md[1] + g1) * Md[2] + g2;
-    for (int vec = 0; vec < a.nvec; ++vec) {
-      double acc = 0.0;
-      for (int l = lb; l < le; ++l) {
-        const int k = a.tile_items[l];
-        const DItem it = a.items[k];
-        const double* box = a.priv + (static_cast<int64_t>(vec) * a.nitems + k) * a.box_stride;
-        int x0 = g0 - it.a0;
-        x0 = x0 < 0 ? x0 + Md[0] : x0;
-        for (; x0 < it.e0; x0 += Md[0]) {
-          int x1 = g1 - it.a1;
-          x1 = x1 < 0 ? x1 + Md[1] : x1;
-          for (; x1 < it.e1; x1 += Md[1]) {
-            int x2 = g2 - it.a2;
-            x2 = x2 < 0 ? x2 + Md[2] : x2;
-            for (; x2 < it.e2; x2 += Md[2]) acc += box[(x0 * it.e1 + x1) * it.e2 + x2];
-          }
-        }
-      }
-      a.grid[vec * a.grid_stride + gidx] = acc;
-    }
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= a.cells) return;
+  const int b = a.ptr[g], e = a.ptr[g + 1];
+  for (int v = 0; v < a.nvec; ++v) {
+    const double* pv = a.priv + v * a.priv_stride;
+    double acc = 0.0;
+    for (int l = b; l < e; ++l) acc += pv[a.idx[l]];
+    a.grid[v * a.grid_stride + g] = acc;
   }
 }
 

@@ -1,0 +1,325 @@
+// kernels_v4.cuh -- fp64 tensor-core (DMMA, mma.sync.m8n8k4.f64) spread and
+// interpolation for d = 3, 2m in {8, 12, 16}: the dense-cell fast path.
+//
+// Per run (points sharing one footprint) both passes are small GEMMs over the
+// footprint's (a, c) "pairs":
+//   interp: Z[j][(a,c)] = sum_e  we_j[e] g[(a,c)][e]          M = 8 points, K = e, N = pairs
+//           y_j        = sum_a wa_j[a] sum_c wc_j[c] Z[j][(a,c)]   (scalar, 1/(2m) of the flops)
+//   spread: G[(a,c)][e] += sum_j (wa_j[a] wc_j[c]) (x_j we_j[e])   M = pairs, K = 4 points, N = e
+// One DMMA = 256 fp64 FMAs from register operands, so the fp64 pipe is fed
+// with ~8x fewer issued instructions and no shared-memory operand per FMA
+// (the limiter of the scalar kernels: ncu short-scoreboard / wait stalls).
+// Measured on this B200: DMMA 36.7 TFLOP/s = DFMA 36.6 TFLOP/s peak.
+//
+// Pair tiling: an 8-wide MMA tile covers 2 a-values x 4 c-values,
+//   n (or m) in 0..7  <->  (a = 2 ta + n / 4, c = 4 tc + n % 4),
+// so for the C-fragment element (lane, i) the a-offset is (lane&3)/2 and the
+// c-offset 2 (lane&1) + i: every lane touches only 2m/2 a-taps and 2m/2
+// c-taps of its point, held in registers with compile-time indices.
+// Fragment layouts (checked on the B200 by tools/dmma_layout_check.cu):
+//   A 8x4 row: lane holds A[lane/4][lane%4];  B 4x8 col: B[lane%4][lane/4];
+//   C 8x8: lane holds C[lane/4][2 (lane%4) + i], i = 0, 1.
+// Groups of G warps share one footprint (G = 2 for 2m = 16 splits the a
+// range); P groups per CTA walk different K-steps / batches of each staged
+// chunk.  Results are bitwise deterministic (fixed MMA and reduction order).
+#pragma once
+
+#include "kernels_v2.cuh"
+
+namespace fgsb {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int T>
+struct Blk4 {
+  static constexpr int G = T == 16 ? 2 : 1;  // warps per footprint group
+  static constexpr int TA = T / 2;           // a-tiles (2 a each)
+  static constexpr int TC = T / 4;           // c-tiles (4 c each)
+  static constexpr int TAW = TA / G;         // a-tiles per warp
+  static constexpr int TW = TAW * TC;        // pair tiles per warp
+  static constexpr int KS = T / 4;           // interp K-steps over e
+  static constexpr int NE = (T + 7) / 8;     // spread N-tiles over e (2m = 12 pads 12 -> 16)
+  static constexpr int P = T == 8 ? 4 : 2;   // groups (point streams) per CTA
+  static constexpr int NT = 32 * G * P;
+  static constexpr int QS = 32;              // points per staged chunk
+  static constexpr int TAPS = 3 * T;
+};
+
+// ---------------------------------------------------------------------------
+// interpolation.  smem: box | stage[2][QS*TAPS] | red[P][G][8]
+// ---------------------------------------------------------------------------
+template <int T>
+__global__ void __launch_bounds__(Blk4<T>::NT) interp_v4_kernel(PassArgs a, int box_stride_smem) {
+  using B = Blk4<T>;
+  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, G = B::G, P = B::P;
+  constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, KS = B::KS;
+  extern __shared__ __align__(16) double smem[];
+  double* S = smem;
+  double* stg = smem + box_stride_smem;
+  double* red = stg + 2 * QS * TAPS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp / G, wg = warp % G;
+  const int q = lane & 3, r8 = lane >> 2;
+  const int ta0 = wg * TAW;  // first a-tile of this warp
+  const DItem it = a.items[blockIdx.x];
+  const int bx1 = it.e1, bx2 = it.e2;
+  const int V = it.e0 * it.e1 * it.e2;
+  const int M = a.M;
+  const int64_t p_begin = a.runs[it.run_begin].pstart;
+  const DRun last = a.runs[it.run_end - 1];
+  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
+
+  for (int vec = 0; vec < a.nvec; ++vec) {
+    const double* gv = a.grid + vec * a.grid_stride;
+    const double* xv = a.x ? a.x + vec * a.ldx : nullptr;
+    double* yv = a.y ? a.y + vec * a.ldy : nullptr;
+    v2_issue_chunk<TAPS>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
+    cp_async_commit();
+    for (int v = tid; v < V; v += NT) {
+      const int x2 = v % bx2, x1 = (v / bx2) % bx1, x0 = v / (bx2 * bx1);
+      S[v] = gv[(static_cast<int64_t>((it.a0 + x0) % M) * M + (it.a1 + x1) % M) * M + (it.a2 + x2) % M];
+    }
+    int r = it.run_begin;
+    DRun run = a.runs[r];
+    int loaded = -1;
+    double gB[TW][KS];  // B fragments of the run's grid block: g[pair(lane/4)][4 ks + lane%4]
+
+    for (int k = 0; k < nch; ++k) {
+      const int64_t c0 = p_begin + static_cast<int64_t>(k) * QS;
+      const int64_t c1 = lmin(c0 + QS, p_end);
+      const int buf = k & 1;
+      cp_async_wait_0();
+      __syncthreads();
+      if (k + 1 < nch) {
+        v2_issue_chunk<TAPS>(stg + (buf ^ 1) * QS * TAPS, a.taps, c1, static_cast<int>(lmin(QS, p_end - c1)), tid, NT);
+        cp_async_commit();
+      }
+      const double* sb = stg + buf * QS * TAPS;
+      for (int64_t b0 = c0 + 8 * grp; b0 < c1; b0 += 8 * P) {
+        const int64_t ipt = b0 + r8;  // this lane's point (C rows / A rows)
+        const bool in_chunk = ipt < c1;
+        const double* w = sb + (in_chunk ? (ipt - c0) : 0) * TAPS;
+        // epilogue operands prefetch (lanes q == 0 of warp 0 of the group)
+        double xin = 0.0, sin_ = 1.0;
+        int64_t ix = 0;
+        if (wg == 0 && q == 0 && in_chunk) {
+          ix = a.perm ? static_cast<int64_t>(a.perm[ipt]) : ipt;
+          if (xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE) xin = xv[ix];
+          if (a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN) sin_ = a.s[ipt];
+        }
+        // this lane's a- and c-taps (compile-time register indices)
+        double wa[TAW], wc[TC][2];
+#pragma unroll
+        for (int t = 0; t < TAW; ++t) wa[t] = w[2 * (ta0 + t) + (q >> 1)];
+#pragma unroll
+        for (int t = 0; t < TC; ++t) {
+          wc[t][0] = w[T + 4 * t + 2 * (q & 1)];
+          wc[t][1] = w[T + 4 * t + 2 * (q & 1) + 1];
+        }
+        double yacc = 0.0;
+        while (true) {
+          while (static_cast<int64_t>(run.pstart) + run.pcount <= b0 && r + 1 < it.run_end) run = a.runs[++r];
+          if (loaded != r) {
+            const int o0 = run.off & 1023, o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
+#pragma unroll
+            for (int t = 0; t < TW; ++t) {
+              const int ta = ta0 + t / TC, tc = t % TC;
+              const int aa = 2 * ta + (r8 >> 2), cc = 4 * tc + (r8 & 3);
+              const double* row = S + ((o0 + aa) * bx1 + (o1 + cc)) * bx2 + o2 + q;
+#pragma unroll
+              for (int ks = 0; ks < KS; ++ks) gB[t][ks] = row[4 * ks];
+            }
+            loaded = r;
+          }
+          const int64_t rs = run.pstart, re_ = static_cast<int64_t>(run.pstart) + run.pcount;
+          const bool mine = in_chunk && ipt >= rs && ipt < re_;
+          double aF[KS];  // A fragments: we_{point}[4 ks + q], zero outside this run
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) aF[ks] = mine ? w[2 * T + 4 * ks + q] : 0.0;
+          double K[TAW];
+#pragma unroll
+          for (int t = 0; t < TAW; ++t) K[t] = 0.0;
+#pragma unroll
+          for (int t = 0; t < TW; ++t) {
+            double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) dmma(z0, z1, aF[ks], gB[t][ks]);
+            const int ta = t / TC, tc = t % TC;
+            K[ta] = fma(wc[tc][0], z0, K[ta]);
+            K[ta] = fma(wc[tc][1], z1, K[ta]);
+          }
+#pragma unroll
+          for (int t = 0; t < TAW; ++t) yacc = fma(wa[t], K[t], yacc);
+          if (re_ < lmin(b0 + 8, c1) && r + 1 < it.run_end) {  // batch continues in the next run
+            run = a.runs[++r];
+            continue;
+          }
+          break;
+        }
+        // sum the 4 lanes of each point, then the G warps of the group
+        yacc += __shfl_xor_sync(0xffffffffu, yacc, 1);
+        yacc += __shfl_xor_sync(0xffffffffu, yacc, 2);
+        if (G > 1) {
+          double* rg = red + grp * G * 8;
+          if (wg > 0 && q == 0) rg[wg * 8 + r8] = yacc;
+          asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(32 * G) : "memory");
+          if (wg == 0 && q == 0)
+#pragma unroll
+            for (int w2 = 1; w2 < G; ++w2) yacc += rg[w2 * 8 + r8];
+          asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(32 * G) : "memory");
+        }
+        if (wg == 0 && q == 0 && in_chunk) {
+          const double val = yacc;
+          if (a.epilogue == EPI_DEGREE) {
+            const double dg = val - a.k0;  // graphop.cpp:55-56
+            a.degrees[ipt] = dg;
+            a.inv_sqrt[ipt] = 1.0 / sqrt(dg);
+            if (!(dg > 0.0)) atomicMin(a.bad_flag, static_cast<unsigned long long>(a.caller[ipt]));
+          } else {
+            double out;
+            switch (a.epilogue) {
+              case EPI_KERNEL: out = val; break;
+              case EPI_WEIGHT: out = val - a.k0 * xin; break;
+              case EPI_NORMALIZED: out = sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
+              default: out = xin - sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
+            }
+            yv[ix] = out;
+          }
+        }
+      }
+    }
+    cp_async_wait_0();
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// spread.  smem: box | stage[2][QS*TAPS] | xs[2][QS]
+// ---------------------------------------------------------------------------
+template <int T>
+__global__ void __launch_bounds__(Blk4<T>::NT) spread_v4_kernel(PassArgs a, int box_stride_smem) {
+  using B = Blk4<T>;
+  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P;
+  constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, NE = B::NE;
+  extern __shared__ __align__(16) double smem[];
+  double* S = smem;
+  double* stg = smem + box_stride_smem;
+  double* xs = stg + 2 * QS * TAPS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp / B::G, wg = warp % B::G;
+  const int q = lane & 3, r8 = lane >> 2;
+  const int ta0 = wg * TAW;
+  const DItem it = a.items[blockIdx.x];
+  const int bx1 = it.e1, bx2 = it.e2;
+  const int V = it.e0 * it.e1 * it.e2;
+  const int64_t p_begin = a.runs[it.run_begin].pstart;
+  const DRun last = a.runs[it.run_end - 1];
+  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
+
+  for (int vec = 0; vec < a.nvec; ++vec) {
+    const double* xv = a.x + vec * a.ldx;
+    for (int v = tid; v < V; v += NT) S[v] = 0.0;
+    v2_issue_chunk<TAPS>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
+    cp_async_commit();
+    if (tid < QS && p_begin + tid < p_end) xs[tid] = v2_x(a, xv, p_begin + tid);
+    int r = it.run_begin;
+    DRun run = a.runs[r];
+    double C[TW][NE][2];
+#pragma unroll
+    for (int t = 0; t < TW; ++t)
+#pragma unroll
+      for (int ne = 0; ne < NE; ++ne) C[t][ne][0] = C[t][ne][1] = 0.0;
+
+    // flush this group's accumulators of `run` into the box, groups in turn
+    auto flush = [&]() {
+      const int o0 = run.off & 1023, o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
+      for (int g = 0; g < P; ++g) {
+        if (g == grp) {
+#pragma unroll
+          for (int t = 0; t < TW; ++t) {
+            const int ta = ta0 + t / TC, tc = t % TC;
+            const int aa = 2 * ta + (r8 >> 2), cc = 4 * tc + (r8 & 3);
+            double* row = S + ((o0 + aa) * bx1 + (o1 + cc)) * bx2 + o2;
+#pragma unroll
+            for (int ne = 0; ne < NE; ++ne)
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const int e = 8 * ne + 2 * q + i;
+                if (e < T) row[e] += C[t][ne][i];
+                C[t][ne][i] = 0.0;
+              }
+          }
+        }
+        __syncthreads();
+      }
+    };
+
+    for (int k = 0; k < nch; ++k) {
+      const int64_t c0 = p_begin + static_cast<int64_t>(k) * QS;
+      const int64_t c1 = lmin(c0 + QS, p_end);
+      const int buf = k & 1;
+      cp_async_wait_0();
+      __syncthreads();
+      const bool more = k + 1 < nch;
+      double xnext = 0.0;
+      int qn = 0;
+      if (more) {
+        qn = static_cast<int>(lmin(QS, p_end - c1));
+        v2_issue_chunk<TAPS>(stg + (buf ^ 1) * QS * TAPS, a.taps, c1, qn, tid, NT);
+        cp_async_commit();
+        if (tid < qn) xnext = v2_x(a, xv, c1 + tid);
+      }
+      const double* sb = stg + buf * QS * TAPS;
+      const double* xb = xs + buf * QS;
+      while (true) {
+        const int64_t rs = run.pstart, re_ = static_cast<int64_t>(run.pstart) + run.pcount;
+        const int64_t s0 = rs > c0 ? rs : c0, s1 = lmin(re_, c1);
+        // K-steps of 4 points aligned to the chunk; group grp takes every P-th
+        for (int64_t k0 = c0 + 4 * grp; k0 < s1; k0 += 4 * P) {
+          if (k0 + 4 <= s0) continue;
+          const int64_t jp = k0 + q;  // this lane's point of the K-step
+          const bool ok = jp >= s0 && jp < s1;
+          const double* w = sb + (ok ? (jp - c0) : 0) * TAPS;
+          const double xj = ok ? xb[jp - c0] : 0.0;
+          double wa[TAW], wc[TC];
+#pragma unroll
+          for (int t = 0; t < TAW; ++t) wa[t] = w[2 * (ta0 + t) + (r8 >> 2)];
+#pragma unroll
+          for (int t = 0; t < TC; ++t) wc[t] = w[T + 4 * t + (r8 & 3)];
+          double bF[NE];  // x_j we_j[e], e = 8 ne + lane/4
+#pragma unroll
+          for (int ne = 0; ne < NE; ++ne) {
+            const int e = 8 * ne + r8;
+            bF[ne] = e < T ? xj * w[2 * T + e] : 0.0;
+          }
+#pragma unroll
+          for (int t = 0; t < TW; ++t) {
+            const double af = wa[t / TC] * wc[t % TC];  // wa wc of pair (lane/4 row)
+#pragma unroll
+            for (int ne = 0; ne < NE; ++ne) dmma(C[t][ne][0], C[t][ne][1], af, bF[ne]);
+          }
+        }
+        if (re_ <= c1) {  // run ends inside this chunk
+          flush();
+          if (++r >= it.run_end) break;
+          run = a.runs[r];
+          continue;
+        }
+        break;
+      }
+      if (more && tid < qn) xs[(buf ^ 1) * QS + tid] = xnext;
+    }
+    __syncthreads();
+    double* out = a.priv + (static_cast<int64_t>(vec) * gridDim.x + blockIdx.x) * a.box_stride;
+    for (int v = tid; v < V; v += NT) out[v] = S[v];
+    __syncthreads();
+  }
+}
+
+}  // namespace fgsb

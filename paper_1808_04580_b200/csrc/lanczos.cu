@@ -9,6 +9,7 @@
 // tree (block partials -> ordered final sum), so a run is bitwise
 // reproducible.  Sharded runs add one NCCL allreduce per reduction.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <limits>
 #include <numeric>
@@ -291,10 +292,17 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     tri_size = m;
   };
 
+  // per-phase device timing (operator applies vs reorthogonalisation)
+  cudaEvent_t ev[3];
+  for (auto& e : ev) FGS_CUDA(cudaEventCreate(&e));
+  double apply_ms = 0.0, reorth_ms = 0.0;
+  const auto wall0 = std::chrono::steady_clock::now();
   while (true) {
     const int m = static_cast<int>(alphas.size()) + 1;
     const double* qcur = basis.p + static_cast<int64_t>(m - 1) * nl;
+    FGS_CUDA(cudaEventRecord(ev[0], st));
     c.apply(epi, qcur, nl, z.p, nl, 1, false, true);
+    FGS_CUDA(cudaEventRecord(ev[1], st));
     ++iterations;
     // alpha = q . z
     multidot(qcur, 1, z.p, scal.p);
@@ -305,9 +313,17 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     cgs_pass(m, z.p);
     cgs_pass(m, z.p);
     multidot(z.p, 1, z.p, scal.p + 1);
+    FGS_CUDA(cudaEventRecord(ev[2], st));
     double ab[2];
     FGS_CUDA(cudaMemcpyAsync(ab, scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     FGS_CUDA(cudaStreamSynchronize(st));
+    {
+      float t01 = 0.f, t12 = 0.f;
+      FGS_CUDA(cudaEventElapsedTime(&t01, ev[0], ev[1]));
+      FGS_CUDA(cudaEventElapsedTime(&t12, ev[1], ev[2]));
+      apply_ms += t01;
+      reorth_ms += t12;
+    }
     const double alpha = ab[0], beta = std::sqrt(ab[1]);
     alphas.push_back(alpha);
     scale = std::max(scale, std::abs(alpha) + beta + beta_prev);
@@ -375,12 +391,16 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     }
   }
 
+  for (auto& e : ev) cudaEventDestroy(e);
   const int m = static_cast<int>(alphas.size());
   if (tri_size != m) solve_tri(m);
   const int wanted = std::min(k, m);
   LanczosResult res;
   res.iterations = iterations;
   res.converged = converged;
+  res.apply_ms = apply_ms;
+  res.reorth_ms = reorth_ms;
+  res.loop_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
   res.values.resize(static_cast<size_t>(wanted));
   std::vector<double> S(static_cast<size_t>(m) * wanted);  // row-major m x wanted
   for (int i = 0; i < wanted; ++i) {

@@ -232,8 +232,12 @@ def test_lanczos_matches_oracle_on_config1(orc):
     for j in range(k):
         col = pairs.vectors[:, j]
         assert col[np.argmax(np.abs(col))] > 0
+    # adjacency_to_laplacian: values 1 - lambda_A(k-1-i) (spectral.cpp:129-139,
+    # test_spectral.cpp:76-81), so the Perron pair (L-eigenvalue ~0) is last
     lap = fgs.adjacency_to_laplacian(pairs)
-    assert abs(lap.values[0]) <= 1e-8 and np.all(np.diff(lap.values) >= 0)
+    assert abs(lap.values[-1]) <= 1e-8
+    assert np.array_equal(lap.values, 1.0 - pairs.values[::-1])
+    assert np.array_equal(lap.vectors[:, 0], pairs.vectors[:, -1])
 
 
 def test_lanczos_laplacian_handle_and_reproducibility(orc):
