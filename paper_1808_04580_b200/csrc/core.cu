@@ -164,6 +164,10 @@ bool kernel_env(const char* v) {
   const char* e = std::getenv("FGS_KERNEL");
   return e && std::string(e) == v;
 }
+// the tensor-core spread needs runs of >= this many points (K-steps of 4,
+// one block flush per run); sparser plans use the scalar register-blocked one
+constexpr double kDenseRun = 12.0;
+
 bool use_v1() {
   static const bool v1 = kernel_env("v1");
   return v1;
@@ -200,7 +204,7 @@ struct LaunchShape {
 };
 
 template <int D, int T>
-LaunchShape shape_t() {
+LaunchShape shape_t(bool dense) {
   if (use_v1()) {
     const size_t base = static_cast<size_t>(kQ) * D * T + kQ;
     return {nt_of<D, T>(), base, base + nt_of<D, T>()};
@@ -212,26 +216,27 @@ LaunchShape shape_t() {
   if constexpr (has_v3<D, T>()) {
     using B3 = Blk3<T>;
     if (use_v3()) interp = 2 * static_cast<size_t>(B3::QS) * B3::TAPS + static_cast<size_t>(B3::P) * B3::G * B3::QB;
-    using B4 = Blk4<T>;
+    using B4i = Blk4<T, true>;
+    using B4s = Blk4<T, false>;
     if (use_v4()) {
-      interp = 2 * static_cast<size_t>(B4::QS) * B4::TAPS + static_cast<size_t>(B4::P) * B4::G * 8;
-      spread = 2 * static_cast<size_t>(B4::QS) * B4::TAPS + 2 * B4::QS;
+      interp = 2 * static_cast<size_t>(B4i::QS) * B4i::TAPS + static_cast<size_t>(B4i::P) * B4i::G * 8;
+      if (dense) spread = 2 * static_cast<size_t>(B4s::QS) * B4s::TAPS + 2 * B4s::QS;
     }
   }
   return {B::NT, spread, interp};
 }
 
 template <int D>
-LaunchShape shape_of(int T) {
+LaunchShape shape_of(int T, bool dense) {
   switch (T) {
-    case 2: return shape_t<D, 2>();
-    case 4: return shape_t<D, 4>();
-    case 6: return shape_t<D, 6>();
-    case 8: return shape_t<D, 8>();
-    case 10: return shape_t<D, 10>();
-    case 12: return shape_t<D, 12>();
-    case 14: return shape_t<D, 14>();
-    case 16: return shape_t<D, 16>();
+    case 2: return shape_t<D, 2>(dense);
+    case 4: return shape_t<D, 4>(dense);
+    case 6: return shape_t<D, 6>(dense);
+    case 8: return shape_t<D, 8>(dense);
+    case 10: return shape_t<D, 10>(dense);
+    case 12: return shape_t<D, 12>(dense);
+    case 14: return shape_t<D, 14>(dense);
+    case 16: return shape_t<D, 16>(dense);
     default: break;
   }
   const size_t base = static_cast<size_t>(kQ) * D * T + kQ;
@@ -239,7 +244,7 @@ LaunchShape shape_of(int T) {
 }
 
 template <int D, int T>
-void launch_t(bool interp, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
+void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
   if (use_v1()) {
     constexpr int E = e_of<D, T>();
     constexpr int NT = nt_of<D, T>();
@@ -256,15 +261,15 @@ void launch_t(bool interp, const PassArgs& a, int nitems, size_t smem, int box_s
   }
   constexpr int NT = Blk<D, T>::NT;
   if constexpr (has_v3<D, T>()) {
-    if (use_v4()) {
+    if (use_v4() && (interp || dense)) {
       if (interp) {
         auto k = interp_v4_kernel<T>;
         FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        k<<<nitems, Blk4<T>::NT, smem, s>>>(a, box_stride);
+        k<<<nitems, Blk4<T, true>::NT, smem, s>>>(a, box_stride);
       } else {
         auto k = spread_v4_kernel<T>;
         FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        k<<<nitems, Blk4<T>::NT, smem, s>>>(a, box_stride);
+        k<<<nitems, Blk4<T, false>::NT, smem, s>>>(a, box_stride);
       }
       return;
     }
@@ -287,16 +292,17 @@ void launch_t(bool interp, const PassArgs& a, int nitems, size_t smem, int box_s
 }
 
 template <int D>
-void dispatch(bool interp, int T, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
+void dispatch(bool interp, bool dense, int T, const PassArgs& a, int nitems, size_t smem, int box_stride,
+              cudaStream_t s) {
   switch (T) {
-    case 2: return launch_t<D, 2>(interp, a, nitems, smem, box_stride, s);
-    case 4: return launch_t<D, 4>(interp, a, nitems, smem, box_stride, s);
-    case 6: return launch_t<D, 6>(interp, a, nitems, smem, box_stride, s);
-    case 8: return launch_t<D, 8>(interp, a, nitems, smem, box_stride, s);
-    case 10: return launch_t<D, 10>(interp, a, nitems, smem, box_stride, s);
-    case 12: return launch_t<D, 12>(interp, a, nitems, smem, box_stride, s);
-    case 14: return launch_t<D, 14>(interp, a, nitems, smem, box_stride, s);
-    case 16: return launch_t<D, 16>(interp, a, nitems, smem, box_stride, s);
+    case 2: return launch_t<D, 2>(interp, dense, a, nitems, smem, box_stride, s);
+    case 4: return launch_t<D, 4>(interp, dense, a, nitems, smem, box_stride, s);
+    case 6: return launch_t<D, 6>(interp, dense, a, nitems, smem, box_stride, s);
+    case 8: return launch_t<D, 8>(interp, dense, a, nitems, smem, box_stride, s);
+    case 10: return launch_t<D, 10>(interp, dense, a, nitems, smem, box_stride, s);
+    case 12: return launch_t<D, 12>(interp, dense, a, nitems, smem, box_stride, s);
+    case 14: return launch_t<D, 14>(interp, dense, a, nitems, smem, box_stride, s);
+    case 16: return launch_t<D, 16>(interp, dense, a, nitems, smem, box_stride, s);
     default: break;
   }
   // runtime-2m fallback (m > 8): one value per unit, 256 threads
@@ -504,8 +510,11 @@ void Core::build_plan(const double* nodes_colmajor) {
   n_local = n * (rank + 1) / world - offset;
 
   // ---- work items: runs of cells inside one tile, <= chunk points ---------
-  int64_t target_items = 4 * 148;
-  int chunk = static_cast<int>(std::max<int64_t>(64, std::min<int64_t>(4096, (n_local + target_items - 1) / target_items)));
+  // items (CTAs) per pass: enough to fill every SM several times over; small
+  // problems get short items (their cost is the serial staging chain)
+  int64_t target_items = 16 * 148;
+  if (const char* e = std::getenv("FGS_ITEM_TARGET")) target_items = std::max<int64_t>(1, std::atoll(e));
+  int chunk = static_cast<int>(std::max<int64_t>(32, std::min<int64_t>(4096, (n_local + target_items - 1) / target_items)));
   chunk = (chunk + 31) / 32 * 32;
   int BD = 1;
   for (int t = 0; t < d; ++t) BD *= B;
@@ -582,6 +591,11 @@ void Core::build_plan(const double* nodes_colmajor) {
   std::stable_sort(hitems.begin(), hitems.end(), [](const HItem& x, const HItem& y) { return x.npts > y.npts; });
 
   nitems = static_cast<int>(hitems.size());
+  {
+    size_t nr = 0;
+    for (const HItem& h : hitems) nr += h.runs.size();
+    mean_run = nr ? static_cast<double>(n_local) / static_cast<double>(nr) : 0.0;
+  }
   std::vector<DItem> ditems;
   std::vector<DRun> druns;
   const int Md[3] = {d == 3 ? M : 1, d >= 2 ? M : 1, M};
@@ -780,7 +794,8 @@ Workspace& Core::workspace(int nvec) {
 }
 
 size_t Core::smem_bytes(bool interp) const {
-  const LaunchShape sh = d == 3 ? shape_of<3>(T) : (d == 2 ? shape_of<2>(T) : shape_of<1>(T));
+  const bool dense = mean_run >= kDenseRun;
+  const LaunchShape sh = d == 3 ? shape_of<3>(T, dense) : (d == 2 ? shape_of<2>(T, dense) : shape_of<1>(T, dense));
   return (static_cast<size_t>(box_stride) + (interp ? sh.extra_interp : sh.extra_spread)) * sizeof(double);
 }
 
@@ -788,9 +803,10 @@ void Core::launch_spread(const PassArgs& a) {
   if (nitems == 0) return;
   const size_t smem = smem_bytes(false);
   if (smem > 227 * 1024) fail(FGS_ERESOURCE, "tile box exceeds shared memory (cutoff too large for d = 3)");
-  if (d == 3) dispatch<3>(false, T, a, nitems, smem, static_cast<int>(box_stride), stream);
-  if (d == 2) dispatch<2>(false, T, a, nitems, smem, static_cast<int>(box_stride), stream);
-  if (d == 1) dispatch<1>(false, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  const bool dense = mean_run >= kDenseRun;
+  if (d == 3) dispatch<3>(false, dense, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  if (d == 2) dispatch<2>(false, dense, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  if (d == 1) dispatch<1>(false, dense, T, a, nitems, smem, static_cast<int>(box_stride), stream);
   ++launches;
   FGS_CUDA(cudaGetLastError());
 }
@@ -799,9 +815,9 @@ void Core::launch_interp(const PassArgs& a) {
   if (nitems == 0) return;
   const size_t smem = smem_bytes(true);
   if (smem > 227 * 1024) fail(FGS_ERESOURCE, "tile box exceeds shared memory (cutoff too large for d = 3)");
-  if (d == 3) dispatch<3>(true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
-  if (d == 2) dispatch<2>(true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
-  if (d == 1) dispatch<1>(true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  if (d == 3) dispatch<3>(true, true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  if (d == 2) dispatch<2>(true, true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  if (d == 1) dispatch<1>(true, true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
   ++launches;
   FGS_CUDA(cudaGetLastError());
 }
@@ -809,7 +825,14 @@ void Core::launch_interp(const PassArgs& a) {
 void Core::launch_assemble(Workspace& w, int nvec) {
   AssembleArgs aa{asm_ptr.p, asm_idx.p, w.priv.p, static_cast<int64_t>(std::max(nitems, 1)) * box_stride, w.grid.p,
                   grid_elems, grid_elems, nvec};
-  assemble_kernel<<<ceil_div(grid_elems, 256), 256, 0, stream>>>(aa);
+  // lanes per grid cell from the mean CSR list length
+  const double mean_list = static_cast<double>(asm_idx.n) / static_cast<double>(std::max<int64_t>(grid_elems, 1));
+  if (mean_list >= 16.0)
+    assemble_kernel<8><<<ceil_div(grid_elems * 8, 256), 256, 0, stream>>>(aa);
+  else if (mean_list >= 4.0)
+    assemble_kernel<4><<<ceil_div(grid_elems * 4, 256), 256, 0, stream>>>(aa);
+  else
+    assemble_kernel<1><<<ceil_div(grid_elems, 256), 256, 0, stream>>>(aa);
   ++launches;
   FGS_CUDA(cudaGetLastError());
 }

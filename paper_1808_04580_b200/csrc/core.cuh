@@ -92,6 +92,7 @@ class Core {
   DBuf<cufftDoubleComplex> mult;  // compact Hermitian multiplier (FASTSUM)
   DBuf<double> deconv_d;
   int nitems = 0;
+  double mean_run = 0.0;  // points per run (cell piece) of this shard: picks the spread kernel
   int64_t box_stride = 0;
   int64_t grid_elems = 0, spec_elems = 0, window_elems = 0;
   std::vector<int> host_perm;

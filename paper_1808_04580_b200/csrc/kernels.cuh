@@ -244,15 +244,29 @@ struct AssembleArgs {
   int nvec;
 };
 
+// L lanes per grid cell (1, 4 or 8 by the mean list length): each sums a
+// contiguous slice of the cell's entry list in order, then the slices are
+// combined by a fixed shuffle tree, so the result is bitwise reproducible.
+template <int kAsmLanes>
 __global__ void assemble_kernel(AssembleArgs a) {
-  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (g >= a.cells) return;
-  const int b = a.ptr[g], e = a.ptr[g + 1];
+  const int64_t gt = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t g = gt / kAsmLanes;
+  const int sub = static_cast<int>(gt % kAsmLanes);
+  const bool valid = g < a.cells;
+  int b = 0, e = 0;
+  if (valid) {
+    const int b0 = a.ptr[g], e0 = a.ptr[g + 1];
+    const int per = (e0 - b0 + kAsmLanes - 1) / kAsmLanes;
+    b = min(e0, b0 + sub * per);
+    e = min(e0, b + per);
+  }
   for (int v = 0; v < a.nvec; ++v) {
     const double* pv = a.priv + v * a.priv_stride;
     double acc = 0.0;
     for (int l = b; l < e; ++l) acc += pv[a.idx[l]];
-    a.grid[v * a.grid_stride + g] = acc;
+#pragma unroll
+    for (int off = 1; off < kAsmLanes; off <<= 1) acc += __shfl_down_sync(0xffffffffu, acc, off, kAsmLanes > 1 ? kAsmLanes : 32);
+    if (valid && sub == 0) a.grid[v * a.grid_stride + g] = acc;
   }
 }
 

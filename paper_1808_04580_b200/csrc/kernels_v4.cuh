@@ -19,8 +19,8 @@
 // Fragment layouts (checked on the B200 by tools/dmma_layout_check.cu):
 //   A 8x4 row: lane holds A[lane/4][lane%4];  B 4x8 col: B[lane%4][lane/4];
 //   C 8x8: lane holds C[lane/4][2 (lane%4) + i], i = 0, 1.
-// Groups of G warps share one footprint (G = 2 for 2m = 16 splits the a
-// range); P groups per CTA walk different K-steps / batches of each staged
+// Groups of G warps share one footprint (G > 1 splits the a range: 2m = 12
+// G = 2; 2m = 16 G = 4 spread / 2 interpolation); P groups per CTA walk different K-steps / batches of each staged
 // chunk.  Results are bitwise deterministic (fixed MMA and reduction order).
 #pragma once
 
@@ -34,16 +34,18 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int T>
+template <int T, bool INTERP>
 struct Blk4 {
-  static constexpr int G = T == 16 ? 2 : 1;  // warps per footprint group
+  // warps per footprint group: more warps per footprint = fewer registers
+  // per lane (ncu: 236-255 regs capped occupancy at 8 warps/SM with G = 1)
+  static constexpr int G = T == 16 ? (INTERP ? 2 : 4) : (T == 12 ? 2 : 1);
   static constexpr int TA = T / 2;           // a-tiles (2 a each)
   static constexpr int TC = T / 4;           // c-tiles (4 c each)
   static constexpr int TAW = TA / G;         // a-tiles per warp
   static constexpr int TW = TAW * TC;        // pair tiles per warp
   static constexpr int KS = T / 4;           // interp K-steps over e
   static constexpr int NE = (T + 7) / 8;     // spread N-tiles over e (2m = 12 pads 12 -> 16)
-  static constexpr int P = T == 8 ? 4 : 2;   // groups (point streams) per CTA
+  static constexpr int P = T == 8 ? 4 : (T == 12 ? 2 : (INTERP ? 2 : 1));  // groups (point streams) per CTA
   static constexpr int NT = 32 * G * P;
   static constexpr int QS = 32;              // points per staged chunk
   static constexpr int TAPS = 3 * T;
@@ -53,8 +55,8 @@ struct Blk4 {
 // interpolation.  smem: box | stage[2][QS*TAPS] | red[P][G][8]
 // ---------------------------------------------------------------------------
 template <int T>
-__global__ void __launch_bounds__(Blk4<T>::NT) interp_v4_kernel(PassArgs a, int box_stride_smem) {
-  using B = Blk4<T>;
+__global__ void __launch_bounds__(Blk4<T, true>::NT) interp_v4_kernel(PassArgs a, int box_stride_smem) {
+  using B = Blk4<T, true>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, G = B::G, P = B::P;
   constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, KS = B::KS;
   extern __shared__ __align__(16) double smem[];
@@ -144,14 +146,23 @@ __global__ void __launch_bounds__(Blk4<T>::NT) interp_v4_kernel(PassArgs a, int 
           double K[TAW];
 #pragma unroll
           for (int t = 0; t < TAW; ++t) K[t] = 0.0;
+          // tiles in groups of TG so TG independent accumulator chains interleave
+          constexpr int TG = TW % 4 == 0 ? 4 : (TW % 3 == 0 ? 3 : (TW % 2 == 0 ? 2 : 1));
 #pragma unroll
-          for (int t = 0; t < TW; ++t) {
-            double z0 = 0.0, z1 = 0.0;
+          for (int t0 = 0; t0 < TW; t0 += TG) {
+            double z[TG][2];
 #pragma unroll
-            for (int ks = 0; ks < KS; ++ks) dmma(z0, z1, aF[ks], gB[t][ks]);
-            const int ta = t / TC, tc = t % TC;
-            K[ta] = fma(wc[tc][0], z0, K[ta]);
-            K[ta] = fma(wc[tc][1], z1, K[ta]);
+            for (int u = 0; u < TG; ++u) z[u][0] = z[u][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+              for (int u = 0; u < TG; ++u) dmma(z[u][0], z[u][1], aF[ks], gB[t0 + u][ks]);
+#pragma unroll
+            for (int u = 0; u < TG; ++u) {
+              const int ta = (t0 + u) / TC, tc = (t0 + u) % TC;
+              K[ta] = fma(wc[tc][0], z[u][0], K[ta]);
+              K[ta] = fma(wc[tc][1], z[u][1], K[ta]);
+            }
           }
 #pragma unroll
           for (int t = 0; t < TAW; ++t) yacc = fma(wa[t], K[t], yacc);
@@ -202,8 +213,8 @@ __global__ void __launch_bounds__(Blk4<T>::NT) interp_v4_kernel(PassArgs a, int 
 // spread.  smem: box | stage[2][QS*TAPS] | xs[2][QS]
 // ---------------------------------------------------------------------------
 template <int T>
-__global__ void __launch_bounds__(Blk4<T>::NT) spread_v4_kernel(PassArgs a, int box_stride_smem) {
-  using B = Blk4<T>;
+__global__ void __launch_bounds__(Blk4<T, false>::NT) spread_v4_kernel(PassArgs a, int box_stride_smem) {
+  using B = Blk4<T, false>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P;
   constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, NE = B::NE;
   extern __shared__ __align__(16) double smem[];
@@ -298,12 +309,13 @@ __global__ void __launch_bounds__(Blk4<T>::NT) spread_v4_kernel(PassArgs a, int 
             const int e = 8 * ne + r8;
             bF[ne] = e < T ? xj * w[2 * T + e] : 0.0;
           }
+          double af[TW];  // wa wc of pair (lane/4 row), all tiles first
 #pragma unroll
-          for (int t = 0; t < TW; ++t) {
-            const double af = wa[t / TC] * wc[t % TC];  // wa wc of pair (lane/4 row)
+          for (int t = 0; t < TW; ++t) af[t] = wa[t / TC] * wc[t % TC];
 #pragma unroll
-            for (int ne = 0; ne < NE; ++ne) dmma(C[t][ne][0], C[t][ne][1], af, bF[ne]);
-          }
+          for (int ne = 0; ne < NE; ++ne)
+#pragma unroll
+            for (int t = 0; t < TW; ++t) dmma(C[t][ne][0], C[t][ne][1], af[t], bF[ne]);
         }
         if (re_ <= c1) {  // run ends inside this chunk
           flush();
