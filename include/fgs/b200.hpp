@@ -1,0 +1,378 @@
+// fgs/b200.hpp -- C++ drop-in for the reference's hot-path interface over the
+// B200 C ABI (fgs_b200.h).  Header-only; link with -lfgs_b200.
+//
+// Mirrors, name for name (reference: /root/reference/proj/include/fgs):
+//   errors.hpp:8-49      ParameterError, RangeError, ShapeError, NumericalError, ResourceError
+//   kernels.hpp:20-35    KernelFamily, KernelSpec
+//   fastsum.hpp:13-23    FastsumParams (+ preset)
+//   nfft.hpp:59-94       NfftPlan (forward, adjoint, forward_real)
+//   fastsum.hpp:34-67    FastsumPlan (apply, scaling, output_factor, kernel_zero,
+//                        coefficients, kernel_error_estimate)
+//   graphop.hpp:45-97    AdjacencyOperator (degrees, apply_kernel/weight/normalized/
+//                        sym_laplacian)
+//   spectral.hpp:33-70   EigenPairs, LanczosOptions, LanczosInfo, lanczos_largest,
+//                        adjacency_to_laplacian
+// Differences a caller sees: lanczos_largest takes the AdjacencyOperator itself
+// (the Krylov basis stays in HBM; the reference's std::function handle would
+// copy every vector through the host), and the vector types are Eigen's when
+// FGS_B200_WITH_EIGEN is defined, else the minimal column-major stand-ins
+// below (Eigen is not installed in this build image).
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "fgs_b200.h"
+
+#ifdef FGS_B200_WITH_EIGEN
+#include <Eigen/Dense>
+#endif
+
+namespace fgs {
+
+// ---- errors.hpp ------------------------------------------------------------
+class ParameterError : public std::invalid_argument {
+ public:
+  using std::invalid_argument::invalid_argument;
+};
+class RangeError : public std::invalid_argument {
+ public:
+  using std::invalid_argument::invalid_argument;
+};
+class ShapeError : public std::invalid_argument {
+ public:
+  using std::invalid_argument::invalid_argument;
+};
+class NumericalError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ResourceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+/// CUDA / cuFFT / NCCL runtime failure (no reference analogue).
+class DeviceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void check(fgs_status s) {
+  if (s == FGS_OK) return;
+  const std::string msg = fgs_last_error();
+  switch (s) {
+    case FGS_EPARAM: throw ParameterError(msg);
+    case FGS_ERANGE: throw RangeError(msg);
+    case FGS_ESHAPE: throw ShapeError(msg);
+    case FGS_ENUMERIC: throw NumericalError(msg);
+    case FGS_ERESOURCE: throw ResourceError(msg);
+    default: throw DeviceError(msg);
+  }
+}
+}  // namespace detail
+
+// ---- vector types ----------------------------------------------------------
+#ifdef FGS_B200_WITH_EIGEN
+using Eigen::MatrixXd;
+using Eigen::VectorXcd;
+using Eigen::VectorXd;
+using Index = Eigen::Index;
+#else
+using Index = std::int64_t;
+template <class T>
+class BasicVector {
+ public:
+  BasicVector() = default;
+  explicit BasicVector(Index n) : v_(static_cast<size_t>(n), T(0)) {}
+  static BasicVector Zero(Index n) { return BasicVector(n); }
+  static BasicVector Ones(Index n) {
+    BasicVector r(n);
+    for (auto& x : r.v_) x = T(1);
+    return r;
+  }
+  Index size() const { return static_cast<Index>(v_.size()); }
+  T& operator()(Index i) { return v_[static_cast<size_t>(i)]; }
+  const T& operator()(Index i) const { return v_[static_cast<size_t>(i)]; }
+  T* data() { return v_.data(); }
+  const T* data() const { return v_.data(); }
+  void resize(Index n) { v_.resize(static_cast<size_t>(n)); }
+
+ private:
+  std::vector<T> v_;
+};
+using VectorXd = BasicVector<double>;
+using VectorXcd = BasicVector<std::complex<double>>;
+
+/// Column-major dense matrix (Eigen's default layout).
+class MatrixXd {
+ public:
+  MatrixXd() = default;
+  MatrixXd(Index r, Index c) : r_(r), c_(c), a_(static_cast<size_t>(r * c), 0.0) {}
+  Index rows() const { return r_; }
+  Index cols() const { return c_; }
+  double& operator()(Index i, Index j) { return a_[static_cast<size_t>(j * r_ + i)]; }
+  double operator()(Index i, Index j) const { return a_[static_cast<size_t>(j * r_ + i)]; }
+  double* data() { return a_.data(); }
+  const double* data() const { return a_.data(); }
+  VectorXd col(Index j) const {
+    VectorXd v(r_);
+    for (Index i = 0; i < r_; ++i) v(i) = (*this)(i, j);
+    return v;
+  }
+
+ private:
+  Index r_ = 0, c_ = 0;
+  std::vector<double> a_;
+};
+#endif
+
+// ---- kernels.hpp / fastsum.hpp parameters ----------------------------------
+enum class KernelFamily { Gaussian, LaplacianRbf, Multiquadric, InverseMultiquadric };
+
+struct KernelSpec {
+  KernelFamily family = KernelFamily::Gaussian;
+  double shape = 1.0;
+  static KernelSpec gaussian(double s) { return make(KernelFamily::Gaussian, s); }
+  static KernelSpec laplacian_rbf(double s) { return make(KernelFamily::LaplacianRbf, s); }
+  static KernelSpec multiquadric(double c) { return make(KernelFamily::Multiquadric, c); }
+  static KernelSpec inverse_multiquadric(double c) { return make(KernelFamily::InverseMultiquadric, c); }
+
+ private:
+  static KernelSpec make(KernelFamily f, double s) {  // kernels.cpp:18-22
+    if (!(s > 0.0) || !(s < 1e308)) throw ParameterError("kernel shape parameter must be positive and finite");
+    return KernelSpec{f, s};
+  }
+};
+
+struct FastsumParams {
+  int bandwidth = 32;
+  int cutoff = 4;
+  int smoothness = 4;
+  double eps_b = 0.0;
+  double oversampling = 2.0;
+  static FastsumParams preset(int level, double eps_b = 0.0) {
+    fgs_fastsum_params p;
+    detail::check(fgs_fastsum_preset(level, eps_b, &p));
+    return FastsumParams{p.bandwidth, p.cutoff, p.smoothness, p.eps_b, p.oversampling};
+  }
+  fgs_fastsum_params c() const { return {bandwidth, cutoff, smoothness, eps_b, oversampling}; }
+};
+
+inline double bessel_i0(double x) {
+  double r;
+  detail::check(fgs_bessel_i0(x, &r));
+  return r;
+}
+
+// ---- NfftPlan --------------------------------------------------------------
+class NfftPlan {
+ public:
+  NfftPlan(int dims, int bandwidth, int cutoff, const MatrixXd& nodes, double oversampling = 2.0, int device = 0)
+      : n_(nodes.rows()), d_(dims), N_(bandwidth), m_(cutoff) {
+    detail::check(fgs_nfft_create(dims, bandwidth, cutoff, nodes.data(), nodes.rows(), oversampling, device, &h_));
+    int M = 0;
+    std::int64_t F = 0;
+    detail::check(fgs_nfft_info(h_, &M, &F));
+    M_ = M;
+    F_ = F;
+  }
+  ~NfftPlan() { fgs_nfft_destroy(h_); }
+  NfftPlan(NfftPlan&& o) noexcept { *this = std::move(o); }
+  NfftPlan& operator=(NfftPlan&& o) noexcept {
+    std::swap(h_, o.h_);
+    n_ = o.n_;
+    d_ = o.d_;
+    N_ = o.N_;
+    m_ = o.m_;
+    M_ = o.M_;
+    F_ = o.F_;
+    return *this;
+  }
+  NfftPlan(const NfftPlan&) = delete;
+  NfftPlan& operator=(const NfftPlan&) = delete;
+
+  int dims() const { return d_; }
+  int bandwidth() const { return N_; }
+  int cutoff() const { return m_; }
+  Index node_count() const { return n_; }
+  std::size_t coefficient_count() const { return static_cast<std::size_t>(F_); }
+  int grid_size() const { return M_; }
+
+  VectorXcd forward(const VectorXcd& fhat) const {
+    VectorXcd out(n_);
+    detail::check(fgs_nfft_forward(h_, reinterpret_cast<const double*>(fhat.data()), fhat.size(),
+                                   reinterpret_cast<double*>(out.data())));
+    return out;
+  }
+  VectorXcd adjoint(const VectorXcd& x) const {
+    VectorXcd out(F_);
+    detail::check(fgs_nfft_adjoint(h_, reinterpret_cast<const double*>(x.data()), x.size(),
+                                   reinterpret_cast<double*>(out.data())));
+    return out;
+  }
+  VectorXd forward_real(const VectorXcd& fhat) const {
+    VectorXd out(n_);
+    detail::check(fgs_nfft_forward_real(h_, reinterpret_cast<const double*>(fhat.data()), fhat.size(), out.data()));
+    return out;
+  }
+
+ private:
+  fgs_nfft_t h_ = nullptr;
+  Index n_ = 0;
+  int d_ = 0, N_ = 0, m_ = 0, M_ = 0;
+  std::int64_t F_ = 0;
+};
+
+// ---- FastsumPlan -----------------------------------------------------------
+class FastsumPlan {
+ public:
+  FastsumPlan(const MatrixXd& nodes, const KernelSpec& kernel, const FastsumParams& params, int device = 0)
+      : n_(nodes.rows()), d_(static_cast<int>(nodes.cols())), kernel_(kernel), params_(params) {
+    const fgs_fastsum_params p = params.c();
+    detail::check(fgs_fastsum_create(nodes.data(), nodes.rows(), d_, static_cast<fgs_kernel>(kernel.family),
+                                     kernel.shape, &p, device, &h_));
+    detail::check(fgs_fastsum_info(h_, &rho_, &of_, &k0_, &scaled_shape_));
+  }
+  ~FastsumPlan() { fgs_fastsum_destroy(h_); }
+  FastsumPlan(const FastsumPlan&) = delete;
+  FastsumPlan& operator=(const FastsumPlan&) = delete;
+
+  Index size() const { return n_; }
+  int dims() const { return d_; }
+  const FastsumParams& params() const { return params_; }
+  const KernelSpec& kernel() const { return kernel_; }
+  KernelSpec scaled_kernel() const { return KernelSpec{kernel_.family, scaled_shape_}; }
+  double scaling() const { return rho_; }
+  double output_factor() const { return of_; }
+  double kernel_zero() const { return k0_; }
+  VectorXcd coefficients() const {
+    Index F = 1;
+    for (int t = 0; t < d_; ++t) F *= params_.bandwidth;
+    VectorXcd c(F);
+    detail::check(fgs_fastsum_coefficients(h_, reinterpret_cast<double*>(c.data())));
+    return c;
+  }
+  VectorXd apply(const VectorXd& x) const {
+    VectorXd y(n_);
+    detail::check(fgs_fastsum_apply(h_, x.data(), x.size(), y.data()));
+    return y;
+  }
+  double kernel_error_estimate(int sample_count, std::uint64_t seed) const {
+    double r;
+    detail::check(fgs_fastsum_error_estimate(h_, sample_count, seed, &r));
+    return r;
+  }
+
+ private:
+  fgs_fastsum_t h_ = nullptr;
+  Index n_ = 0;
+  int d_ = 0;
+  KernelSpec kernel_;
+  FastsumParams params_;
+  double rho_ = 1.0, of_ = 1.0, k0_ = 0.0, scaled_shape_ = 1.0;
+};
+
+// ---- AdjacencyOperator -----------------------------------------------------
+class AdjacencyOperator {
+ public:
+  AdjacencyOperator(const MatrixXd& nodes, const KernelSpec& kernel, const FastsumParams& params, int device = 0)
+      : n_(nodes.rows()), d_(static_cast<int>(nodes.cols())), kernel_(kernel) {
+    const fgs_fastsum_params p = params.c();
+    std::int64_t bad = -1;
+    detail::check(fgs_adjacency_create(nodes.data(), nodes.rows(), d_, static_cast<fgs_kernel>(kernel.family),
+                                       kernel.shape, &p, device, &h_, &bad));
+    detail::check(fgs_adjacency_info(h_, nullptr, nullptr, &k0_, nullptr, nullptr));
+    degrees_ = VectorXd(n_);
+    detail::check(fgs_adjacency_degrees(h_, degrees_.data()));
+  }
+  ~AdjacencyOperator() { fgs_adjacency_destroy(h_); }
+  AdjacencyOperator(const AdjacencyOperator&) = delete;
+  AdjacencyOperator& operator=(const AdjacencyOperator&) = delete;
+
+  Index size() const { return n_; }
+  int dims() const { return d_; }
+  const KernelSpec& kernel() const { return kernel_; }
+  double kernel_zero() const { return k0_; }
+  const VectorXd& degrees() const { return degrees_; }
+  VectorXd apply_kernel(const VectorXd& x) const { return apply(FGS_OP_KERNEL, x); }
+  VectorXd apply_weight(const VectorXd& x) const { return apply(FGS_OP_WEIGHT, x); }
+  VectorXd apply_normalized(const VectorXd& x) const { return apply(FGS_OP_NORMALIZED, x); }
+  VectorXd apply_sym_laplacian(const VectorXd& x) const { return apply(FGS_OP_SYM_LAPLACIAN, x); }
+  fgs_adjacency_t handle() const { return h_; }
+
+ private:
+  VectorXd apply(fgs_op op, const VectorXd& x) const {
+    if (x.size() != n_) throw ShapeError("input length does not match operator dimension");
+    VectorXd y(n_);
+    detail::check(fgs_adjacency_apply(h_, op, x.data(), y.data(), 1, n_));
+    return y;
+  }
+  fgs_adjacency_t h_ = nullptr;
+  Index n_ = 0;
+  int d_ = 0;
+  KernelSpec kernel_;
+  double k0_ = 0.0;
+  VectorXd degrees_;
+};
+
+// ---- spectral.hpp ----------------------------------------------------------
+struct EigenPairs {
+  VectorXd values;
+  MatrixXd vectors;
+  Index count() const { return values.size(); }
+};
+
+struct LanczosOptions {
+  int max_iter = 1000;
+  double tol = 1e-12;
+  std::uint64_t seed = 1;
+};
+
+struct LanczosInfo {
+  int iterations = 0;
+  bool converged = false;
+};
+
+/// k largest eigenpairs of A = D^-1/2 W D^-1/2 (what lanczos_largest(
+/// adjacency_handle(op), ...) computes in the reference, spectral.cpp:91-96).
+inline EigenPairs lanczos_largest(const AdjacencyOperator& op, int k, const LanczosOptions& opts = {},
+                                  LanczosInfo* info = nullptr) {
+  const Index n = op.size();
+  std::vector<double> vals(static_cast<size_t>(k > 0 ? k : 1));
+  MatrixXd vecs(n, k > 0 ? k : 1);
+  int count = 0, it = 0, conv = 0;
+  detail::check(fgs_lanczos_largest(op.handle(), 0, k, opts.max_iter, opts.tol, opts.seed, vals.data(),
+                                    vecs.data(), &count, &it, &conv));
+  if (info) {
+    info->iterations = it;
+    info->converged = conv != 0;
+  }
+  EigenPairs out;
+  out.values = VectorXd(count);
+  out.vectors = MatrixXd(n, count);
+  for (int i = 0; i < count; ++i) {
+    out.values(i) = vals[static_cast<size_t>(i)];
+    for (Index r = 0; r < n; ++r) out.vectors(r, i) = vecs(r, i);
+  }
+  return out;
+}
+
+/// spectral.cpp:129-139
+inline EigenPairs adjacency_to_laplacian(const EigenPairs& pairs) {
+  const Index k = pairs.count();
+  EigenPairs out;
+  out.values = VectorXd(k);
+  out.vectors = MatrixXd(pairs.vectors.rows(), k);
+  for (Index i = 0; i < k; ++i) {
+    out.values(i) = 1.0 - pairs.values(k - 1 - i);
+    for (Index r = 0; r < pairs.vectors.rows(); ++r) out.vectors(r, i) = pairs.vectors(r, k - 1 - i);
+  }
+  return out;
+}
+
+}  // namespace fgs

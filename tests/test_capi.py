@@ -81,3 +81,9 @@ def test_no_gpu_means_a_loud_failure_not_a_fallback():
     nodes = np.random.default_rng(0).uniform(-0.2, 0.2, (50, 2))
     with pytest.raises((fgs.CudaError, fgs.ResourceError)):
         fgs.FastsumPlan(nodes, fgs.KernelSpec.gaussian(1.0))
+
+
+def test_cpp_dropin_layer_compiles_against_the_header():
+    import __graft_entry__ as g
+    exe = g.build_cpp_dropin_test()
+    assert os.path.exists(exe)

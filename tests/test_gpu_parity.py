@@ -250,3 +250,12 @@ def test_lanczos_laplacian_handle_and_reproducibility(orc):
     lv, lV, it, conv = ref.lanczos_largest(3, tol=1e-10, which=1)
     lp = fgs.lanczos_largest(op, 3, fgs.LanczosOptions(tol=1e-10), which=1)
     assert np.max(np.abs(lp.values - lv)) <= 1e-8 * np.max(np.abs(lv))
+
+
+def test_cpp_dropin_program_passes():
+    # the reference's test cases written against include/fgs/b200.hpp
+    import subprocess
+    import __graft_entry__ as g
+    exe = g.build_cpp_dropin_test()
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
