@@ -220,7 +220,8 @@ def run_b200(args, rank, world, local_rank):
     else:
         op = fgs.AdjacencyOperator(X, kernel, params, device=dev)
     setup_s = time.perf_counter() - t0
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)  # non-default: applies replay captured CUDA graphs
+    torch.cuda.set_stream(stream)
     op.set_stream(stream.cuda_stream)
     nl = op.n_local
     geom = op.geometry()
@@ -249,7 +250,6 @@ def run_b200(args, rank, world, local_rank):
     clocks.start()
     time.sleep(0.15)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    op.profile(True)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -263,9 +263,17 @@ def run_b200(args, rank, world, local_rank):
     w1 = time.time()
     if dist:
         dist.barrier()
+    launches = op.launch_count() - launches0
+    # per-kernel durations: the same K steps again with stage events between
+    # the launches (direct launches; kernel durations do not depend on graph
+    # vs direct launch)
+    op.profile(True)
+    for _ in range(args.steps):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
     op.profile(False)
     stage_ms, napp = op.profile_read()
-    launches = op.launch_count() - launches0
     time.sleep(0.1)
     clocks.stop()
     total_ms = sum(s.elapsed_time(e) for s, e in ev)

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <numeric>
 
@@ -160,6 +162,18 @@ __global__ void permute_kernel(const double* x, int64_t ldx, double* y, int64_t 
 // 2m <= 16: register-blocked cp.async kernels (kernels_v2.cuh); FGS_KERNEL=v1
 // selects the first-generation single-row kernels (kept for A/B timing);
 // 2m > 16: runtime-2m single-value kernels (kernels.cuh).
+// cudaFuncSetAttribute is a driver call; raise each kernel's dynamic shared
+// memory limit once, not on every launch (ncu/launch-overhead hygiene)
+void set_smem(const void* func, size_t smem) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(func);
+  if (it != done.end() && it->second >= smem) return;
+  FGS_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  done[func] = smem;
+}
+
 bool kernel_env(const char* v) {
   const char* e = std::getenv("FGS_KERNEL");
   return e && std::string(e) == v;
@@ -250,11 +264,11 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
     constexpr int NT = nt_of<D, T>();
     if (interp) {
       auto k = interp_kernel<D, T, E, NT>;
-      FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      set_smem(reinterpret_cast<const void*>(k), smem);
       k<<<nitems, NT, smem, s>>>(a, T, box_stride);
     } else {
       auto k = spread_kernel<D, T, E, NT>;
-      FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      set_smem(reinterpret_cast<const void*>(k), smem);
       k<<<nitems, NT, smem, s>>>(a, T, box_stride);
     }
     return;
@@ -264,29 +278,29 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
     if (use_v4() && (interp || dense)) {
       if (interp) {
         auto k = interp_v4_kernel<T>;
-        FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        set_smem(reinterpret_cast<const void*>(k), smem);
         k<<<nitems, Blk4<T, true>::NT, smem, s>>>(a, box_stride);
       } else {
         auto k = spread_v4_kernel<T>;
-        FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        set_smem(reinterpret_cast<const void*>(k), smem);
         k<<<nitems, Blk4<T, false>::NT, smem, s>>>(a, box_stride);
       }
       return;
     }
     if (interp && use_v3()) {
       auto k = interp_v3_kernel<T>;
-      FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      set_smem(reinterpret_cast<const void*>(k), smem);
       k<<<nitems, Blk3<T>::NT, smem, s>>>(a, box_stride);
       return;
     }
   }
   if (interp) {
     auto k = interp_v2_kernel<D, T>;
-    FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    set_smem(reinterpret_cast<const void*>(k), smem);
     k<<<nitems, NT, smem, s>>>(a, box_stride);
   } else {
     auto k = spread_v2_kernel<D, T>;
-    FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    set_smem(reinterpret_cast<const void*>(k), smem);
     k<<<nitems, NT, smem, s>>>(a, box_stride);
   }
 }
@@ -308,11 +322,11 @@ void dispatch(bool interp, bool dense, int T, const PassArgs& a, int nitems, siz
   // runtime-2m fallback (m > 8): one value per unit, 256 threads
   if (interp) {
     auto k = interp_kernel<D, 0, 1, 256>;
-    FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    set_smem(reinterpret_cast<const void*>(k), smem);
     k<<<nitems, 256, smem, s>>>(a, T, box_stride);
   } else {
     auto k = spread_kernel<D, 0, 1, 256>;
-    FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    set_smem(reinterpret_cast<const void*>(k), smem);
     k<<<nitems, 256, smem, s>>>(a, T, box_stride);
   }
 }
@@ -414,6 +428,8 @@ Core::~Core() {
     if (kv.second->has_z2z) cufftDestroy(kv.second->z2z);
   }
   ws_.clear();
+  for (auto& g : graphs_) cudaGraphExecDestroy(g.exec);
+  graphs_.clear();
   for (auto& evs : ev_pending_)
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
@@ -423,6 +439,8 @@ Core::~Core() {
 
 void Core::set_stream(cudaStream_t s) {
   FGS_CUDA(cudaStreamSynchronize(stream));
+  for (auto& g : graphs_) cudaGraphExecDestroy(g.exec);
+  graphs_.clear();
   if (own_stream) cudaStreamDestroy(stream);
   stream = s;
   own_stream = false;
@@ -512,7 +530,7 @@ void Core::build_plan(const double* nodes_colmajor) {
   // ---- work items: runs of cells inside one tile, <= chunk points ---------
   // items (CTAs) per pass: enough to fill every SM several times over; small
   // problems get short items (their cost is the serial staging chain)
-  int64_t target_items = 16 * 148;
+  int64_t target_items = n_local < 300000 ? 16 * 148 : 4 * 148;
   if (const char* e = std::getenv("FGS_ITEM_TARGET")) target_items = std::max<int64_t>(1, std::atoll(e));
   int chunk = static_cast<int>(std::max<int64_t>(32, std::min<int64_t>(4096, (n_local + target_items - 1) / target_items)));
   chunk = (chunk + 31) / 32 * 32;
@@ -839,6 +857,53 @@ void Core::launch_assemble(Workspace& w, int nvec) {
 
 void Core::apply(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec, bool caller_order,
                  bool scale_input) {
+  // Steady-state applies replay a CUDA graph of the whole launch sequence
+  // (spread, assemble, cuFFT, multiply/exchange, cuFFT, interpolation), keyed
+  // by the call's arguments: one launch instead of ~10 host launches.
+  static const bool graphs_on = [] {
+    const char* e = std::getenv("FGS_GRAPHS");
+    return !(e && std::string(e) == "0");
+  }();
+  if (!graphs_on || profile_ || stream == nullptr || epilogue == EPI_DEGREE) {
+    apply_launches(epilogue, x, ldx, y, ldy, nvec, caller_order, scale_input);
+    return;
+  }
+  const GraphKey key{epilogue, x, ldx, y, ldy, nvec, caller_order, scale_input};
+  for (auto& g : graphs_) {
+    if (g.key == key) {
+      FGS_CUDA(cudaGraphLaunch(g.exec, stream));
+      launches += g.launches;
+      return;
+    }
+  }
+  workspace(nvec);  // allocate / plan outside the capture
+  const int64_t before = launches;
+  FGS_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    apply_launches(epilogue, x, ldx, y, ldy, nvec, caller_order, scale_input);
+  } catch (...) {
+    cudaGraph_t broken = nullptr;
+    cudaStreamEndCapture(stream, &broken);
+    if (broken) cudaGraphDestroy(broken);
+    throw;
+  }
+  cudaGraph_t graph = nullptr;
+  FGS_CUDA(cudaStreamEndCapture(stream, &graph));
+  cudaGraphExec_t exec = nullptr;
+  FGS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  if (graphs_.size() >= 8) {
+    cudaGraphExecDestroy(graphs_.front().exec);
+    graphs_.erase(graphs_.begin());
+  }
+  graphs_.push_back({key, exec, launches - before});
+  launches = before;
+  FGS_CUDA(cudaGraphLaunch(exec, stream));
+  launches += graphs_.back().launches;
+}
+
+void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
+                          bool caller_order, bool scale_input) {
   Workspace& w = workspace(nvec);
   PassArgs a{};
   a.items = items.p;

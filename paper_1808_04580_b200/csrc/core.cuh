@@ -132,6 +132,27 @@ class Core {
 
  private:
   std::map<int, std::unique_ptr<Workspace>> ws_;
+  struct GraphKey {
+    int epi;
+    const double* x;
+    int64_t ldx;
+    double* y;
+    int64_t ldy;
+    int nvec;
+    bool caller_order, scale;
+    bool operator==(const GraphKey& o) const {
+      return epi == o.epi && x == o.x && ldx == o.ldx && y == o.y && ldy == o.ldy && nvec == o.nvec &&
+             caller_order == o.caller_order && scale == o.scale;
+    }
+  };
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    int64_t launches;
+  };
+  std::vector<GraphEntry> graphs_;
+  void apply_launches(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
+                      bool caller_order, bool scale_input);
   bool profile_ = false;
   std::vector<cudaEvent_t> ev_pool_;
   std::vector<std::vector<cudaEvent_t>> ev_pending_;

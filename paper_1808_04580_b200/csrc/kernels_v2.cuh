@@ -276,6 +276,15 @@ __global__ void __launch_bounds__(Blk<D, T>::NT) interp_v2_kernel(PassArgs a, in
       const double* sb = stg + buf * QS * TAPS;
       for (int64_t b0 = c0; b0 < c1; b0 += QB) {
         const int qb = static_cast<int>(lmin(QB, c1 - b0));
+        // prefetch this thread's epilogue operands (their latency hides under the batch)
+        int64_t eix = 0;
+        double exin = 0.0, esin = 1.0;
+        if (tid < qb) {
+          const int64_t ip = b0 + tid;
+          eix = a.perm ? static_cast<int64_t>(a.perm[ip]) : ip;
+          if (xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE) exin = xv[eix];
+          if (a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN) esin = a.s[ip];
+        }
         double p[QB];
 #pragma unroll
         for (int i = 0; i < QB; ++i) p[i] = 0.0;
@@ -330,14 +339,20 @@ __global__ void __launch_bounds__(Blk<D, T>::NT) interp_v2_kernel(PassArgs a, in
 #pragma unroll
           for (int w = 0; w < NW; ++w) val += rbuf[w * QB + tid];
           const int64_t ip = b0 + tid;
-          const int64_t ix = a.perm ? static_cast<int64_t>(a.perm[ip]) : ip;
           if (a.epilogue == EPI_DEGREE) {
             const double dg = val - a.k0;  // graphop.cpp:55-56
             a.degrees[ip] = dg;
             a.inv_sqrt[ip] = 1.0 / sqrt(dg);
             if (!(dg > 0.0)) atomicMin(a.bad_flag, static_cast<unsigned long long>(a.caller[ip]));
           } else {
-            yv[ix] = epilogue(a, val, ip, ix, xv);
+            double out;
+            switch (a.epilogue) {
+              case EPI_KERNEL: out = val; break;
+              case EPI_WEIGHT: out = val - a.k0 * exin; break;
+              case EPI_NORMALIZED: out = esin * (val - a.k0 * __dmul_rn(esin, exin)); break;
+              default: out = exin - esin * (val - a.k0 * __dmul_rn(esin, exin)); break;
+            }
+            yv[eix] = out;
           }
         }
         rb ^= 1;  // the next batch writes the other red buffer: no second barrier

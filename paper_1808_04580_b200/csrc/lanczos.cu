@@ -10,6 +10,8 @@
 // reproducible.  Sharded runs add one NCCL allreduce per reduction.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <numeric>
@@ -244,9 +246,10 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   for (int64_t p = 0; p < nl; ++p) local[static_cast<size_t>(p)] = start[static_cast<size_t>(c.host_perm[static_cast<size_t>(c.offset + p)])] / sn;
 
   int64_t cap = std::min<int64_t>(n, 64);
-  DBuf<double> basis, z, partial, hbuf, scal;
+  DBuf<double> basis, z, partial, hbuf, scal, qin;
   basis.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)) * cap);
   z.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)));
+  qin.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)));  // fixed apply input -> graph-cached apply
   const int nblk = std::max(1, ceil_div(nl, kRowsPerBlock));
   hbuf.alloc(static_cast<size_t>(std::min<int64_t>(n, max_iter) + 2));
   partial.alloc(static_cast<size_t>(nblk) * (std::min<int64_t>(n, max_iter) + 2));
@@ -297,11 +300,18 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   for (auto& e : ev) FGS_CUDA(cudaEventCreate(&e));
   double apply_ms = 0.0, reorth_ms = 0.0;
   const auto wall0 = std::chrono::steady_clock::now();
+  static const bool trace = std::getenv("FGS_LANCZOS_TRACE") != nullptr;
+  auto now_ms = [] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  double t_launch = 0.0, t_sync = 0.0, t_tri = 0.0, t_tail = 0.0;
   while (true) {
     const int m = static_cast<int>(alphas.size()) + 1;
     const double* qcur = basis.p + static_cast<int64_t>(m - 1) * nl;
+    const double h0 = now_ms();
     FGS_CUDA(cudaEventRecord(ev[0], st));
-    c.apply(epi, qcur, nl, z.p, nl, 1, false, true);
+    FGS_CUDA(cudaMemcpyAsync(qin.p, qcur, sizeof(double) * nl, cudaMemcpyDeviceToDevice, st));
+    c.apply(epi, qin.p, nl, z.p, nl, 1, false, true);
     FGS_CUDA(cudaEventRecord(ev[1], st));
     ++iterations;
     // alpha = q . z
@@ -314,9 +324,13 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     cgs_pass(m, z.p);
     multidot(z.p, 1, z.p, scal.p + 1);
     FGS_CUDA(cudaEventRecord(ev[2], st));
+    const double h1 = now_ms();
     double ab[2];
     FGS_CUDA(cudaMemcpyAsync(ab, scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     FGS_CUDA(cudaStreamSynchronize(st));
+    const double h2 = now_ms();
+    t_launch += h1 - h0;
+    t_sync += h2 - h1;
     {
       float t01 = 0.f, t12 = 0.f;
       FGS_CUDA(cudaEventElapsedTime(&t01, ev[0], ev[1]));
@@ -329,6 +343,7 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     scale = std::max(scale, std::abs(alpha) + beta + beta_prev);
 
     const bool last = iterations >= max_iter || m == static_cast<int>(n);
+    const double h3 = now_ms();
     if (m >= k && (m >= next_check || last)) {  // spectral.cpp:200-215
       solve_tri(m);
       bool all_small = true;
@@ -358,6 +373,8 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
       std::swap(basis.n, nb.n);
       cap = ncap;
     }
+    const double h4 = now_ms();
+    t_tri += h4 - h3;
     double* qnext = basis.p + static_cast<int64_t>(m) * nl;
     if (beta > 1e-14 * std::max(scale, 1.0)) {
       betas.push_back(beta);
@@ -392,6 +409,13 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   }
 
   for (auto& e : ev) cudaEventDestroy(e);
+  if (trace)
+    std::fprintf(stderr,
+                 "[lanczos] iters %d  device apply %.2f ms  reorth %.2f ms | host launch %.2f ms  sync-wait %.2f ms  "
+                 "tridiag %.2f ms  loop wall %.2f ms\n",
+                 iterations, apply_ms, reorth_ms, t_launch, t_sync, t_tri,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count());
+  (void)t_tail;
   const int m = static_cast<int>(alphas.size());
   if (tri_size != m) solve_tri(m);
   const int wanted = std::min(k, m);
