@@ -16,6 +16,7 @@
 #include "kernels_v2.cuh"
 #include "kernels_v3.cuh"
 #include "kernels_v4.cuh"
+#include "conv2d.cuh"
 #include "nccl_shim.hpp"
 
 namespace fgsb {
@@ -409,6 +410,14 @@ Core::Core(const double* nodes_colmajor, int64_t n_, int d_, Kind kind_, const K
 
   build_plan(nodes_colmajor);
   if (kind == FASTSUM) build_coefficients();
+  if (kind == FASTSUM && d == 2) {  // twiddles e^{-2 pi i j / M} for the pruned 2-D convolution
+    std::vector<double2> tw(static_cast<size_t>(M));
+    for (int j = 0; j < M; ++j) {
+      const double ang = 2.0 * kPi * static_cast<double>(j) / M;
+      tw[static_cast<size_t>(j)] = make_double2(std::cos(ang), -std::sin(ang));
+    }
+    tw2.upload(tw.data(), tw.size(), stream);
+  }
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
@@ -798,6 +807,7 @@ Workspace& Core::workspace(int nvec) {
   w->grid.alloc(static_cast<size_t>(grid_elems) * nvec);
   w->spec.alloc(static_cast<size_t>(spec_elems) * nvec);
   if (world > 1) w->window.alloc(static_cast<size_t>(window_elems) * nvec);
+  if (use_conv2d()) w->cgrid.alloc(static_cast<size_t>(M) * (N / 2 + 1) * nvec);
   int dims[3] = {M, M, M};
   FGS_CUFFT(cufftPlanMany(&w->r2c, d, dims, nullptr, 1, static_cast<int>(grid_elems), nullptr, 1,
                           static_cast<int>(spec_elems), CUFFT_D2Z, nvec));
@@ -936,28 +946,42 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
   if (profile_) mark(evs);
   launch_assemble(w, nvec);
   if (profile_) mark(evs);
-  FGS_CUFFT(cufftExecD2Z(w.r2c, w.grid.p, w.spec.p));
-  if (profile_) mark(evs);
-  if (world == 1) {
-    MultiplyArgs ma{w.spec.p, mult.p, spec_elems, spec_elems, nvec, d, M, N};
-    multiply_kernel<<<ceil_div(spec_elems, 256), 256, 0, stream>>>(ma);
-    ++launches;
+  if (use_conv2d()) {
+    // d = 2: pruned direct-DFT convolution over the (N+1)(N/2+1) window
+    const int H = N / 2 + 1;
+    Conv2Args ca{w.grid.p, w.grid.p, w.cgrid.p, mult.p, tw2.p, M, N, nvec, grid_elems, static_cast<int64_t>(M) * H};
+    conv2_rows_fwd<<<dim3(M, nvec), kConvThreads, sizeof(double2) * M + sizeof(double) * M, stream>>>(ca);
+    if (profile_) mark(evs);
+    conv2_cols<<<dim3(H, nvec), kConvThreads, sizeof(double2) * (2 * M + N + 1), stream>>>(ca);
+    if (profile_) mark(evs);
+    conv2_rows_inv<<<dim3(M, nvec), kConvThreads, sizeof(double2) * (M + H), stream>>>(ca);
+    launches += 3;
     FGS_CUDA(cudaGetLastError());
+    if (profile_) mark(evs);
   } else {
-    WindowArgs wa{w.spec.p, w.window.p, mult.p, spec_elems, window_elems, window_elems, nvec, d, M, N};
-    pack_window_kernel<<<ceil_div(window_elems, 256), 256, 0, stream>>>(wa);
-    ++launches;
-    nccl_check(nccl().all_reduce(w.window.p, w.window.p, static_cast<size_t>(window_elems) * nvec * 2, ncclDouble,
-                                 ncclSum, comm, stream),
-               "ncclAllReduce of the truncated spectrum");
-    FGS_CUDA(cudaMemsetAsync(w.spec.p, 0, sizeof(cufftDoubleComplex) * spec_elems * nvec, stream));
-    unpack_multiply_kernel<<<ceil_div(window_elems, 256), 256, 0, stream>>>(wa);
-    ++launches;
-    FGS_CUDA(cudaGetLastError());
+    FGS_CUFFT(cufftExecD2Z(w.r2c, w.grid.p, w.spec.p));
+    if (profile_) mark(evs);
+    if (world == 1) {
+      MultiplyArgs ma{w.spec.p, mult.p, spec_elems, spec_elems, nvec, d, M, N};
+      multiply_kernel<<<ceil_div(spec_elems, 256), 256, 0, stream>>>(ma);
+      ++launches;
+      FGS_CUDA(cudaGetLastError());
+    } else {
+      WindowArgs wa{w.spec.p, w.window.p, mult.p, spec_elems, window_elems, window_elems, nvec, d, M, N};
+      pack_window_kernel<<<ceil_div(window_elems, 256), 256, 0, stream>>>(wa);
+      ++launches;
+      nccl_check(nccl().all_reduce(w.window.p, w.window.p, static_cast<size_t>(window_elems) * nvec * 2, ncclDouble,
+                                   ncclSum, comm, stream),
+                 "ncclAllReduce of the truncated spectrum");
+      FGS_CUDA(cudaMemsetAsync(w.spec.p, 0, sizeof(cufftDoubleComplex) * spec_elems * nvec, stream));
+      unpack_multiply_kernel<<<ceil_div(window_elems, 256), 256, 0, stream>>>(wa);
+      ++launches;
+      FGS_CUDA(cudaGetLastError());
+    }
+    if (profile_) mark(evs);
+    FGS_CUFFT(cufftExecZ2D(w.c2r, w.spec.p, w.grid.p));
+    if (profile_) mark(evs);
   }
-  if (profile_) mark(evs);
-  FGS_CUFFT(cufftExecZ2D(w.c2r, w.spec.p, w.grid.p));
-  if (profile_) mark(evs);
   launch_interp(a);
   if (profile_) {
     mark(evs);
@@ -997,6 +1021,16 @@ void Core::read_profile(double* ms, int64_t* applies) {
   }
   if (applies) *applies = static_cast<int64_t>(ev_pending_.size());
   ev_pending_.clear();
+}
+
+// opt-in (FGS_CONV2D=1): at C2 size (M = 128) its three latency-bound launches
+// measured no faster than cuFFT D2Z + multiply + Z2D (32.5 vs 32.9 us)
+bool Core::use_conv2d() const {
+  static const bool on = [] {
+    const char* e = std::getenv("FGS_CONV2D");
+    return e && std::string(e) == "1";
+  }();
+  return on && d == 2 && world == 1 && kind == FASTSUM && M <= 1024 && tw2.p != nullptr;
 }
 
 void Core::compute_degrees(int64_t* bad_node) {

@@ -91,6 +91,8 @@ class Core {
   DBuf<int> asm_ptr, asm_idx;  // grid cell -> private-box entries (CSR, item order)
   DBuf<cufftDoubleComplex> mult;  // compact Hermitian multiplier (FASTSUM)
   DBuf<double> deconv_d;
+  DBuf<double2> tw2;  // d = 2 pruned-convolution twiddles
+  bool use_conv2d() const;
   int nitems = 0;
   double mean_run = 0.0;  // points per run (cell piece) of this shard: picks the spread kernel
   int64_t box_stride = 0;
