@@ -466,7 +466,10 @@ def lanczos_largest(op: AdjacencyOperator, k: int, opts: LanczosOptions = None, 
     if info is not None:
         info.iterations, info.converged = it.value, bool(conv.value)
     c = cnt.value
-    return EigenPairs(values[:c].copy(), vectors[:, :c].copy() if want_vectors else None)
+    vecs = None
+    if want_vectors:
+        vecs = vectors if c == vectors.shape[1] else vectors[:, :c].copy()
+    return EigenPairs(values[:c].copy(), vecs)
 
 
 def adjacency_to_laplacian(pairs: EigenPairs) -> EigenPairs:

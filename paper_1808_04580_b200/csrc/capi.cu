@@ -489,21 +489,8 @@ fgs_status fgs_lanczos_largest(fgs_adjacency_t h, int which, int k, int max_iter
                      [&](int a, int b) { return r.values[static_cast<size_t>(a)] > r.values[static_cast<size_t>(b)]; });
     for (int i = 0; i < cnt; ++i) values[i] = r.values[static_cast<size_t>(order[static_cast<size_t>(i)])];
     if (vectors) {
-      const int64_t n = c.n;
-      std::vector<double> col(static_cast<size_t>(n));
-      for (int i = 0; i < cnt; ++i) {
-        const double* src = r.local_vectors.data() + static_cast<int64_t>(order[static_cast<size_t>(i)]) * n;
-        for (int64_t p = 0; p < n; ++p) col[static_cast<size_t>(c.host_perm[static_cast<size_t>(p)])] = src[p];
-        int64_t at = 0;
-        double best = -1.0;
-        for (int64_t r2 = 0; r2 < n; ++r2)
-          if (std::abs(col[static_cast<size_t>(r2)]) > best) {
-            best = std::abs(col[static_cast<size_t>(r2)]);
-            at = r2;
-          }
-        const double sgn = col[static_cast<size_t>(at)] < 0.0 ? -1.0 : 1.0;
-        for (int64_t r2 = 0; r2 < n; ++r2) vectors[static_cast<int64_t>(i) * n + r2] = sgn * col[static_cast<size_t>(r2)];
-      }
+      std::vector<int> ord(order.begin(), order.end());
+      fgsb::lanczos_finish_vectors(c, r, ord, vectors);
     }
     if (count) *count = cnt;
     if (iterations) *iterations = r.iterations;

@@ -82,16 +82,91 @@ __global__ void __launch_bounds__(kRedThreads) multidot_kernel(const double* __r
   }
 }
 
-// out[j] = scale_sign * sum_b partial[b][j]  (ordered); optional sqrt
+// out[j] = sum_b partial[b][j]: one warp per column, lanes take block
+// residues mod 32 in increasing order, then a fixed shuffle tree
+// (deterministic; the serial per-column loop cost ~0.5 ms at n = 2M)
 __global__ void reduce_partials_kernel(const double* __restrict__ partial, int nblocks, int m,
                                        double* __restrict__ out, int take_sqrt) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (j >= m) return;
   double s = 0.0;
-  for (int b = 0; b < nblocks; ++b) s += partial[static_cast<int64_t>(b) * m + j];
-  out[j] = take_sqrt ? sqrt(s) : s;
+  for (int b = lane; b < nblocks; b += 32) s += partial[static_cast<int64_t>(b) * m + j];
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+  if (lane == 0) out[j] = take_sqrt ? sqrt(s) : s;
 }
 
+// column-wise first index of the largest |v| (make_eigenpairs' convention,
+// spectral.cpp:120-124): per block (max, first index), then ordered fold
+__global__ void colmax_partial_kernel(const double* __restrict__ V, int64_t ldv, int64_t n, int chunk,
+                                      double* __restrict__ pval, int64_t* __restrict__ pidx) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  const int col = blockIdx.y;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t r1 = r0 + chunk < n ? r0 + chunk : n;
+  double best = -1.0;
+  int64_t bi = -1;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const double v = fabs(V[col * ldv + r]);
+    if (v > best) {
+      best = v;
+      bi = r;
+    }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double v2 = sv[threadIdx.x + s];
+      const int64_t i2 = si[threadIdx.x + s];
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 >= 0 && (si[threadIdx.x] < 0 || i2 < si[threadIdx.x]))) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pval[static_cast<int64_t>(col) * gridDim.x + blockIdx.x] = sv[0];
+    pidx[static_cast<int64_t>(col) * gridDim.x + blockIdx.x] = si[0];
+  }
+}
+
+// sign[col] = -1 if V[first argmax |.|] < 0; then V[:, col] *= sign
+__global__ void colsign_kernel(double* __restrict__ V, int64_t ldv, int64_t n, const double* __restrict__ pval,
+                               const int64_t* __restrict__ pidx, int nparts) {
+  const int col = blockIdx.y;
+  __shared__ double sgn;
+  if (threadIdx.x == 0) {
+    double best = -1.0;
+    int64_t bi = 0;
+    for (int p = 0; p < nparts; ++p) {  // parts in row order: first index wins ties
+      const double v = pval[static_cast<int64_t>(col) * nparts + p];
+      if (v > best) {
+        best = v;
+        bi = pidx[static_cast<int64_t>(col) * nparts + p];
+      }
+    }
+    sgn = (n > 0 && V[col * ldv + bi] < 0.0) ? -1.0 : 1.0;
+  }
+  __syncthreads();
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    V[col * ldv + r] *= sgn;
+}
+
+__global__ void unpermute_cols_kernel(const double* __restrict__ Vi, int64_t ldi, double* __restrict__ Vc,
+                                      int64_t ldc, const int* __restrict__ perm, const int* __restrict__ order,
+                                      int64_t n) {
+  const int col = blockIdx.y;
+  const int src = order[col];
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    Vc[col * ldc + perm[r]] = Vi[src * ldi + r];
+}
 
 // z[r] -= sum_j Q[r, j] * h[j]   (the GEMV of one CGS pass, spectral.cpp:195)
 __global__ void update_kernel(const double* __restrict__ Q, int64_t ldq, int m, const double* __restrict__ h,
@@ -264,7 +339,7 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   // out[0..m) = Q[:, 0..m)^T v  (global, fixed order)
   auto multidot = [&](const double* Q, int m, const double* v, double* out) {
     multidot_kernel<<<nblk, kRedThreads, 0, st>>>(Q, nl, m, v, nl, partial.p);
-    reduce_partials_kernel<<<ceil_div(m, 128), 128, 0, st>>>(partial.p, nblk, m, out, 0);
+    reduce_partials_kernel<<<ceil_div(m, 8), 256, 0, st>>>(partial.p, nblk, m, out, 0);
     c.launches += 2;
     allreduce(out, m);
   };
@@ -433,20 +508,43 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
       S[static_cast<size_t>(j) * wanted + i] = tvecs[static_cast<size_t>(m - 1 - i) * m + j];
   }
   if (want_vectors) {
-    DBuf<double> dS, V;
+    DBuf<double> dS;
     dS.upload(S.data(), S.size(), st);
-    V.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)) * wanted);
+    res.vectors_dev.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)) * wanted);
     for (int c0 = 0; c0 < wanted; c0 += 8) {
-      ritz_kernel<8><<<ceil_div(std::max<int64_t>(nl, 1), 128), 128, 0, st>>>(basis.p, nl, m, dS.p, wanted, c0, V.p,
-                                                                             nl, nl);
+      ritz_kernel<8><<<ceil_div(std::max<int64_t>(nl, 1), 128), 128, 0, st>>>(basis.p, nl, m, dS.p, wanted, c0,
+                                                                             res.vectors_dev.p, nl, nl);
       ++c.launches;
     }
-    res.local_vectors.resize(static_cast<size_t>(nl) * wanted);
-    FGS_CUDA(cudaMemcpyAsync(res.local_vectors.data(), V.p, sizeof(double) * nl * wanted, cudaMemcpyDeviceToHost, st));
   }
   FGS_CUDA(cudaStreamSynchronize(st));
   FGS_CUDA(cudaGetLastError());
   return res;
+}
+
+void lanczos_finish_vectors(Core& c, LanczosResult& r, const std::vector<int>& order, double* host_out) {
+  const int64_t n = c.n;
+  const int cnt = static_cast<int>(order.size());
+  if (cnt == 0) return;
+  cudaStream_t st = c.stream;
+  DBuf<int> dorder;
+  dorder.upload(order.data(), order.size(), st);
+  DBuf<double> Vc;
+  Vc.alloc(static_cast<size_t>(n) * cnt);
+  const int gx = std::max(1, std::min(ceil_div(n, 256), 4096));
+  unpermute_cols_kernel<<<dim3(gx, cnt), 256, 0, st>>>(r.vectors_dev.p, n, Vc.p, n, c.perm.p, dorder.p, n);
+  const int chunk = 1 << 16;
+  const int parts = std::max(1, ceil_div(n, chunk));
+  DBuf<double> pval;
+  DBuf<int64_t> pidx;
+  pval.alloc(static_cast<size_t>(parts) * cnt);
+  pidx.alloc(static_cast<size_t>(parts) * cnt);
+  colmax_partial_kernel<<<dim3(parts, cnt), 256, 0, st>>>(Vc.p, n, n, chunk, pval.p, pidx.p);
+  colsign_kernel<<<dim3(gx, cnt), 256, 0, st>>>(Vc.p, n, n, pval.p, pidx.p, parts);
+  c.launches += 3;
+  FGS_CUDA(cudaMemcpyAsync(host_out, Vc.p, sizeof(double) * n * cnt, cudaMemcpyDeviceToHost, st));
+  FGS_CUDA(cudaStreamSynchronize(st));
+  FGS_CUDA(cudaGetLastError());
 }
 
 }  // namespace fgsb
