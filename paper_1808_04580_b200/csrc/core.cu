@@ -192,6 +192,10 @@ template <int D, int T>
 constexpr bool has_v3() {
   return D == 3 && (T == 8 || T == 12 || T == 16);
 }
+template <int D, int T>
+constexpr bool has_v4_2d() {
+  return D == 2 && (T == 8 || T == 12 || T == 16);
+}
 bool use_v3() {
   static const bool v3 = kernel_env("v3");
   return v3;
@@ -234,8 +238,15 @@ LaunchShape shape_t(bool dense) {
     using B4i = Blk4<T, true>;
     using B4s = Blk4<T, false>;
     if (use_v4()) {
-      interp = 2 * static_cast<size_t>(B4i::QS) * B4i::TAPS + static_cast<size_t>(B4i::P) * B4i::G * 8;
-      if (dense) spread = 2 * static_cast<size_t>(B4s::QS) * B4s::TAPS + 2 * B4s::QS;
+      interp = 2 * static_cast<size_t>(B4i::QS) * B4i::STRIDE + static_cast<size_t>(B4i::P) * B4i::G * 8;
+      if (dense) spread = 2 * static_cast<size_t>(B4s::QS) * B4s::STRIDE + 2 * B4s::QS;
+    }
+  }
+  if constexpr (has_v4_2d<D, T>()) {
+    using B4 = Blk4d2<T>;
+    if (use_v4()) {
+      interp = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE;
+      if (dense) spread = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE + 2 * B4::QS;
     }
   }
   return {B::NT, spread, interp};
@@ -275,6 +286,34 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
     return;
   }
   constexpr int NT = Blk<D, T>::NT;
+  if constexpr (has_v4_2d<D, T>()) {
+    if (use_v4() && (interp || dense)) {
+      if (interp) {
+        auto k = interp_v4_2d_kernel<T>;
+        set_smem(reinterpret_cast<const void*>(k), smem);
+        k<<<nitems, Blk4d2<T>::NT, smem, s>>>(a, box_stride);
+      } else {
+        static const int ps = [] {
+          const char* e = std::getenv("FGS_SPREAD2D_P");
+          return e ? std::atoi(e) : 1;
+        }();
+        if (ps == 4) {
+          auto k = spread_v4_2d_kernel<T, 4>;
+          set_smem(reinterpret_cast<const void*>(k), smem);
+          k<<<nitems, Blk4d2<T, 4>::NT, smem, s>>>(a, box_stride);
+        } else if (ps == 2) {
+          auto k = spread_v4_2d_kernel<T, 2>;
+          set_smem(reinterpret_cast<const void*>(k), smem);
+          k<<<nitems, Blk4d2<T, 2>::NT, smem, s>>>(a, box_stride);
+        } else {
+          auto k = spread_v4_2d_kernel<T, 1>;
+          set_smem(reinterpret_cast<const void*>(k), smem);
+          k<<<nitems, Blk4d2<T, 1>::NT, smem, s>>>(a, box_stride);
+        }
+      }
+      return;
+    }
+  }
   if constexpr (has_v3<D, T>()) {
     if (use_v4() && (interp || dense)) {
       if (interp) {

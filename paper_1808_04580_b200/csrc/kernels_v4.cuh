@@ -49,7 +49,24 @@ struct Blk4 {
   static constexpr int NT = 32 * G * P;
   static constexpr int QS = 32;              // points per staged chunk
   static constexpr int TAPS = 3 * T;
+  // staged row stride: = 4 or 12 (mod 16 doubles) so the 4 (spread) or 8
+  // (interp) points a warp reads per LDS fall on distinct bank pairs; 2m = 16
+  // rows of 48 doubles all started on the same bank (ncu: 9e9 conflicts, C5)
+  static constexpr int STRIDE = (TAPS % 16 == 4 || TAPS % 16 == 12) ? TAPS
+                              : (TAPS % 16 == 0 ? TAPS + 4 : TAPS + ((12 - TAPS % 16 + 16) % 16));
 };
+
+// cp.async a chunk of q points' taps into rows of STRIDE doubles
+template <int TAPS, int STRIDE>
+__device__ __forceinline__ void v4_issue_chunk(double* buf, const double* taps, int64_t p, int q, int tid, int nt) {
+  constexpr int H = TAPS / 2;  // 16-byte pieces per point
+  const double* src = taps + p * TAPS;
+  const int n16 = q * H;
+  for (int k = tid; k < n16; k += nt) {
+    const int pt = k / H, r = k - pt * H;
+    cp_async16(buf + pt * STRIDE + 2 * r, src + 2 * k);
+  }
+}
 
 // ---------------------------------------------------------------------------
 // interpolation.  smem: box | stage[2][QS*TAPS] | red[P][G][8]
@@ -57,12 +74,12 @@ struct Blk4 {
 template <int T>
 __global__ void __launch_bounds__(Blk4<T, true>::NT) interp_v4_kernel(PassArgs a, int box_stride_smem) {
   using B = Blk4<T, true>;
-  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, G = B::G, P = B::P;
+  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, G = B::G, P = B::P, SR = B::STRIDE;
   constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, KS = B::KS;
   extern __shared__ __align__(16) double smem[];
   double* S = smem;
   double* stg = smem + box_stride_smem;
-  double* red = stg + 2 * QS * TAPS;
+  double* red = stg + 2 * QS * SR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = warp / G, wg = warp % G;
   const int q = lane & 3, r8 = lane >> 2;
@@ -80,7 +97,7 @@ __global__ void __launch_bounds__(Blk4<T, true>::NT) interp_v4_kernel(PassArgs a
     const double* gv = a.grid + vec * a.grid_stride;
     const double* xv = a.x ? a.x + vec * a.ldx : nullptr;
     double* yv = a.y ? a.y + vec * a.ldy : nullptr;
-    v2_issue_chunk<TAPS>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
+    v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
     cp_async_commit();
     for (int v = tid; v < V; v += NT) {
       const int x2 = v % bx2, x1 = (v / bx2) % bx1, x0 = v / (bx2 * bx1);
@@ -98,14 +115,14 @@ __global__ void __launch_bounds__(Blk4<T, true>::NT) interp_v4_kernel(PassArgs a
       cp_async_wait_0();
       __syncthreads();
       if (k + 1 < nch) {
-        v2_issue_chunk<TAPS>(stg + (buf ^ 1) * QS * TAPS, a.taps, c1, static_cast<int>(lmin(QS, p_end - c1)), tid, NT);
+        v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, static_cast<int>(lmin(QS, p_end - c1)), tid, NT);
         cp_async_commit();
       }
-      const double* sb = stg + buf * QS * TAPS;
+      const double* sb = stg + buf * QS * SR;
       for (int64_t b0 = c0 + 8 * grp; b0 < c1; b0 += 8 * P) {
         const int64_t ipt = b0 + r8;  // this lane's point (C rows / A rows)
         const bool in_chunk = ipt < c1;
-        const double* w = sb + (in_chunk ? (ipt - c0) : 0) * TAPS;
+        const double* w = sb + (in_chunk ? (ipt - c0) : 0) * SR;
         // epilogue operands prefetch (lanes q == 0 of warp 0 of the group)
         double xin = 0.0, sin_ = 1.0;
         int64_t ix = 0;
@@ -215,12 +232,12 @@ __global__ void __launch_bounds__(Blk4<T, true>::NT) interp_v4_kernel(PassArgs a
 template <int T>
 __global__ void __launch_bounds__(Blk4<T, false>::NT) spread_v4_kernel(PassArgs a, int box_stride_smem) {
   using B = Blk4<T, false>;
-  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P;
+  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE;
   constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, NE = B::NE;
   extern __shared__ __align__(16) double smem[];
   double* S = smem;
   double* stg = smem + box_stride_smem;
-  double* xs = stg + 2 * QS * TAPS;
+  double* xs = stg + 2 * QS * SR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = warp / B::G, wg = warp % B::G;
   const int q = lane & 3, r8 = lane >> 2;
@@ -236,7 +253,7 @@ __global__ void __launch_bounds__(Blk4<T, false>::NT) spread_v4_kernel(PassArgs 
   for (int vec = 0; vec < a.nvec; ++vec) {
     const double* xv = a.x + vec * a.ldx;
     for (int v = tid; v < V; v += NT) S[v] = 0.0;
-    v2_issue_chunk<TAPS>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
+    v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
     cp_async_commit();
     if (tid < QS && p_begin + tid < p_end) xs[tid] = v2_x(a, xv, p_begin + tid);
     int r = it.run_begin;
@@ -282,11 +299,11 @@ __global__ void __launch_bounds__(Blk4<T, false>::NT) spread_v4_kernel(PassArgs 
       int qn = 0;
       if (more) {
         qn = static_cast<int>(lmin(QS, p_end - c1));
-        v2_issue_chunk<TAPS>(stg + (buf ^ 1) * QS * TAPS, a.taps, c1, qn, tid, NT);
+        v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, qn, tid, NT);
         cp_async_commit();
         if (tid < qn) xnext = v2_x(a, xv, c1 + tid);
       }
-      const double* sb = stg + buf * QS * TAPS;
+      const double* sb = stg + buf * QS * SR;
       const double* xb = xs + buf * QS;
       while (true) {
         const int64_t rs = run.pstart, re_ = static_cast<int64_t>(run.pstart) + run.pcount;
@@ -296,7 +313,7 @@ __global__ void __launch_bounds__(Blk4<T, false>::NT) spread_v4_kernel(PassArgs 
           if (k0 + 4 <= s0) continue;
           const int64_t jp = k0 + q;  // this lane's point of the K-step
           const bool ok = jp >= s0 && jp < s1;
-          const double* w = sb + (ok ? (jp - c0) : 0) * TAPS;
+          const double* w = sb + (ok ? (jp - c0) : 0) * SR;
           const double xj = ok ? xb[jp - c0] : 0.0;
           double wa[TAW], wc[TC];
 #pragma unroll
@@ -318,6 +335,262 @@ __global__ void __launch_bounds__(Blk4<T, false>::NT) spread_v4_kernel(PassArgs 
             for (int t = 0; t < TW; ++t) dmma(C[t][ne][0], C[t][ne][1], af[t], bF[ne]);
         }
         if (re_ <= c1) {  // run ends inside this chunk
+          flush();
+          if (++r >= it.run_end) break;
+          run = a.runs[r];
+          continue;
+        }
+        break;
+      }
+      if (more && tid < qn) xs[(buf ^ 1) * QS + tid] = xnext;
+    }
+    __syncthreads();
+    double* out = a.priv + (static_cast<int64_t>(vec) * gridDim.x + blockIdx.x) * a.box_stride;
+    for (int v = tid; v < V; v += NT) out[v] = S[v];
+    __syncthreads();
+  }
+}
+
+
+// ===========================================================================
+// d = 2 tensor-core variants (2m in {8, 12, 16}).  The footprint is a
+// (2m) x (2m) block g[c][e]:
+//   interp: Z[j][c] = sum_e we_j[e] g[c][e]   M = 8 points, K = e, N = c (padded to 8k)
+//           y_j = sum_c wc_j[c] Z[j][c]
+//   spread: G[c][e] += sum_j (x_j wc_j[c]) we_j[e]   M = c, K = 4 points, N = e
+// One warp per point stream, P streams per CTA, the same chunk / run / flush
+// protocol as the d = 3 kernels above.
+// ===========================================================================
+template <int T, int PS = 4>
+struct Blk4d2 {
+  static constexpr int NC = (T + 7) / 8;  // c tiles (M or N dimension, padded)
+  static constexpr int NE = (T + 7) / 8;  // e tiles (spread N dimension, padded)
+  static constexpr int KS = T / 4;        // interp K-steps over e
+  static constexpr int P = PS;  // point streams (warps) per CTA
+  static constexpr int NT = 32 * P;
+  static constexpr int QS = 32;
+  static constexpr int TAPS = 2 * T;
+  static constexpr int STRIDE = (TAPS % 16 == 4 || TAPS % 16 == 12) ? TAPS
+                              : (TAPS % 16 == 0 ? TAPS + 4 : TAPS + ((12 - TAPS % 16 + 16) % 16));
+};
+
+template <int T>
+__global__ void __launch_bounds__(Blk4d2<T>::NT) interp_v4_2d_kernel(PassArgs a, int box_stride_smem) {
+  using B = Blk4d2<T>;
+  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE, NC = B::NC, KS = B::KS;
+  extern __shared__ __align__(16) double smem[];
+  double* S = smem;
+  double* stg = smem + box_stride_smem;
+  const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
+  const int q = lane & 3, r8 = lane >> 2;
+  const DItem it = a.items[blockIdx.x];
+  const int bx2 = it.e2;
+  const int V = it.e1 * it.e2;
+  const int M = a.M;
+  const int64_t p_begin = a.runs[it.run_begin].pstart;
+  const DRun last = a.runs[it.run_end - 1];
+  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
+
+  for (int vec = 0; vec < a.nvec; ++vec) {
+    const double* gv = a.grid + vec * a.grid_stride;
+    const double* xv = a.x ? a.x + vec * a.ldx : nullptr;
+    double* yv = a.y ? a.y + vec * a.ldy : nullptr;
+    v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
+    cp_async_commit();
+    for (int v = tid; v < V; v += NT) {
+      const int x2 = v % bx2, x1 = v / bx2;
+      S[v] = gv[static_cast<int64_t>((it.a1 + x1) % M) * M + (it.a2 + x2) % M];
+    }
+    int r = it.run_begin;
+    DRun run = a.runs[r];
+    int loaded = -1;
+    double gB[NC][KS];  // B[k = e][n = c]: g[c = 8 nc + lane/4][e = 4 ks + lane%4]
+    for (int k = 0; k < nch; ++k) {
+      const int64_t c0 = p_begin + static_cast<int64_t>(k) * QS;
+      const int64_t c1 = lmin(c0 + QS, p_end);
+      const int buf = k & 1;
+      cp_async_wait_0();
+      __syncthreads();
+      if (k + 1 < nch) {
+        v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, static_cast<int>(lmin(QS, p_end - c1)), tid, NT);
+        cp_async_commit();
+      }
+      const double* sb = stg + buf * QS * SR;
+      for (int64_t b0 = c0 + 8 * grp; b0 < c1; b0 += 8 * P) {
+        const int64_t ipt = b0 + r8;
+        const bool in_chunk = ipt < c1;
+        const double* w = sb + (in_chunk ? (ipt - c0) : 0) * SR;
+        double xin = 0.0, sin_ = 1.0;
+        int64_t ix = 0;
+        if (q == 0 && in_chunk) {
+          ix = a.perm ? static_cast<int64_t>(a.perm[ipt]) : ipt;
+          if (xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE) xin = xv[ix];
+          if (a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN) sin_ = a.s[ipt];
+        }
+        double wc[NC][2];  // c = 8 nc + 2 q + i
+#pragma unroll
+        for (int nc = 0; nc < NC; ++nc)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int cc = 8 * nc + 2 * q + i;
+            wc[nc][i] = cc < T ? w[cc] : 0.0;
+          }
+        double yacc = 0.0;
+        while (true) {
+          while (static_cast<int64_t>(run.pstart) + run.pcount <= b0 && r + 1 < it.run_end) run = a.runs[++r];
+          if (loaded != r) {
+            const int o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+              const int cc = 8 * nc + r8;
+              const double* row = S + (o1 + (cc < T ? cc : 0)) * bx2 + o2 + q;
+#pragma unroll
+              for (int ks = 0; ks < KS; ++ks) gB[nc][ks] = cc < T ? row[4 * ks] : 0.0;
+            }
+            loaded = r;
+          }
+          const int64_t rs = run.pstart, re_ = static_cast<int64_t>(run.pstart) + run.pcount;
+          const bool mine = in_chunk && ipt >= rs && ipt < re_;
+          double aF[KS];
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) aF[ks] = mine ? w[T + 4 * ks + q] : 0.0;
+#pragma unroll
+          for (int nc = 0; nc < NC; ++nc) {
+            double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) dmma(z0, z1, aF[ks], gB[nc][ks]);
+            yacc = fma(wc[nc][0], z0, yacc);
+            yacc = fma(wc[nc][1], z1, yacc);
+          }
+          if (re_ < lmin(b0 + 8, c1) && r + 1 < it.run_end) {
+            run = a.runs[++r];
+            continue;
+          }
+          break;
+        }
+        yacc += __shfl_xor_sync(0xffffffffu, yacc, 1);
+        yacc += __shfl_xor_sync(0xffffffffu, yacc, 2);
+        if (q == 0 && in_chunk) {
+          const double val = yacc;
+          if (a.epilogue == EPI_DEGREE) {
+            const double dg = val - a.k0;  // graphop.cpp:55-56
+            a.degrees[ipt] = dg;
+            a.inv_sqrt[ipt] = 1.0 / sqrt(dg);
+            if (!(dg > 0.0)) atomicMin(a.bad_flag, static_cast<unsigned long long>(a.caller[ipt]));
+          } else {
+            double out;
+            switch (a.epilogue) {
+              case EPI_KERNEL: out = val; break;
+              case EPI_WEIGHT: out = val - a.k0 * xin; break;
+              case EPI_NORMALIZED: out = sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
+              default: out = xin - sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
+            }
+            yv[ix] = out;
+          }
+        }
+      }
+    }
+    cp_async_wait_0();
+    __syncthreads();
+  }
+}
+
+template <int T, int PS>
+__global__ void __launch_bounds__(Blk4d2<T, PS>::NT) spread_v4_2d_kernel(PassArgs a, int box_stride_smem) {
+  using B = Blk4d2<T, PS>;
+  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE, NC = B::NC, NE = B::NE;
+  extern __shared__ __align__(16) double smem[];
+  double* S = smem;
+  double* stg = smem + box_stride_smem;
+  double* xs = stg + 2 * QS * SR;
+  const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
+  const int q = lane & 3, r8 = lane >> 2;
+  const DItem it = a.items[blockIdx.x];
+  const int bx2 = it.e2;
+  const int V = it.e1 * it.e2;
+  const int64_t p_begin = a.runs[it.run_begin].pstart;
+  const DRun last = a.runs[it.run_end - 1];
+  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
+
+  for (int vec = 0; vec < a.nvec; ++vec) {
+    const double* xv = a.x + vec * a.ldx;
+    for (int v = tid; v < V; v += NT) S[v] = 0.0;
+    v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
+    cp_async_commit();
+    if (tid < QS && p_begin + tid < p_end) xs[tid] = v2_x(a, xv, p_begin + tid);
+    int r = it.run_begin;
+    DRun run = a.runs[r];
+    double C[NC][NE][2];  // C[m = c][n = e]: lane holds c = 8 mc + lane/4, e = 8 ne + 2 (lane%4) + i
+#pragma unroll
+    for (int mc = 0; mc < NC; ++mc)
+#pragma unroll
+      for (int ne = 0; ne < NE; ++ne) C[mc][ne][0] = C[mc][ne][1] = 0.0;
+    auto flush = [&]() {
+      const int o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
+      for (int g = 0; g < P; ++g) {
+        if (g == grp) {
+#pragma unroll
+          for (int mc = 0; mc < NC; ++mc) {
+            const int cc = 8 * mc + r8;
+            double* row = S + (o1 + (cc < T ? cc : 0)) * bx2 + o2;
+#pragma unroll
+            for (int ne = 0; ne < NE; ++ne)
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const int e = 8 * ne + 2 * q + i;
+                if (cc < T && e < T) row[e] += C[mc][ne][i];
+                C[mc][ne][i] = 0.0;
+              }
+          }
+        }
+        __syncthreads();
+      }
+    };
+    for (int k = 0; k < nch; ++k) {
+      const int64_t c0 = p_begin + static_cast<int64_t>(k) * QS;
+      const int64_t c1 = lmin(c0 + QS, p_end);
+      const int buf = k & 1;
+      cp_async_wait_0();
+      __syncthreads();
+      const bool more = k + 1 < nch;
+      double xnext = 0.0;
+      int qn = 0;
+      if (more) {
+        qn = static_cast<int>(lmin(QS, p_end - c1));
+        v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, qn, tid, NT);
+        cp_async_commit();
+        if (tid < qn) xnext = v2_x(a, xv, c1 + tid);
+      }
+      const double* sb = stg + buf * QS * SR;
+      const double* xb = xs + buf * QS;
+      while (true) {
+        const int64_t rs = run.pstart, re_ = static_cast<int64_t>(run.pstart) + run.pcount;
+        const int64_t s0 = rs > c0 ? rs : c0, s1 = lmin(re_, c1);
+        for (int64_t k0 = c0 + 4 * grp; k0 < s1; k0 += 4 * P) {
+          if (k0 + 4 <= s0) continue;
+          const int64_t jp = k0 + q;
+          const bool ok = jp >= s0 && jp < s1;
+          const double* w = sb + (ok ? (jp - c0) : 0) * SR;
+          const double xj = ok ? xb[jp - c0] : 0.0;
+          double af[NC], bF[NE];
+#pragma unroll
+          for (int mc = 0; mc < NC; ++mc) {
+            const int cc = 8 * mc + r8;
+            af[mc] = cc < T ? xj * w[cc] : 0.0;  // x wc
+          }
+#pragma unroll
+          for (int ne = 0; ne < NE; ++ne) {
+            const int e = 8 * ne + r8;
+            bF[ne] = e < T ? w[T + e] : 0.0;  // we
+          }
+#pragma unroll
+          for (int mc = 0; mc < NC; ++mc)
+#pragma unroll
+            for (int ne = 0; ne < NE; ++ne) dmma(C[mc][ne][0], C[mc][ne][1], af[mc], bF[ne]);
+        }
+        if (re_ <= c1) {
           flush();
           if (++r >= it.run_end) break;
           run = a.runs[r];
