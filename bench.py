@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--no-lanczos", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--also", default="4", help="comma list of extra configs measured after the main line "
+                   "(device matvecs/s + Lanczos time-to-k), '' to skip; N=1 only")
     return p.parse_args()
 
 
@@ -194,6 +196,58 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ---- secondary configurations (reported under "also") ----------------------
+def secondary(cfg, steps, dev):
+    """Device matvecs/s and Lanczos time-to-k of another BASELINE config on
+    the same GPU (graph replays, L2 flushed between steps)."""
+    import torch
+    import paper_1808_04580_b200 as fgs
+    info = fgs.workload_info(cfg)
+    nvec = 16 if cfg == 5 else 1
+    X = fgs.workload_nodes(cfg, SEED)
+    n = X.shape[0]
+    t0 = time.perf_counter()
+    op = fgs.AdjacencyOperator(X, fgs.KernelSpec.gaussian(info["sigma"]),
+                               fgs.FastsumParams(info["N"], info["m"], info["p"], 0.0), device=dev)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    op.set_stream(stream.cuda_stream)
+    xh = fgs.workload_vectors(n, nvec, 99)
+    xh = xh if xh.ndim == 2 else xh[:, None]
+    xc = torch.from_numpy(np.asfortranarray(xh).T.copy()).to(f"cuda:{dev}")
+    xi = torch.empty((nvec, n), dtype=torch.float64, device=f"cuda:{dev}")
+    for v in range(nvec):
+        op.permute_device(xc[v].data_ptr(), xi[v].data_ptr(), nvec=1, ld=n, direction=0)
+    yi = torch.empty_like(xi)
+    flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def step():
+        op.apply_device(fgs.OP_SYM_LAPLACIAN, xi.data_ptr(), yi.data_ptr(), nvec=nvec, ld=n, internal_order=True)
+
+    for _ in range(3):
+        step()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for s0, s1 in ev:
+        flush.zero_()
+        s0.record(stream)
+        step()
+        s1.record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    out = {"workload": f"config{cfg}", "n": n, "d": info["d"], "N": info["N"], "m": info["m"], "nvec": nvec,
+           "value": nvec / (ms / 1000.0), "unit": "matvecs/s", "ms_per_step": ms, "setup_s": setup_s}
+    if cfg <= 4:
+        li = fgs.LanczosInfo()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fgs.lanczos_largest(op, info["k"], fgs.LanczosOptions(tol=1e-8, seed=1), li)
+        torch.cuda.synchronize()
+        out["lanczos"] = {"k": info["k"], "tol": 1e-8, "solve_s": time.perf_counter() - t0,
+                          "iterations": li.iterations, "converged": li.converged, "phases": op.lanczos_stats()}
+    return out
+
+
 # ---- B200 arm --------------------------------------------------------------
 def run_b200(args, rank, world, local_rank):
     import torch
@@ -302,6 +356,14 @@ def run_b200(args, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": b / t / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": (b / t / 1e9) / peaks["hbm_gbs"], "traffic": None,
                 "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json)"}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(f"config{args.config}", {}).get(dom)
+        if tr:
+            roof["traffic"] = tr["dram_bytes"] * (nvec if args.config != 5 else 1)
+            roof["traffic_source"] = f"ncu --set full, {tr['source']} ({tr['kernel']}), dram read+write per launch"
+    except (OSError, ValueError):
+        pass
     roof.update({"kernel": dom, "launch_ms": per_launch[dom], "algorithmic_bytes": b, "algorithmic_flops": f,
                  "t_roof_ms": 1e3 * max(t_hbm, t_fp), "frac_of_max_roof": max(t_hbm, t_fp) / t,
                  "stage_ms_per_step": {k: per_launch[k] for k in STAGES}})
@@ -350,6 +412,15 @@ def run_b200(args, rank, world, local_rank):
         cpu = {"value": rate, "unit": "matvecs/s", "cores": 1, "kind": "port", "sample": desc,
                "cpu": cpu_model(), "host_cores": os.cpu_count(), "setup_s": csetup}
 
+    also = []
+    if world == 1 and args.also:
+        for cfg in [int(c) for c in args.also.split(",") if c.strip()]:
+            if cfg != args.config:
+                try:
+                    also.append(secondary(cfg, 10 if cfg != 5 else 2, dev))
+                except Exception as e:  # noqa: BLE001 - report, do not lose the main line
+                    also.append({"workload": f"config{cfg}", "error": str(e)[:200]})
+
     if rank == 0:
         line = {
             "metric": "fp64 Laplacian matvecs/sec", "value": value, "unit": "matvecs/s", "n_gpus": world,
@@ -361,7 +432,7 @@ def run_b200(args, rank, world, local_rank):
                        "parallelism": f"points sharded x{world}" if world > 1 else "single GPU",
                        "l2": "flushed (256 MB write) between timed steps, outside the events"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks.summary(w0, w1), "lanczos": lanczos, "setup_s": setup_s,
+            "clocks": clocks.summary(w0, w1), "lanczos": lanczos, "setup_s": setup_s, "also": also,
         }
         print(json.dumps(line), flush=True)
 

@@ -913,7 +913,8 @@ void Core::apply(int epilogue, const double* x, int64_t ldx, double* y, int64_t 
     const char* e = std::getenv("FGS_GRAPHS");
     return !(e && std::string(e) == "0");
   }();
-  if (!graphs_on || profile_ || stream == nullptr || epilogue == EPI_DEGREE) {
+  // sharded handles launch directly: NCCL inside stream capture is not exercised on this 1-GPU pool
+  if (!graphs_on || profile_ || stream == nullptr || epilogue == EPI_DEGREE || world > 1) {
     apply_launches(epilogue, x, ldx, y, ldy, nvec, caller_order, scale_input);
     return;
   }
