@@ -32,7 +32,6 @@ void validate_params(const Params& p) {  // fastsum.cpp:25-36
 namespace {
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
-inline int round32(int x) { return (x + 31) / 32 * 32; }
 
 // ---- small device kernels of the complex NfftPlan path -------------------
 __global__ void merge_complex_kernel(const double* re, const double* im, cufftDoubleComplex* out, int64_t n) {

@@ -379,7 +379,7 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   auto now_ms = [] {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
   };
-  double t_launch = 0.0, t_sync = 0.0, t_tri = 0.0, t_tail = 0.0;
+  double t_launch = 0.0, t_sync = 0.0, t_tri = 0.0;
   while (true) {
     const int m = static_cast<int>(alphas.size()) + 1;
     const double* qcur = basis.p + static_cast<int64_t>(m - 1) * nl;
@@ -490,7 +490,6 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
                  "tridiag %.2f ms  loop wall %.2f ms\n",
                  iterations, apply_ms, reorth_ms, t_launch, t_sync, t_tri,
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count());
-  (void)t_tail;
   const int m = static_cast<int>(alphas.size());
   if (tri_size != m) solve_tri(m);
   const int wanted = std::min(k, m);
