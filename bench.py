@@ -357,8 +357,8 @@ def run_b200(args, rank, world, local_rank):
                 "frac": (b / t / 1e9) / peaks["hbm_gbs"], "traffic": None,
                 "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json)"}
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(f"config{args.config}", {}).get(dom)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(f"config{args.config}", {}).get(dom)
         if tr:
             roof["traffic"] = tr["dram_bytes"] * (nvec if args.config != 5 else 1)
             roof["traffic_source"] = f"ncu --set full, {tr['source']} ({tr['kernel']}), dram read+write per launch"
