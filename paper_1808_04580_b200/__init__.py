@@ -301,7 +301,7 @@ class AdjacencyOperator:
         h = C.c_void_p()
         bad = C.c_int64(-1)
         cp = params._c()
-        if world > 1:
+        if world > 1 or nccl_id is not None:
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
             st = lib().fgs_adjacency_create_sharded(_dp(nd), C.c_int64(n), int(d), int(kernel.family),
                                                     C.c_double(kernel.shape), C.byref(cp), int(device),

@@ -322,8 +322,8 @@ fgs_status fgs_nccl_unique_id(void* out128) {
 fgs_status fgs_adjacency_create_sharded(const double* nodes, int64_t n, int d, fgs_kernel kernel, double shape,
                                         const fgs_fastsum_params* params, int device, int rank, int world,
                                         const void* nccl_id, fgs_adjacency_t* out, int64_t* bad_node) {
-  if (world > 1 && !nccl_id) {
-    g_err = "nccl_id must not be NULL for world > 1";
+  if (!nccl_id) {
+    g_err = "nccl_id must not be NULL for a sharded handle";
     return FGS_EPARAM;
   }
   return adjacency_create_impl(nodes, n, d, kernel, shape, params, device, rank, world, nccl_id, out, bad_node);

@@ -456,7 +456,8 @@ Core::Core(const double* nodes_colmajor, int64_t n_, int d_, Kind kind_, const K
     }
     tw2.upload(tw.data(), tw.size(), stream);
   }
-  if (world > 1) {
+  if (nccl_id != nullptr) {  // sharded handle (world may be 1: exercises the exchange path)
+    sharded = true;
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
     nccl_check(nccl().comm_init_rank(&comm, world, id, rank), "ncclCommInitRank");
@@ -844,7 +845,7 @@ Workspace& Core::workspace(int nvec) {
   w->priv.alloc(static_cast<size_t>(std::max(nitems, 1)) * box_stride * nvec);
   w->grid.alloc(static_cast<size_t>(grid_elems) * nvec);
   w->spec.alloc(static_cast<size_t>(spec_elems) * nvec);
-  if (world > 1) w->window.alloc(static_cast<size_t>(window_elems) * nvec);
+  if (sharded) w->window.alloc(static_cast<size_t>(window_elems) * nvec);
   if (use_conv2d()) w->cgrid.alloc(static_cast<size_t>(M) * (N / 2 + 1) * nvec);
   int dims[3] = {M, M, M};
   FGS_CUFFT(cufftPlanMany(&w->r2c, d, dims, nullptr, 1, static_cast<int>(grid_elems), nullptr, 1,
@@ -913,7 +914,7 @@ void Core::apply(int epilogue, const double* x, int64_t ldx, double* y, int64_t 
     return !(e && std::string(e) == "0");
   }();
   // sharded handles launch directly: NCCL inside stream capture is not exercised on this 1-GPU pool
-  if (!graphs_on || profile_ || stream == nullptr || epilogue == EPI_DEGREE || world > 1) {
+  if (!graphs_on || profile_ || stream == nullptr || epilogue == EPI_DEGREE || sharded) {
     apply_launches(epilogue, x, ldx, y, ldy, nvec, caller_order, scale_input);
     return;
   }
@@ -1000,7 +1001,7 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
   } else {
     FGS_CUFFT(cufftExecD2Z(w.r2c, w.grid.p, w.spec.p));
     if (profile_) mark(evs);
-    if (world == 1) {
+    if (!sharded) {
       MultiplyArgs ma{w.spec.p, mult.p, spec_elems, spec_elems, nvec, d, M, N};
       multiply_kernel<<<ceil_div(spec_elems, 256), 256, 0, stream>>>(ma);
       ++launches;
@@ -1069,7 +1070,7 @@ bool Core::use_conv2d() const {
     const char* e = std::getenv("FGS_CONV2D");
     return e && std::string(e) == "1";
   }();
-  return on && d == 2 && world == 1 && kind == FASTSUM && M <= 1024 && tw2.p != nullptr;
+  return on && d == 2 && !sharded && kind == FASTSUM && M <= 1024 && tw2.p != nullptr;
 }
 
 void Core::compute_degrees(int64_t* bad_node) {
@@ -1083,7 +1084,7 @@ void Core::compute_degrees(int64_t* bad_node) {
   unsigned long long init = ULLONG_MAX;
   FGS_CUDA(cudaMemcpyAsync(flag.p, &init, sizeof(init), cudaMemcpyHostToDevice, stream));
   apply(EPI_DEGREE, ones.p, n_local, nullptr, 0, 1, false, false);
-  if (world > 1) {
+  if (sharded) {
     nccl_check(nccl().all_reduce(flag.p, flag.p, 1, ncclUint64, ncclMin, comm, stream),
                "ncclAllReduce of the degree flag");
   }

@@ -94,6 +94,7 @@ class Core {
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   ncclComm_t comm = nullptr;
+  bool sharded = false;  // created through fgs_adjacency_create_sharded (owns an NCCL communicator)
   int64_t launches = 0;
   double lanczos_stats[4] = {0, 0, 0, 0};  // last run: apply ms, reorth ms, loop wall ms, iterations
 

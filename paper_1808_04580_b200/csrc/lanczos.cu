@@ -332,7 +332,7 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   FGS_CUDA(cudaMemcpyAsync(basis.p, local.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, st));
 
   auto allreduce = [&](double* v, int count) {
-    if (c.world > 1)
+    if (c.sharded)
       nccl_check(nccl().all_reduce(v, v, static_cast<size_t>(count), ncclDouble, ncclSum, c.comm, st),
                  "ncclAllReduce in Lanczos");
   };

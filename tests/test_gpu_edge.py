@@ -121,3 +121,30 @@ def test_device_apply_caller_order(orc):
     op.permute_device(dyi.data_ptr(), back.data_ptr(), direction=1)
     torch.cuda.synchronize()
     assert np.array_equal(back.cpu().numpy(), dy.cpu().numpy())
+
+
+def test_sharded_exchange_path_with_one_rank(orc):
+    # The N>1 data path (truncated-spectrum window pack -> ncclAllReduce ->
+    # unpack-multiply, NCCL-reduced Lanczos dots, ncclMin degree flag) run
+    # with a single-rank communicator must reproduce the unsharded operator.
+    import torch
+    X = fgs.workload_nodes(1, seed=2024)[:6000]
+    info = fgs.workload_info(1)
+    params = fgs.FastsumParams(info["N"], info["m"], info["p"])
+    kern = fgs.KernelSpec.gaussian(info["sigma"])
+    plain = fgs.AdjacencyOperator(X, kern, params)
+    shard = fgs.AdjacencyOperator(X, kern, params, rank=0, world=1, nccl_id=fgs.nccl_unique_id())
+    assert shard.n_local == X.shape[0] and shard.offset == 0
+    x = np.random.default_rng(14).standard_normal(X.shape[0])
+    dx = torch.from_numpy(x).cuda()
+    di = torch.empty_like(dx)
+    shard.permute_device(dx.data_ptr(), di.data_ptr(), direction=0)
+    dy = torch.empty_like(dx)
+    shard.apply_device(fgs.OP_SYM_LAPLACIAN, di.data_ptr(), dy.data_ptr(), internal_order=True)
+    back = torch.empty_like(dx)
+    shard.permute_device(dy.data_ptr(), back.data_ptr(), direction=1)
+    torch.cuda.synchronize()
+    assert rel(back.cpu().numpy(), plain.apply_sym_laplacian(x)) <= 1e-12
+    a = fgs.lanczos_largest(plain, 4, fgs.LanczosOptions(tol=1e-10))
+    b = fgs.lanczos_largest(shard, 4, fgs.LanczosOptions(tol=1e-10))
+    assert np.max(np.abs(a.values - b.values)) <= 1e-12
