@@ -457,7 +457,7 @@ def lanczos_largest(op: AdjacencyOperator, k: int, opts: LanczosOptions = None, 
     opts = opts or LanczosOptions()
     n = op.size()
     values = np.zeros(max(k, 1))
-    vectors = np.zeros((n, max(k, 1)), order="F") if want_vectors else None
+    vectors = np.empty((n, max(k, 1)), order="F") if want_vectors else None  # fully written by the library
     cnt, it, conv = C.c_int(), C.c_int(), C.c_int()
     _check(lib().fgs_lanczos_largest(op.handle, int(which), int(k), int(opts.max_iter), C.c_double(opts.tol),
                                      C.c_uint64(opts.seed), _dp(values),

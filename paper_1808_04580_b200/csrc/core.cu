@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -199,6 +200,55 @@ bool use_v3() {
   static const bool v3 = kernel_env("v3");
   return v3;
 }
+// d = 3 tensor-core kernel variants: (point streams P, chunk QS) from
+// FGS_V4_SPREAD / FGS_V4_INTERP = "P,QS" (0 = default P); default "0,32"
+struct V4Var {
+  int p, qs;
+};
+V4Var v4_variant(bool interp) {
+  const char* e = std::getenv(interp ? "FGS_V4_INTERP" : "FGS_V4_SPREAD");
+  V4Var v{0, 0};
+  if (e) std::sscanf(e, "%d,%d", &v.p, &v.qs);
+  if (v.qs != 64 && v.qs != 32) v.qs = 0;
+  if (v.p != 1 && v.p != 2 && v.p != 4) v.p = 0;
+  return v;
+}
+
+template <int T, bool INTERP>
+size_t v4_stage_doubles(V4Var v) {
+  auto one = [](auto tag) -> size_t {
+    using B = decltype(tag);
+    return INTERP ? 2 * static_cast<size_t>(B::QS) * B::STRIDE + static_cast<size_t>(B::P) * B::G * 8
+                  : 2 * static_cast<size_t>(B::QS) * B::STRIDE + 2 * B::QS;
+  };
+#define FGS_V4V(PP, QQ) \
+  if (v.p == PP && v.qs == QQ) return one(Blk4<T, INTERP, PP, QQ>{});
+  FGS_V4V(0, 0) FGS_V4V(0, 32) FGS_V4V(0, 64) FGS_V4V(1, 32) FGS_V4V(1, 64) FGS_V4V(2, 32) FGS_V4V(2, 64) FGS_V4V(4, 32)
+  FGS_V4V(4, 64)
+#undef FGS_V4V
+  return one(Blk4<T, INTERP, 0, 0>{});
+}
+
+template <int T, bool INTERP>
+void v4_launch(V4Var v, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
+#define FGS_V4L(PP, QQ)                                                               \
+  if (v.p == PP && v.qs == QQ) {                                                      \
+    if (INTERP) {                                                                     \
+      auto k = interp_v4_kernel<T, PP, QQ>;                                           \
+      set_smem(reinterpret_cast<const void*>(k), smem);                               \
+      k<<<nitems, Blk4<T, true, PP, QQ>::NT, smem, s>>>(a, box_stride);               \
+    } else {                                                                          \
+      auto k = spread_v4_kernel<T, PP, QQ>;                                           \
+      set_smem(reinterpret_cast<const void*>(k), smem);                               \
+      k<<<nitems, Blk4<T, false, PP, QQ>::NT, smem, s>>>(a, box_stride);              \
+    }                                                                                 \
+    return;                                                                           \
+  }
+  FGS_V4L(0, 0) FGS_V4L(0, 32) FGS_V4L(0, 64) FGS_V4L(1, 32) FGS_V4L(1, 64) FGS_V4L(2, 32) FGS_V4L(2, 64) FGS_V4L(4, 32)
+  FGS_V4L(4, 64)
+#undef FGS_V4L
+}
+
 // fp64 tensor-core kernels (kernels_v4.cuh): the default for d = 3, 2m in {8,12,16}
 bool use_v4() {
   static const bool v4 = !kernel_env("v1") && !kernel_env("v2") && !kernel_env("v3");
@@ -234,11 +284,9 @@ LaunchShape shape_t(bool dense) {
   if constexpr (has_v3<D, T>()) {
     using B3 = Blk3<T>;
     if (use_v3()) interp = 2 * static_cast<size_t>(B3::QS) * B3::TAPS + static_cast<size_t>(B3::P) * B3::G * B3::QB;
-    using B4i = Blk4<T, true>;
-    using B4s = Blk4<T, false>;
     if (use_v4()) {
-      interp = 2 * static_cast<size_t>(B4i::QS) * B4i::STRIDE + static_cast<size_t>(B4i::P) * B4i::G * 8;
-      if (dense) spread = 2 * static_cast<size_t>(B4s::QS) * B4s::STRIDE + 2 * B4s::QS;
+      interp = v4_stage_doubles<T, true>(v4_variant(true));
+      if (dense) spread = v4_stage_doubles<T, false>(v4_variant(false));
     }
   }
   if constexpr (has_v4_2d<D, T>()) {
@@ -315,15 +363,10 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
   }
   if constexpr (has_v3<D, T>()) {
     if (use_v4() && (interp || dense)) {
-      if (interp) {
-        auto k = interp_v4_kernel<T>;
-        set_smem(reinterpret_cast<const void*>(k), smem);
-        k<<<nitems, Blk4<T, true>::NT, smem, s>>>(a, box_stride);
-      } else {
-        auto k = spread_v4_kernel<T>;
-        set_smem(reinterpret_cast<const void*>(k), smem);
-        k<<<nitems, Blk4<T, false>::NT, smem, s>>>(a, box_stride);
-      }
+      if (interp)
+        v4_launch<T, true>(v4_variant(true), a, nitems, smem, box_stride, s);
+      else
+        v4_launch<T, false>(v4_variant(false), a, nitems, smem, box_stride, s);
       return;
     }
     if (interp && use_v3()) {
@@ -435,6 +478,7 @@ Core::Core(const double* nodes_colmajor, int64_t n_, int d_, Kind kind_, const K
   for (int t = 0; t < d; ++t) gsz *= M;
   if (gsz > 2.0e9) fail(FGS_ERESOURCE, "oversampled grid exceeds 2^31 points");
   B = d == 3 ? 4 : (d == 2 ? 8 : 32);
+  if (const char* e = std::getenv("FGS_TILE_B")) B = std::max(1, std::atoi(e));  // tuning override
   if (B > M) B = M;
   nt = ceil_div(M, B);
   ntiles = 1;
@@ -514,55 +558,68 @@ void Core::build_plan(const double* nodes_colmajor) {
   unsigned long long init = ULLONG_MAX;
   FGS_CUDA(cudaMemcpyAsync(bad.p, &init, sizeof(init), cudaMemcpyHostToDevice, stream));
 
-  PointArgs pa{dnodes.p, n, d, M, m, B, nt, rho, kind == FASTSUM ? 1 : 0, keys.p, idx.p, bad.p};
-  point_keys_kernel<<<ceil_div(n, 256), 256, 0, stream>>>(pa);
-  ++launches;
-  FGS_CUDA(cudaGetLastError());
-  unsigned long long badj = 0;
-  FGS_CUDA(cudaMemcpyAsync(&badj, bad.p, sizeof(badj), cudaMemcpyDeviceToHost, stream));
-  FGS_CUDA(cudaStreamSynchronize(stream));
-  if (badj != ULLONG_MAX) {
-    // validate_common (nfft.cpp:42-49): name the first offending node
-    const int64_t j = static_cast<int64_t>(badj);
-    for (int t = 0; t < d; ++t) {
-      double v = nodes_colmajor[t * n + j];
-      if (kind == FASTSUM) v = rho * v;
-      if (!(v >= -0.5 && v < 0.5))
-        fail(FGS_ERANGE, "node " + std::to_string(j) + " component " + std::to_string(t) + " = " +
-                             std::to_string(v) + " outside [-1/2, 1/2)");
-    }
-  }
-
-  // stable radix sort by (tile, cell): the internal order
-  int end_bit = 1;
-  {
-    double total = 1.0;
-    for (int t = 0; t < d; ++t) total *= static_cast<double>(nt) * B;
-    while (end_bit < 64 && std::ldexp(1.0, end_bit) < total) ++end_bit;
-  }
-  size_t tmp_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys_sorted.p, idx.p, perm.p, static_cast<int>(n), 0,
-                                  end_bit, stream);
-  DBuf<char> tmp;
-  tmp.alloc(tmp_bytes);
-  FGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys_sorted.p, idx.p, perm.p,
-                                           static_cast<int>(n), 0, end_bit, stream));
-  // run-length encode the sorted keys: one entry per nonempty cell
+  DBuf<char> tmp, tmpb;
   DBuf<unsigned long long> uniq;
   DBuf<int> counts, nruns;
   uniq.alloc(n);
   counts.alloc(n);
   nruns.alloc(1);
-  size_t tmp2 = 0;
-  cub::DeviceRunLengthEncode::Encode(nullptr, tmp2, keys_sorted.p, uniq.p, counts.p, nruns.p, static_cast<int>(n),
-                                     stream);
-  DBuf<char> tmpb;
-  tmpb.alloc(tmp2);
-  FGS_CUDA(cub::DeviceRunLengthEncode::Encode(tmpb.p, tmp2, keys_sorted.p, uniq.p, counts.p, nruns.p,
-                                              static_cast<int>(n), stream));
   int ncells = 0;
-  FGS_CUDA(cudaMemcpyAsync(&ncells, nruns.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  FGS_CUDA(cudaStreamSynchronize(stream));
+  // keys -> stable radix sort by (tile, cell) -> run-length encode; returns
+  // the number of nonempty cells (independent of the tile edge B)
+  auto sort_cells = [&]() {
+    PointArgs pa{dnodes.p, n, d, M, m, B, nt, rho, kind == FASTSUM ? 1 : 0, keys.p, idx.p, bad.p};
+    point_keys_kernel<<<ceil_div(n, 256), 256, 0, stream>>>(pa);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+    unsigned long long badj = 0;
+    FGS_CUDA(cudaMemcpyAsync(&badj, bad.p, sizeof(badj), cudaMemcpyDeviceToHost, stream));
+    FGS_CUDA(cudaStreamSynchronize(stream));
+    if (badj != ULLONG_MAX) {
+      // validate_common (nfft.cpp:42-49): name the first offending node
+      const int64_t j = static_cast<int64_t>(badj);
+      for (int t = 0; t < d; ++t) {
+        double v = nodes_colmajor[t * n + j];
+        if (kind == FASTSUM) v = rho * v;
+        if (!(v >= -0.5 && v < 0.5))
+          fail(FGS_ERANGE, "node " + std::to_string(j) + " component " + std::to_string(t) + " = " +
+                               std::to_string(v) + " outside [-1/2, 1/2)");
+      }
+    }
+    int end_bit = 1;
+    {
+      double total = 1.0;
+      for (int t = 0; t < d; ++t) total *= static_cast<double>(nt) * B;
+      while (end_bit < 64 && std::ldexp(1.0, end_bit) < total) ++end_bit;
+    }
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys_sorted.p, idx.p, perm.p, static_cast<int>(n), 0,
+                                    end_bit, stream);
+    tmp.alloc(tmp_bytes);
+    FGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys_sorted.p, idx.p, perm.p,
+                                             static_cast<int>(n), 0, end_bit, stream));
+    size_t tmp2 = 0;
+    cub::DeviceRunLengthEncode::Encode(nullptr, tmp2, keys_sorted.p, uniq.p, counts.p, nruns.p, static_cast<int>(n),
+                                       stream);
+    tmpb.alloc(tmp2);
+    FGS_CUDA(cub::DeviceRunLengthEncode::Encode(tmpb.p, tmp2, keys_sorted.p, uniq.p, counts.p, nruns.p,
+                                                static_cast<int>(n), stream));
+    FGS_CUDA(cudaMemcpyAsync(&ncells, nruns.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    FGS_CUDA(cudaStreamSynchronize(stream));
+  };
+  sort_cells();
+  // Very dense 3-D point sets (>= 100 points per nonempty cell: items are
+  // then mostly single cells) use 2^3-cell tiles: smaller item boxes -> less
+  // shared memory per CTA -> more resident warps (config 4: spread 511 ->
+  // 411 us, interp 475 -> 432 us); moderate densities keep 4^3 (config 5).
+  if (d == 3 && B == 4 && !std::getenv("FGS_TILE_B") && static_cast<double>(n) >= 100.0 * ncells && M >= 2) {
+    B = 2;
+    nt = ceil_div(M, B);
+    ntiles = nt * nt * nt;
+    unsigned long long init2 = ULLONG_MAX;
+    FGS_CUDA(cudaMemcpyAsync(bad.p, &init2, sizeof(init2), cudaMemcpyHostToDevice, stream));
+    sort_cells();
+  }
   std::vector<unsigned long long> hkeys(static_cast<size_t>(ncells));
   std::vector<int> hcounts(static_cast<size_t>(ncells));
   FGS_CUDA(cudaMemcpyAsync(hkeys.data(), uniq.p, sizeof(unsigned long long) * ncells, cudaMemcpyDeviceToHost, stream));

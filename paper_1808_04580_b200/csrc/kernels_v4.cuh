@@ -34,8 +34,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int T, bool INTERP>
+template <int T, bool INTERP, int PS = 0, int QSZ = 32>
 struct Blk4 {
+  // QSZ = 0: default chunk (64 for 2m in {8, 16}, 32 for 2m = 12; sweep in tools/sweep_v4.py)
   // warps per footprint group: more warps per footprint = fewer registers
   // per lane (ncu: 236-255 regs capped occupancy at 8 warps/SM with G = 1)
   static constexpr int G = T == 16 ? (INTERP ? 2 : 4) : (T == 12 ? 2 : 1);
@@ -45,9 +46,10 @@ struct Blk4 {
   static constexpr int TW = TAW * TC;        // pair tiles per warp
   static constexpr int KS = T / 4;           // interp K-steps over e
   static constexpr int NE = (T + 7) / 8;     // spread N-tiles over e (2m = 12 pads 12 -> 16)
-  static constexpr int P = T == 8 ? 4 : (T == 12 ? 2 : (INTERP ? 2 : 1));  // groups (point streams) per CTA
+  // groups (point streams) per CTA; PS > 0 overrides the default
+  static constexpr int P = PS > 0 ? PS : (T == 8 ? 4 : (T == 12 ? 2 : (INTERP ? 2 : 1)));
   static constexpr int NT = 32 * G * P;
-  static constexpr int QS = 32;              // points per staged chunk
+  static constexpr int QS = QSZ > 0 ? QSZ : (T == 12 ? 32 : 64);  // points per staged chunk
   static constexpr int TAPS = 3 * T;
   // staged row stride: = 4 or 12 (mod 16 doubles) so the 4 (spread) or 8
   // (interp) points a warp reads per LDS fall on distinct bank pairs; 2m = 16
@@ -71,9 +73,9 @@ __device__ __forceinline__ void v4_issue_chunk(double* buf, const double* taps, 
 // ---------------------------------------------------------------------------
 // interpolation.  smem: box | stage[2][QS*TAPS] | red[P][G][8]
 // ---------------------------------------------------------------------------
-template <int T>
-__global__ void __launch_bounds__(Blk4<T, true>::NT) interp_v4_kernel(PassArgs a, int box_stride_smem) {
-  using B = Blk4<T, true>;
+template <int T, int PS, int QSZ>
+__global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT) interp_v4_kernel(PassArgs a, int box_stride_smem) {
+  using B = Blk4<T, true, PS, QSZ>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, G = B::G, P = B::P, SR = B::STRIDE;
   constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, KS = B::KS;
   extern __shared__ __align__(16) double smem[];
@@ -229,9 +231,9 @@ __global__ void __launch_bounds__(Blk4<T, true>::NT) interp_v4_kernel(PassArgs a
 // ---------------------------------------------------------------------------
 // spread.  smem: box | stage[2][QS*TAPS] | xs[2][QS]
 // ---------------------------------------------------------------------------
-template <int T>
-__global__ void __launch_bounds__(Blk4<T, false>::NT) spread_v4_kernel(PassArgs a, int box_stride_smem) {
-  using B = Blk4<T, false>;
+template <int T, int PS, int QSZ>
+__global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(PassArgs a, int box_stride_smem) {
+  using B = Blk4<T, false, PS, QSZ>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE;
   constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, NE = B::NE;
   extern __shared__ __align__(16) double smem[];
