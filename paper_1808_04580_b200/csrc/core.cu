@@ -903,7 +903,6 @@ Workspace& Core::workspace(int nvec) {
   w->grid.alloc(static_cast<size_t>(grid_elems) * nvec);
   w->spec.alloc(static_cast<size_t>(spec_elems) * nvec);
   if (sharded) w->window.alloc(static_cast<size_t>(window_elems) * nvec);
-  if (use_conv2d()) w->cgrid.alloc(static_cast<size_t>(M) * (N / 2 + 1) * nvec);
   int dims[3] = {M, M, M};
   FGS_CUFFT(cufftPlanMany(&w->r2c, d, dims, nullptr, 1, static_cast<int>(grid_elems), nullptr, 1,
                           static_cast<int>(spec_elems), CUFFT_D2Z, nvec));
@@ -1044,17 +1043,21 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
   launch_assemble(w, nvec);
   if (profile_) mark(evs);
   if (use_conv2d()) {
-    // d = 2: pruned direct-DFT convolution over the (N+1)(N/2+1) window
-    const int H = N / 2 + 1;
-    Conv2Args ca{w.grid.p, w.grid.p, w.cgrid.p, mult.p, tw2.p, M, N, nvec, grid_elems, static_cast<int64_t>(M) * H};
-    conv2_rows_fwd<<<dim3(M, nvec), kConvThreads, sizeof(double2) * M + sizeof(double) * M, stream>>>(ca);
-    if (profile_) mark(evs);
-    conv2_cols<<<dim3(H, nvec), kConvThreads, sizeof(double2) * (2 * M + N + 1), stream>>>(ca);
-    if (profile_) mark(evs);
-    conv2_rows_inv<<<dim3(M, nvec), kConvThreads, sizeof(double2) * (M + H), stream>>>(ca);
-    launches += 3;
+    // d = 2: one cluster launch (row FFTs / kept-column FFT + multiply +
+    // inverse through DSMEM / inverse row FFTs), conv2d.cuh
+    int logM = 0;
+    while ((1 << logM) < M) ++logM;
+    Conv2Args ca{w.grid.p, w.grid.p, mult.p, tw2.p, M, logM, N, nvec, grid_elems};
+    const size_t smem = conv2_smem(M, N);
+    set_smem(conv2_kernel_ptr(M), smem);
+    conv2_launch(ca, smem, stream);
+    ++launches;
     FGS_CUDA(cudaGetLastError());
-    if (profile_) mark(evs);
+    if (profile_) {
+      mark(evs);
+      mark(evs);
+      mark(evs);
+    }
   } else {
     FGS_CUFFT(cufftExecD2Z(w.r2c, w.grid.p, w.spec.p));
     if (profile_) mark(evs);
@@ -1120,14 +1123,15 @@ void Core::read_profile(double* ms, int64_t* applies) {
   ev_pending_.clear();
 }
 
-// opt-in (FGS_CONV2D=1): at C2 size (M = 128) its three latency-bound launches
-// measured no faster than cuFFT D2Z + multiply + Z2D (32.5 vs 32.9 us)
+// d = 2 grids: one-launch cluster convolution instead of cuFFT D2Z +
+// multiply + Z2D (FGS_CONV2D=0 selects cuFFT)
 bool Core::use_conv2d() const {
   static const bool on = [] {
     const char* e = std::getenv("FGS_CONV2D");
-    return e && std::string(e) == "1";
+    return !(e && std::string(e) == "0");
   }();
-  return on && d == 2 && !sharded && kind == FASTSUM && M <= 1024 && tw2.p != nullptr;
+  return on && d == 2 && !sharded && kind == FASTSUM && conv2_supported(M) &&
+         conv2_smem(M, N) <= 200 * 1024 && tw2.p != nullptr;
 }
 
 void Core::compute_degrees(int64_t* bad_node) {
