@@ -2,6 +2,8 @@
 // the B200 fast-summation kernels (paper_1808_04580_b200/csrc).
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -40,6 +42,48 @@ struct Error : std::runtime_error {
                                   std::to_string(static_cast<int>(r_)) + " (" + __FILE__ + \
                                   ":" + std::to_string(__LINE__) + ")");             \
   } while (0)
+
+// Programmatic dependent launch: the hot kernels of an apply (spread,
+// assemble, d=2 convolution, interp) start with pdl_wait() -- which blocks
+// until the preceding grid in the stream has completed and its writes are
+// visible -- and then allow their own successor to be scheduled, so each
+// kernel's CTAs are resident and waiting when its predecessor drains
+// instead of paying the launch gap.  A no-op when launched without the
+// attribute.  FGS_PDL=0 launches everything fully serialised.
+// g_pdl_early: 1 = let the successor launch as soon as every CTA of this
+// grid has passed its wait (FGS_PDL=1), 0 = implicit trigger at grid end.
+__device__ int g_pdl_early;
+
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (g_pdl_early) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+// FGS_PDL: 0 off, 1 PDL launches + early trigger, 2 (default) PDL launches,
+// implicit trigger
+inline int pdl_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("FGS_PDL");
+    return e ? std::atoi(e) : 2;
+  }();
+  return mode;
+}
+inline bool pdl_on() { return pdl_mode() != 0; }
+
+template <class... KP, class... Args>
+inline void launch_ex(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl_on() && s != nullptr) ? 1 : 0;
+  FGS_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KP>(args)...));
+}
 
 // One work item = one CTA of the spread / interp kernels: a run list of
 // point cells inside one spatial tile, with the bounding box of the union of

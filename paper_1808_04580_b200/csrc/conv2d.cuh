@@ -182,6 +182,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kConvThre
   const double* gin = a.grid_in + v * a.grid_stride + static_cast<int64_t>(c) * R * M;
   double* gout = a.grid_out + v * a.grid_stride + static_cast<int64_t>(c) * R * M;
   CONV2_MARK(0);
+  pdl_wait();
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
   // my columns' window multipliers, asynchronously (first used after the
   // first cluster barrier)
@@ -277,11 +278,11 @@ inline const void* conv2_kernel_ptr(int M) {
 inline void conv2_launch(const Conv2Args& a, size_t smem, cudaStream_t stream) {
   const dim3 grid(kClusterCtas * a.nvec), block(kConvThreads);
   switch (a.M) {
-    case 16: conv2_cluster_kernel<16><<<grid, block, smem, stream>>>(a); break;
-    case 32: conv2_cluster_kernel<32><<<grid, block, smem, stream>>>(a); break;
-    case 64: conv2_cluster_kernel<64><<<grid, block, smem, stream>>>(a); break;
-    case 128: conv2_cluster_kernel<128><<<grid, block, smem, stream>>>(a); break;
-    default: conv2_cluster_kernel<256><<<grid, block, smem, stream>>>(a); break;
+    case 16: launch_ex(conv2_cluster_kernel<16>, grid, block, smem, stream, a); break;
+    case 32: launch_ex(conv2_cluster_kernel<32>, grid, block, smem, stream, a); break;
+    case 64: launch_ex(conv2_cluster_kernel<64>, grid, block, smem, stream, a); break;
+    case 128: launch_ex(conv2_cluster_kernel<128>, grid, block, smem, stream, a); break;
+    default: launch_ex(conv2_cluster_kernel<256>, grid, block, smem, stream, a); break;
   }
 }
 

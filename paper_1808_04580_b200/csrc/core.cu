@@ -236,11 +236,11 @@ void v4_launch(V4Var v, const PassArgs& a, int nitems, size_t smem, int box_stri
     if (INTERP) {                                                                     \
       auto k = interp_v4_kernel<T, PP, QQ>;                                           \
       set_smem(reinterpret_cast<const void*>(k), smem);                               \
-      k<<<nitems, Blk4<T, true, PP, QQ>::NT, smem, s>>>(a, box_stride);               \
+      launch_ex(k, nitems, Blk4<T, true, PP, QQ>::NT, smem, s, a, box_stride);               \
     } else {                                                                          \
       auto k = spread_v4_kernel<T, PP, QQ>;                                           \
       set_smem(reinterpret_cast<const void*>(k), smem);                               \
-      k<<<nitems, Blk4<T, false, PP, QQ>::NT, smem, s>>>(a, box_stride);              \
+      launch_ex(k, nitems, Blk4<T, false, PP, QQ>::NT, smem, s, a, box_stride);              \
     }                                                                                 \
     return;                                                                           \
   }
@@ -338,7 +338,7 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
       if (interp) {
         auto k = interp_v4_2d_kernel<T>;
         set_smem(reinterpret_cast<const void*>(k), smem);
-        k<<<nitems, Blk4d2<T>::NT, smem, s>>>(a, box_stride);
+        launch_ex(k, nitems, Blk4d2<T>::NT, smem, s, a, box_stride);
       } else {
         static const int ps = [] {
           const char* e = std::getenv("FGS_SPREAD2D_P");
@@ -347,15 +347,15 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
         if (ps == 4) {
           auto k = spread_v4_2d_kernel<T, 4>;
           set_smem(reinterpret_cast<const void*>(k), smem);
-          k<<<nitems, Blk4d2<T, 4>::NT, smem, s>>>(a, box_stride);
+          launch_ex(k, nitems, Blk4d2<T, 4>::NT, smem, s, a, box_stride);
         } else if (ps == 2) {
           auto k = spread_v4_2d_kernel<T, 2>;
           set_smem(reinterpret_cast<const void*>(k), smem);
-          k<<<nitems, Blk4d2<T, 2>::NT, smem, s>>>(a, box_stride);
+          launch_ex(k, nitems, Blk4d2<T, 2>::NT, smem, s, a, box_stride);
         } else {
           auto k = spread_v4_2d_kernel<T, 1>;
           set_smem(reinterpret_cast<const void*>(k), smem);
-          k<<<nitems, Blk4d2<T, 1>::NT, smem, s>>>(a, box_stride);
+          launch_ex(k, nitems, Blk4d2<T, 1>::NT, smem, s, a, box_stride);
         }
       }
       return;
@@ -440,6 +440,10 @@ Core::Core(const double* nodes_colmajor, int64_t n_, int d_, Kind kind_, const K
   T = 2 * m;
   FGS_CUDA(cudaSetDevice(device));
   FGS_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  {
+    const int early = pdl_mode() == 1 ? 1 : 0;
+    FGS_CUDA(cudaMemcpyToSymbol(g_pdl_early, &early, sizeof(int)));
+  }
 
   if (kind == FASTSUM) {
     // common rescaling into the ball of radius 1/4 - eps_b/2 (fastsum.cpp:79-88)
@@ -951,11 +955,11 @@ void Core::launch_assemble(Workspace& w, int nvec) {
   // lanes per grid cell from the mean CSR list length
   const double mean_list = static_cast<double>(asm_idx.n) / static_cast<double>(std::max<int64_t>(grid_elems, 1));
   if (mean_list >= 16.0)
-    assemble_kernel<8><<<ceil_div(grid_elems * 8, 256), 256, 0, stream>>>(aa);
+    launch_ex(assemble_kernel<8>, ceil_div(grid_elems * 8, 256), 256, 0, stream, aa);
   else if (mean_list >= 4.0)
-    assemble_kernel<4><<<ceil_div(grid_elems * 4, 256), 256, 0, stream>>>(aa);
+    launch_ex(assemble_kernel<4>, ceil_div(grid_elems * 4, 256), 256, 0, stream, aa);
   else
-    assemble_kernel<1><<<ceil_div(grid_elems, 256), 256, 0, stream>>>(aa);
+    launch_ex(assemble_kernel<1>, ceil_div(grid_elems, 256), 256, 0, stream, aa);
   ++launches;
   FGS_CUDA(cudaGetLastError());
 }

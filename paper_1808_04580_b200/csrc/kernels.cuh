@@ -249,6 +249,7 @@ struct AssembleArgs {
 // combined by a fixed shuffle tree, so the result is bitwise reproducible.
 template <int kAsmLanes>
 __global__ void assemble_kernel(AssembleArgs a) {
+  pdl_wait();
   const int64_t gt = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t g = gt / kAsmLanes;
   const int sub = static_cast<int>(gt % kAsmLanes);

@@ -75,6 +75,7 @@ __device__ __forceinline__ void v4_issue_chunk(double* buf, const double* taps, 
 // ---------------------------------------------------------------------------
 template <int T, int PS, int QSZ>
 __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT) interp_v4_kernel(PassArgs a, int box_stride_smem) {
+  pdl_wait();
   using B = Blk4<T, true, PS, QSZ>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, G = B::G, P = B::P, SR = B::STRIDE;
   constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, KS = B::KS;
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT) interp_v4_kernel(P
 // ---------------------------------------------------------------------------
 template <int T, int PS, int QSZ>
 __global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(PassArgs a, int box_stride_smem) {
+  pdl_wait();
   using B = Blk4<T, false, PS, QSZ>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE;
   constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, NE = B::NE;
@@ -378,6 +380,7 @@ struct Blk4d2 {
 
 template <int T>
 __global__ void __launch_bounds__(Blk4d2<T>::NT) interp_v4_2d_kernel(PassArgs a, int box_stride_smem) {
+  pdl_wait();
   using B = Blk4d2<T>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE, NC = B::NC, KS = B::KS;
   extern __shared__ __align__(16) double smem[];
@@ -500,6 +503,7 @@ __global__ void __launch_bounds__(Blk4d2<T>::NT) interp_v4_2d_kernel(PassArgs a,
 
 template <int T, int PS>
 __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) spread_v4_2d_kernel(PassArgs a, int box_stride_smem) {
+  pdl_wait();
   using B = Blk4d2<T, PS>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE, NC = B::NC, NE = B::NE;
   extern __shared__ __align__(16) double smem[];
