@@ -278,14 +278,23 @@ class FastsumPlan {
 };
 
 // ---- AdjacencyOperator -----------------------------------------------------
+// graphop.hpp:19-22: Fastsum = NFFT fast summation, Direct = exact O(n^2) sums
+enum class AdjacencyBackend { Fastsum, Direct };
+
 class AdjacencyOperator {
  public:
-  AdjacencyOperator(const MatrixXd& nodes, const KernelSpec& kernel, const FastsumParams& params, int device = 0)
-      : n_(nodes.rows()), d_(static_cast<int>(nodes.cols())), kernel_(kernel) {
+  AdjacencyOperator(const MatrixXd& nodes, const KernelSpec& kernel, const FastsumParams& params,
+                    AdjacencyBackend backend = AdjacencyBackend::Fastsum, int device = 0)
+      : n_(nodes.rows()), d_(static_cast<int>(nodes.cols())), kernel_(kernel), backend_(backend) {
     const fgs_fastsum_params p = params.c();
     std::int64_t bad = -1;
-    detail::check(fgs_adjacency_create(nodes.data(), nodes.rows(), d_, static_cast<fgs_kernel>(kernel.family),
-                                       kernel.shape, &p, device, &h_, &bad));
+    if (backend == AdjacencyBackend::Direct)
+      detail::check(fgs_adjacency_create_direct(nodes.data(), nodes.rows(), d_,
+                                                static_cast<fgs_kernel>(kernel.family), kernel.shape, device, &h_,
+                                                &bad));
+    else
+      detail::check(fgs_adjacency_create(nodes.data(), nodes.rows(), d_, static_cast<fgs_kernel>(kernel.family),
+                                         kernel.shape, &p, device, &h_, &bad));
     detail::check(fgs_adjacency_info(h_, nullptr, nullptr, &k0_, nullptr, nullptr));
     degrees_ = VectorXd(n_);
     detail::check(fgs_adjacency_degrees(h_, degrees_.data()));
@@ -297,6 +306,7 @@ class AdjacencyOperator {
   Index size() const { return n_; }
   int dims() const { return d_; }
   const KernelSpec& kernel() const { return kernel_; }
+  AdjacencyBackend backend() const { return backend_; }
   double kernel_zero() const { return k0_; }
   const VectorXd& degrees() const { return degrees_; }
   VectorXd apply_kernel(const VectorXd& x) const { return apply(FGS_OP_KERNEL, x); }
@@ -316,6 +326,7 @@ class AdjacencyOperator {
   Index n_ = 0;
   int d_ = 0;
   KernelSpec kernel_;
+  AdjacencyBackend backend_ = AdjacencyBackend::Fastsum;
   double k0_ = 0.0;
   VectorXd degrees_;
 };

@@ -108,6 +108,12 @@ void fgs_fastsum_destroy(fgs_fastsum_t h);
 fgs_status fgs_adjacency_create(const double* nodes_colmajor, int64_t n, int d, fgs_kernel kernel,
                                 double shape, const fgs_fastsum_params* params, int device,
                                 fgs_adjacency_t* out, int64_t* bad_node);
+/* AdjacencyBackend::Direct (graphop.hpp:19-22, graphop.cpp:29-34): the exact
+ * O(n^2) operator W~x = sum_i K(||v_j - v_i||) x_i on raw (unscaled) nodes
+ * (fastsum.cpp:126-139 direct_apply), also the recompute-mode dense
+ * reference (spectral.cpp:497-554).  Same apply/degrees/Lanczos calls. */
+fgs_status fgs_adjacency_create_direct(const double* nodes_colmajor, int64_t n, int d, fgs_kernel kernel,
+                                       double shape, int device, fgs_adjacency_t* out, int64_t* bad_node);
 /* Multi-GPU: one process per GPU.  Every rank passes the SAME nodes; rank r
  * owns the r-th contiguous slice of the internal spatial order.  nccl_id is
  * the 128-byte ncclUniqueId from fgs_nccl_unique_id() on rank 0, broadcast

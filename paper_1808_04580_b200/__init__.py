@@ -293,15 +293,30 @@ class FastsumPlan:
 
 
 # ---- AdjacencyOperator (graphop.hpp:45-97) ------------------------------
+BACKEND_FASTSUM, BACKEND_DIRECT = "fastsum", "direct"  # AdjacencyBackend (graphop.hpp:19-22)
+
+
 class AdjacencyOperator:
+    """graphop.hpp:45-97.  backend "fastsum" (default) or "direct" (the exact
+    O(n^2) sum, graphop.cpp:29-34)."""
+
     def __init__(self, nodes, kernel: KernelSpec, params: FastsumParams = None, device=0,
-                 rank=0, world=1, nccl_id: bytes = None):
+                 rank=0, world=1, nccl_id: bytes = None, backend: str = BACKEND_FASTSUM):
         params = params or FastsumParams()
         nd, n, d = _nodes(nodes)
         h = C.c_void_p()
         bad = C.c_int64(-1)
         cp = params._c()
-        if world > 1 or nccl_id is not None:
+        self.backend = backend
+        if backend == BACKEND_DIRECT:
+            if world > 1 or nccl_id is not None:
+                raise ParameterError("the direct backend is single-device")
+            st = lib().fgs_adjacency_create_direct(_dp(nd), C.c_int64(n), int(d), int(kernel.family),
+                                                   C.c_double(kernel.shape), int(device), C.byref(h),
+                                                   C.byref(bad))
+        elif backend != BACKEND_FASTSUM:
+            raise ParameterError(f"unknown adjacency backend {backend!r}")
+        elif world > 1 or nccl_id is not None:
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
             st = lib().fgs_adjacency_create_sharded(_dp(nd), C.c_int64(n), int(d), int(kernel.family),
                                                     C.c_double(kernel.shape), C.byref(cp), int(device),

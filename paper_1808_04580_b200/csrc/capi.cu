@@ -309,6 +309,22 @@ fgs_status fgs_adjacency_create(const double* nodes, int64_t n, int d, fgs_kerne
   return adjacency_create_impl(nodes, n, d, kernel, shape, params, device, 0, 1, nullptr, out, bad_node);
 }
 
+fgs_status fgs_adjacency_create_direct(const double* nodes, int64_t n, int d, fgs_kernel kernel, double shape,
+                                       int device, fgs_adjacency_t* out, int64_t* bad_node) {
+  return guard([&] {
+    need(out, "out");
+    *out = nullptr;
+    if (bad_node) *bad_node = -1;
+    if (n < 2) fail(FGS_ESHAPE, "adjacency operator needs at least two nodes");  // graphop.cpp:39-42
+    if (d < 1 || d > 3) fail(FGS_EPARAM, "node dimension must be 1, 2, or 3");
+    need(nodes, "nodes");
+    auto h = std::make_unique<fgs_adjacency>();
+    h->core = std::make_unique<Core>(nodes, n, d, Core::DIRECT, spec_of(kernel, shape), fgsb::Params{}, device);
+    h->core->compute_degrees(bad_node);
+    *out = h.release();
+  });
+}
+
 fgs_status fgs_nccl_unique_id(void* out128) {
   return guard([&] {
     need(out128, "out");

@@ -18,6 +18,7 @@
 #include "kernels_v3.cuh"
 #include "kernels_v4.cuh"
 #include "conv2d.cuh"
+#include "direct.cuh"
 #include "nccl_shim.hpp"
 
 namespace fgsb {
@@ -424,6 +425,10 @@ Core::Core(const double* nodes_colmajor, int64_t n_, int d_, Kind kind_, const K
     if (n == 0) fail(FGS_ESHAPE, "node set is empty");
     if (d < 1 || d > 3) fail(FGS_ESHAPE, "nodes must have 1, 2, or 3 columns");
     check_spec(kernel);
+  } else if (kind == DIRECT) {
+    if (n == 0) fail(FGS_ESHAPE, "node set is empty");
+    if (d < 1 || d > 3) fail(FGS_EPARAM, "node dimension must be 1, 2, or 3");
+    check_spec(kernel);
   } else {
     if (d < 1 || d > 3) fail(FGS_EPARAM, "dims must be 1, 2, or 3, got " + std::to_string(d));
     if (params.N < 2 || params.N % 2 != 0)
@@ -443,6 +448,19 @@ Core::Core(const double* nodes_colmajor, int64_t n_, int d_, Kind kind_, const K
   {
     const int early = pdl_mode() == 1 ? 1 : 0;
     FGS_CUDA(cudaMemcpyToSymbol(g_pdl_early, &early, sizeof(int)));
+  }
+  if (kind == DIRECT) {  // exact operator: raw nodes, no rescaling (graphop.cpp:29-34, fastsum.cpp:126-139)
+    if (world != 1 || nccl_id) fail(FGS_EPARAM, "the direct backend is single-device");
+    k0 = kernel_value(kernel, 0.0);
+    scaled = kernel;
+    n_local = n;
+    offset = 0;
+    nodes_d.upload(nodes_colmajor, static_cast<size_t>(n) * d, stream);
+    host_perm.resize(static_cast<size_t>(n));
+    for (int64_t j = 0; j < n; ++j) host_perm[static_cast<size_t>(j)] = static_cast<int>(j);
+    perm.upload(host_perm.data(), host_perm.size(), stream);
+    FGS_CUDA(cudaStreamSynchronize(stream));
+    return;
   }
 
   if (kind == FASTSUM) {
@@ -903,6 +921,12 @@ Workspace& Core::workspace(int nvec) {
   if (itw != ws_.end()) return *itw->second;
   auto w = std::make_unique<Workspace>();
   w->nvec = nvec;
+  if (kind == DIRECT) {  // segment partials [nseg][nvec][n]
+    w->priv.alloc(static_cast<size_t>(direct_segments()) * nvec * n);
+    auto& ref = *w;
+    ws_[nvec] = std::move(w);
+    return ref;
+  }
   w->priv.alloc(static_cast<size_t>(std::max(nitems, 1)) * box_stride * nvec);
   w->grid.alloc(static_cast<size_t>(grid_elems) * nvec);
   w->spec.alloc(static_cast<size_t>(spec_elems) * nvec);
@@ -1015,6 +1039,10 @@ void Core::apply(int epilogue, const double* x, int64_t ldx, double* y, int64_t 
 void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
                           bool caller_order, bool scale_input) {
   Workspace& w = workspace(nvec);
+  if (kind == DIRECT) {
+    direct_launches(w, epilogue, x, ldx, y, ldy, nvec, scale_input);
+    return;
+  }
   PassArgs a{};
   a.items = items.p;
   a.runs = runs.p;
@@ -1288,6 +1316,62 @@ double Core::error_estimate(int samples, uint64_t seed) const {
     worst = std::max(worst, std::abs(kernel_value(scaled, std::sqrt(yn)) - acc.real()));
   }
   return std::abs(out_factor) * worst;
+}
+
+// ---- direct backend (exact O(n^2) sums) ------------------------------------
+int Core::direct_segments() const {
+  // enough CTAs to fill the device (~8 per SM) without tiny segments
+  const int64_t tiles = ceil_div(n, static_cast<int64_t>(kDirectThreads));
+  const int64_t want = ceil_div(static_cast<int64_t>(148 * 8), tiles);
+  const int64_t most = ceil_div(n, static_cast<int64_t>(kDirectTile));
+  return static_cast<int>(std::max<int64_t>(1, std::min(want, most)));
+}
+
+void Core::direct_launches(Workspace& w, int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
+                           bool scale_input) {
+  const int nseg = direct_segments();
+  DirectArgs da{};
+  da.nodes = nodes_d.p;
+  da.n = n;
+  da.d = d;
+  da.family = kernel.family;
+  da.shape = kernel.shape;
+  da.x = x;
+  da.ldx = ldx;
+  da.s = inv_sqrt.p;
+  da.scale_input = scale_input ? 1 : 0;
+  da.seg_len = ceil_div(n, static_cast<int64_t>(nseg));
+  da.nseg = nseg;
+  da.partial = w.priv.p;
+  da.nvec = nvec;
+  const dim3 grid(static_cast<unsigned>(ceil_div(n, static_cast<int64_t>(kDirectThreads))), static_cast<unsigned>(nseg));
+  for (int v0 = 0; v0 < nvec; v0 += kDirectVec) {
+    da.vec0 = v0;
+    da.nv = std::min(kDirectVec, nvec - v0);
+    launch_ex(direct_partial_kernel, grid, kDirectThreads, 0, stream, da);
+    ++launches;
+  }
+  DirectFinishArgs fa{};
+  fa.partial = w.priv.p;
+  fa.nseg = nseg;
+  fa.nvec = nvec;
+  fa.n = n;
+  fa.pa.perm = nullptr;
+  fa.pa.x = x;
+  fa.pa.ldx = ldx;
+  fa.pa.s = inv_sqrt.p;
+  fa.pa.y = y;
+  fa.pa.ldy = ldy;
+  fa.pa.epilogue = epilogue;
+  fa.pa.k0 = k0;
+  fa.pa.degrees = degrees.p;
+  fa.pa.inv_sqrt = inv_sqrt.p;
+  fa.pa.bad_flag = flag.p;
+  fa.pa.caller = perm.p;
+  launch_ex(direct_finish_kernel, dim3(static_cast<unsigned>(ceil_div(n, static_cast<int64_t>(256)))), 256, 0, stream,
+            fa);
+  ++launches;
+  FGS_CUDA(cudaGetLastError());
 }
 
 }  // namespace fgsb

@@ -70,7 +70,7 @@ struct Workspace {
 
 class Core {
  public:
-  enum Kind { NFFT = 0, FASTSUM = 1 };
+  enum Kind { NFFT = 0, FASTSUM = 1, DIRECT = 2 };  // DIRECT: exact O(n^2) operator (AdjacencyBackend::Direct)
 
   Core(const double* nodes_colmajor, int64_t n, int d, Kind kind, const KernelSpec& kernel,
        const Params& params, int device, int rank = 0, int world = 1, const void* nccl_id = nullptr);
@@ -107,6 +107,7 @@ class Core {
   DBuf<cufftDoubleComplex> mult;  // compact Hermitian multiplier (FASTSUM)
   DBuf<double> deconv_d;
   DBuf<double2> tw2;  // d = 2 pruned-convolution twiddles
+  DBuf<double> nodes_d;  // DIRECT: raw nodes [d][n], caller order
   bool use_conv2d() const;
   int nitems = 0;
   double mean_run = 0.0;  // points per run (cell piece) of this shard: picks the spread kernel
@@ -180,6 +181,9 @@ class Core {
   void launch_spread(const PassArgs& a);
   void launch_interp(const PassArgs& a);
   void launch_assemble(Workspace& w, int nvec);
+  int direct_segments() const;
+  void direct_launches(Workspace& w, int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
+                       bool scale_input);
   size_t smem_bytes(bool interp) const;
   int threads() const;
 };
