@@ -188,6 +188,21 @@ fgs_status fgs_workload_info(int config, int64_t* n, int* d, double* sigma, int*
 fgs_status fgs_workload_generate(int config, uint64_t seed, double* nodes_colmajor);
 fgs_status fgs_workload_vectors(int64_t n, int nvec, uint64_t seed, double* out);
 
+/* ---- k-means / spectral clustering (learn.hpp, learn.cpp:17-167) --------- */
+/* kmeans(points, k, {restarts, max_iter, seed}) (learn.cpp:140-155): points
+ * column-major n x dim; labels[n]; centroids k x dim column-major and wcss
+ * may be NULL.  k-means++ seeding from std::mt19937_64(seed) shared across
+ * restarts, Lloyd iterations on the device, best run by strict wcss. */
+fgs_status fgs_kmeans(const double* points_colmajor, int64_t n, int dim, int k, int restarts, int max_iter,
+                      uint64_t seed, int device, int* labels, double* centroids_colmajor, double* wcss);
+/* spectral_cluster(pairs, k, opts) (learn.cpp:157-167): unit-normalised rows
+ * of the n x kv eigenvector block (host, or device memory when on_device),
+ * then kmeans.  kv < k -> FGS_EPARAM. */
+fgs_status fgs_spectral_cluster(const double* vectors_colmajor, int64_t n, int kv, int k, int restarts, int max_iter,
+                                uint64_t seed, int device, int on_device, int* labels);
+/* misclassification_rate / _permuted (learn.cpp:441-486), host-side */
+fgs_status fgs_misclassification_rate(const int* predicted, const int* truth, int64_t n, int permuted, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1103,6 +1103,187 @@ LanczosOut lanczos_largest(int64_t n, const ApplyFn& apply, int k, int max_iter,
 
 thread_local std::string g_last_error;
 
+// ---------------------------------------------------------------------------
+// k-means and spectral clustering (learn.cpp:17-167), label metrics
+// (learn.cpp:441-486).  Points column-major n x dim (Eigen's MatrixXd).
+// Row squared norms are left-to-right sums of squares (Eigen's scalar redux
+// over a strided row); dist2.sum() is a serial sum here (Eigen vectorizes
+// that one -- an ulp-level difference that only matters on exact ties of
+// the k-means++ target).
+// ---------------------------------------------------------------------------
+struct KMeansRun {
+  std::vector<int> labels;
+  std::vector<double> centroids;  // k x dim column-major
+  double wcss = 0.0;
+};
+
+double km_dist2(const Mat& pts, int64_t i, const std::vector<double>& cen, int k, int c) {
+  double s = 0.0;
+  for (int64_t t = 0; t < pts.cols; ++t) {
+    const double df = pts(i, t) - cen[static_cast<size_t>(t * k + c)];
+    s += df * df;
+  }
+  return s;
+}
+
+// learn.cpp:30-75
+std::vector<double> km_plus_plus(const Mat& pts, int k, std::mt19937_64& rng) {
+  const int64_t n = pts.rows, dim = pts.cols;
+  std::uniform_int_distribution<int64_t> any(0, n - 1);
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  std::vector<double> cen(static_cast<size_t>(k * dim));
+  std::vector<bool> chosen(static_cast<size_t>(n), false);
+  auto take = [&](int c, int64_t i) {
+    for (int64_t t = 0; t < dim; ++t) cen[static_cast<size_t>(t * k + c)] = pts(i, t);
+    chosen[static_cast<size_t>(i)] = true;
+  };
+  take(0, any(rng));
+  std::vector<double> d2(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) d2[static_cast<size_t>(i)] = km_dist2(pts, i, cen, k, 0);
+  for (int c = 1; c < k; ++c) {
+    double total = 0.0;
+    for (double v : d2) total += v;
+    int64_t pick = -1;
+    if (total > 0.0) {
+      const double target = unif(rng) * total;
+      double running = 0.0;
+      for (int64_t i = 0; i < n; ++i) {
+        running += d2[static_cast<size_t>(i)];
+        if (running >= target) {
+          pick = i;
+          break;
+        }
+      }
+      if (pick < 0) pick = n - 1;
+    } else {  // every remaining distance is zero: uniform among the unchosen
+      std::vector<int64_t> open;
+      for (int64_t i = 0; i < n; ++i)
+        if (!chosen[static_cast<size_t>(i)]) open.push_back(i);
+      if (open.empty())
+        pick = any(rng);
+      else
+        pick = open[std::uniform_int_distribution<size_t>(0, open.size() - 1)(rng)];
+    }
+    take(c, pick);
+    for (int64_t i = 0; i < n; ++i)
+      d2[static_cast<size_t>(i)] = std::min(d2[static_cast<size_t>(i)], km_dist2(pts, i, cen, k, c));
+  }
+  return cen;
+}
+
+// learn.cpp:77-136
+KMeansRun km_lloyd(const Mat& pts, int k, int max_iter, std::mt19937_64& rng) {
+  const int64_t n = pts.rows, dim = pts.cols;
+  KMeansRun r;
+  r.centroids = km_plus_plus(pts, k, rng);
+  r.labels.assign(static_cast<size_t>(n), -1);
+  for (int iter = 0; iter < max_iter; ++iter) {
+    bool changed = false;
+    for (int64_t i = 0; i < n; ++i) {
+      int best = 0;
+      double bd = km_dist2(pts, i, r.centroids, k, 0);
+      for (int c = 1; c < k; ++c) {
+        const double dc = km_dist2(pts, i, r.centroids, k, c);
+        if (dc < bd) {
+          bd = dc;
+          best = c;
+        }
+      }
+      if (best != r.labels[static_cast<size_t>(i)]) {
+        r.labels[static_cast<size_t>(i)] = best;
+        changed = true;
+      }
+    }
+    std::vector<int64_t> counts(static_cast<size_t>(k), 0);
+    std::vector<double> sums(static_cast<size_t>(k * dim), 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+      const int c = r.labels[static_cast<size_t>(i)];
+      for (int64_t t = 0; t < dim; ++t) sums[static_cast<size_t>(t * k + c)] += pts(i, t);
+      ++counts[static_cast<size_t>(c)];
+    }
+    for (int c = 0; c < k; ++c) {
+      if (counts[static_cast<size_t>(c)] > 0) {
+        for (int64_t t = 0; t < dim; ++t)
+          r.centroids[static_cast<size_t>(t * k + c)] =
+              sums[static_cast<size_t>(t * k + c)] / static_cast<double>(counts[static_cast<size_t>(c)]);
+      } else {  // empty cluster: re-seed at the point farthest from its centroid
+        int64_t far = 0;
+        double fd = -1.0;
+        for (int64_t i = 0; i < n; ++i) {
+          const double dd = km_dist2(pts, i, r.centroids, k, r.labels[static_cast<size_t>(i)]);
+          if (dd > fd) {
+            fd = dd;
+            far = i;
+          }
+        }
+        for (int64_t t = 0; t < dim; ++t) r.centroids[static_cast<size_t>(t * k + c)] = pts(far, t);
+        r.labels[static_cast<size_t>(far)] = c;
+        changed = true;
+      }
+    }
+    if (!changed) break;
+  }
+  r.wcss = 0.0;
+  for (int64_t i = 0; i < n; ++i) r.wcss += km_dist2(pts, i, r.centroids, k, r.labels[static_cast<size_t>(i)]);
+  return r;
+}
+
+// learn.cpp:140-155
+KMeansRun km_kmeans(const Mat& pts, int k, int restarts, int max_iter, uint64_t seed) {
+  if (pts.rows < 1) fail(S_SHAPE, "k-means needs at least one point");
+  if (k < 1 || k > pts.rows) fail(S_PARAM, "cluster count must lie in [1, point count]");
+  if (restarts < 1 || max_iter < 1) fail(S_PARAM, "restarts and max_iter must be positive");
+  std::mt19937_64 rng(seed);
+  KMeansRun best;
+  best.wcss = std::numeric_limits<double>::infinity();
+  for (int a = 0; a < restarts; ++a) {
+    KMeansRun run = km_lloyd(pts, k, max_iter, rng);
+    if (run.wcss < best.wcss) best = std::move(run);
+  }
+  return best;
+}
+
+// learn.cpp:157-167: unit-normalised rows of the eigenvectors, then k-means
+Mat km_normalized_rows(const double* vectors, int64_t n, int kv) {
+  Mat rows(n, kv);
+  std::copy(vectors, vectors + n * kv, rows.a.begin());
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int t = 0; t < kv; ++t) s += rows(i, t) * rows(i, t);
+    const double norm = std::sqrt(s);
+    if (norm > 0.0)
+      for (int t = 0; t < kv; ++t) rows(i, t) /= norm;
+  }
+  return rows;
+}
+
+// learn.cpp:441-486
+double km_misclassification(const int* pred, const int* truth, int64_t n, bool permuted) {
+  if (n == 0) return 0.0;
+  if (!permuted) {
+    int64_t wrong = 0;
+    for (int64_t i = 0; i < n; ++i) wrong += pred[i] != truth[i];
+    return static_cast<double>(wrong) / static_cast<double>(n);
+  }
+  int classes = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (pred[i] < 0 || truth[i] < 0) fail(S_RANGE, "labels must be nonnegative");
+    classes = std::max(classes, std::max(pred[i], truth[i]) + 1);
+  }
+  if (classes > 8) fail(S_PARAM, "permutation matching supports at most 8 classes");
+  std::vector<int64_t> cnt(static_cast<size_t>(classes * classes), 0);
+  for (int64_t i = 0; i < n; ++i) ++cnt[static_cast<size_t>(pred[i] * classes + truth[i])];
+  std::vector<int> map(static_cast<size_t>(classes));
+  for (int c = 0; c < classes; ++c) map[static_cast<size_t>(c)] = c;
+  int64_t best = 0;
+  do {
+    int64_t matched = 0;
+    for (int p = 0; p < classes; ++p) matched += cnt[static_cast<size_t>(p * classes + map[static_cast<size_t>(p)])];
+    best = std::max(best, matched);
+  } while (std::next_permutation(map.begin(), map.end()));
+  return 1.0 - static_cast<double>(best) / static_cast<double>(n);
+}
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -1460,6 +1641,49 @@ void orc_random_vector(int64_t n, uint64_t seed, double* out) {
   std::mt19937_64 rng(seed);
   std::normal_distribution<double> dist;
   for (int64_t i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+
+int orc_kmeans(const double* points_colmajor, int64_t n, int dim, int k, int restarts, int max_iter, uint64_t seed,
+               int* labels, double* centroids, double* wcss) {
+  return guarded([&] {
+    if (n < 1) fail(S_SHAPE, "k-means needs at least one point");
+    Mat pts(n, dim);
+    std::copy(points_colmajor, points_colmajor + n * dim, pts.a.begin());
+    KMeansRun r = km_kmeans(pts, k, restarts, max_iter, seed);
+    std::copy(r.labels.begin(), r.labels.end(), labels);
+    if (centroids) std::copy(r.centroids.begin(), r.centroids.end(), centroids);
+    if (wcss) *wcss = r.wcss;
+  });
+}
+
+int orc_spectral_cluster(const double* vectors_colmajor, int64_t n, int kv, int k, int restarts, int max_iter,
+                         uint64_t seed, int* labels) {
+  return guarded([&] {
+    if (kv < k) fail(S_PARAM, "need at least as many eigenvectors as clusters");
+    Mat rows = km_normalized_rows(vectors_colmajor, n, kv);
+    KMeansRun r = km_kmeans(rows, k, restarts, max_iter, seed);
+    std::copy(r.labels.begin(), r.labels.end(), labels);
+  });
+}
+
+int orc_misclassification(const int* pred, const int* truth, int64_t n, int permuted, double* out) {
+  return guarded([&] { *out = km_misclassification(pred, truth, n, permuted != 0); });
+}
+
+// test_learn.cpp:23-39 blobs(): counts[b] points N(center_b, spread^2 I)
+void orc_blobs(const int* counts, int nb, const double* centers_rowmajor, int dim, double spread, uint64_t seed,
+               double* out_colmajor, int* labels) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, spread);
+  int64_t total = 0;
+  for (int b = 0; b < nb; ++b) total += counts[b];
+  int64_t row = 0;
+  for (int b = 0; b < nb; ++b)
+    for (int i = 0; i < counts[b]; ++i, ++row) {
+      for (int t = 0; t < dim; ++t) out_colmajor[t * total + row] = centers_rowmajor[b * dim + t] + gauss(rng);
+      labels[row] = b;
+    }
 }
 
 }  // extern "C"

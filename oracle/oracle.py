@@ -376,3 +376,50 @@ def random_vector(n, seed) -> np.ndarray:
     out = np.zeros(n)
     lib().orc_random_vector(C.c_int64(n), C.c_uint64(seed), _dp(out))
     return out
+
+
+# ---- k-means / spectral clustering (learn.cpp:17-167, 441-486) -------------
+def kmeans(points, k, restarts=10, max_iter=100, seed=1):
+    """-> (labels int32[n], centroids [k][dim], wcss)."""
+    pts = np.asarray(points, dtype=np.float64)
+    pts = pts[:, None] if pts.ndim == 1 else pts
+    n, dim = pts.shape
+    col = np.asfortranarray(pts)
+    labels = np.zeros(n, dtype=np.int32)
+    cen = np.zeros(k * dim) if k > 0 else np.zeros(1)
+    w = C.c_double()
+    _check(lib().orc_kmeans(_dp(col), C.c_int64(n), int(dim), int(k), int(restarts), int(max_iter),
+                            C.c_uint64(seed), labels.ctypes.data_as(C.POINTER(C.c_int)), _dp(cen), C.byref(w)))
+    return labels, cen[:k * dim].reshape(dim, k).T.copy(), w.value
+
+
+def spectral_cluster(vectors, k, restarts=10, max_iter=100, seed=1):
+    v = np.asfortranarray(np.asarray(vectors, dtype=np.float64))
+    n, kv = v.shape
+    labels = np.zeros(n, dtype=np.int32)
+    _check(lib().orc_spectral_cluster(_dp(v), C.c_int64(n), int(kv), int(k), int(restarts), int(max_iter),
+                                      C.c_uint64(seed), labels.ctypes.data_as(C.POINTER(C.c_int))))
+    return labels
+
+
+def misclassification_rate(pred, truth, permuted=False):
+    p = np.ascontiguousarray(pred, dtype=np.int32)
+    t = np.ascontiguousarray(truth, dtype=np.int32)
+    if p.shape != t.shape:
+        raise OracleError(3, "label vectors differ in length")
+    out = C.c_double()
+    _check(lib().orc_misclassification(p.ctypes.data_as(C.POINTER(C.c_int)), t.ctypes.data_as(C.POINTER(C.c_int)),
+                                       C.c_int64(p.size), int(permuted), C.byref(out)))
+    return out.value
+
+
+def blobs(counts, centers, spread, seed):
+    """test_learn.cpp:23-39 -> (points [n][dim], labels)."""
+    cts = np.ascontiguousarray(counts, dtype=np.int32)
+    cen = np.ascontiguousarray(centers, dtype=np.float64)
+    n, dim = int(cts.sum()), cen.shape[1]
+    out = np.zeros(n * dim)
+    labels = np.zeros(n, dtype=np.int32)
+    lib().orc_blobs(cts.ctypes.data_as(C.POINTER(C.c_int)), len(cts), _dp(cen), int(dim), C.c_double(spread),
+                    C.c_uint64(seed), _dp(out), labels.ctypes.data_as(C.POINTER(C.c_int)))
+    return out.reshape(dim, n).T.copy(), labels

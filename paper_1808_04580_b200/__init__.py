@@ -495,6 +495,73 @@ def adjacency_to_laplacian(pairs: EigenPairs) -> EigenPairs:
     return EigenPairs(vals, vecs)
 
 
+# ---- k-means / spectral clustering (learn.hpp, learn.cpp:17-167) ----------
+@dataclass
+class KMeansOptions:
+    restarts: int = 10
+    max_iter: int = 100
+    seed: int = 1
+
+
+@dataclass
+class KMeansResult:
+    labels: np.ndarray     # int32 [n]
+    centroids: np.ndarray  # [k][dim]
+    wcss: float
+
+
+def _ip(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def kmeans(points, k: int, opts: KMeansOptions = None, device: int = 0) -> KMeansResult:
+    """learn.cpp:140-155 on the device (k-means++ seeding, Lloyd, restarts)."""
+    opts = opts or KMeansOptions()
+    pts = np.asarray(points, dtype=np.float64)
+    pts = pts[:, None] if pts.ndim == 1 else pts
+    n, dim = pts.shape
+    col = np.asfortranarray(pts)
+    labels = np.zeros(n, dtype=np.int32)
+    cen = np.zeros(max(k, 1) * dim)
+    w = C.c_double()
+    _check(lib().fgs_kmeans(_dp(col), C.c_int64(n), int(dim), int(k), int(opts.restarts), int(opts.max_iter),
+                            C.c_uint64(opts.seed), int(device), _ip(labels), _dp(cen), C.byref(w)))
+    return KMeansResult(labels, cen[:k * dim].reshape(dim, k).T.copy(), w.value)
+
+
+def spectral_cluster(pairs, k_clusters: int, opts: KMeansOptions = None, device: int = 0) -> np.ndarray:
+    """learn.cpp:157-167: unit rows of the eigenvectors, then k-means.
+    ``pairs`` is an EigenPairs or an n x kv array."""
+    opts = opts or KMeansOptions()
+    vecs = pairs.vectors if isinstance(pairs, EigenPairs) else pairs
+    v = np.asfortranarray(np.asarray(vecs, dtype=np.float64))
+    n, kv = v.shape
+    labels = np.zeros(n, dtype=np.int32)
+    _check(lib().fgs_spectral_cluster(_dp(v), C.c_int64(n), int(kv), int(k_clusters), int(opts.restarts),
+                                      int(opts.max_iter), C.c_uint64(opts.seed), int(device), 0, _ip(labels)))
+    return labels
+
+
+def misclassification_rate(predicted, truth) -> float:
+    """learn.cpp:441-450."""
+    return _misclass(predicted, truth, 0)
+
+
+def misclassification_rate_permuted(predicted, truth) -> float:
+    """learn.cpp:452-486 (best relabeling, at most 8 classes)."""
+    return _misclass(predicted, truth, 1)
+
+
+def _misclass(predicted, truth, permuted):
+    p = np.ascontiguousarray(predicted, dtype=np.int32)
+    t = np.ascontiguousarray(truth, dtype=np.int32)
+    if p.shape != t.shape:
+        raise ShapeError("label vectors differ in length")
+    out = C.c_double()
+    _check(lib().fgs_misclassification_rate(_ip(p), _ip(t), C.c_int64(p.size), int(permuted), C.byref(out)))
+    return out.value
+
+
 # ---- synthetic BASELINE workloads ----------------------------------------
 def workload_info(config: int) -> dict:
     n, d, N, m, p, k = C.c_int64(), C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()

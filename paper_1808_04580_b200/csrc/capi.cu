@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "core.cuh"
+#include "kmeans.hpp"
 #include "fgs_b200.h"
 #include "lanczos.cuh"
 #include "nccl_shim.hpp"
@@ -511,6 +512,61 @@ fgs_status fgs_lanczos_largest(fgs_adjacency_t h, int which, int k, int max_iter
     if (count) *count = cnt;
     if (iterations) *iterations = r.iterations;
     if (converged) *converged = r.converged ? 1 : 0;
+  });
+}
+
+// ---- k-means / spectral clustering (learn.cpp:17-167, 441-486) -----------
+fgs_status fgs_kmeans(const double* points_colmajor, int64_t n, int dim, int k, int restarts, int max_iter,
+                      uint64_t seed, int device, int* labels, double* centroids_colmajor, double* wcss) {
+  return guard([&] {
+    need(points_colmajor, "points");
+    need(labels, "labels");
+    fgsb::kmeans_run(points_colmajor, false, n, dim, k, restarts, max_iter, seed, device, false, labels,
+                     centroids_colmajor, wcss);
+  });
+}
+
+fgs_status fgs_spectral_cluster(const double* vectors_colmajor, int64_t n, int kv, int k, int restarts, int max_iter,
+                                uint64_t seed, int device, int on_device, int* labels) {
+  return guard([&] {
+    need(vectors_colmajor, "vectors");
+    need(labels, "labels");
+    if (kv < k) fail(FGS_EPARAM, "need at least as many eigenvectors as clusters");
+    fgsb::kmeans_run(vectors_colmajor, on_device != 0, n, kv, k, restarts, max_iter, seed, device, true, labels,
+                     nullptr, nullptr);
+  });
+}
+
+fgs_status fgs_misclassification_rate(const int* predicted, const int* truth, int64_t n, int permuted, double* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = 0.0;
+    if (n == 0) return;
+    need(predicted, "predicted");
+    need(truth, "truth");
+    if (!permuted) {
+      int64_t wrong = 0;
+      for (int64_t i = 0; i < n; ++i) wrong += predicted[i] != truth[i];
+      *out = static_cast<double>(wrong) / static_cast<double>(n);
+      return;
+    }
+    int classes = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (predicted[i] < 0 || truth[i] < 0) fail(FGS_ERANGE, "labels must be nonnegative");
+      classes = std::max(classes, std::max(predicted[i], truth[i]) + 1);
+    }
+    if (classes > 8) fail(FGS_EPARAM, "permutation matching supports at most 8 classes");
+    std::vector<int64_t> cnt(static_cast<size_t>(classes) * classes, 0);
+    for (int64_t i = 0; i < n; ++i) ++cnt[static_cast<size_t>(predicted[i]) * classes + truth[i]];
+    std::vector<int> map(static_cast<size_t>(classes));
+    for (int c = 0; c < classes; ++c) map[static_cast<size_t>(c)] = c;
+    int64_t best = 0;
+    do {
+      int64_t matched = 0;
+      for (int p = 0; p < classes; ++p) matched += cnt[static_cast<size_t>(p) * classes + map[static_cast<size_t>(p)]];
+      best = std::max(best, matched);
+    } while (std::next_permutation(map.begin(), map.end()));
+    *out = 1.0 - static_cast<double>(best) / static_cast<double>(n);
   });
 }
 
