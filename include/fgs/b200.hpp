@@ -11,7 +11,10 @@
 //   graphop.hpp:45-97    AdjacencyOperator (degrees, apply_kernel/weight/normalized/
 //                        sym_laplacian)
 //   spectral.hpp:33-70   EigenPairs, LanczosOptions, LanczosInfo, lanczos_largest,
-//                        adjacency_to_laplacian
+//                        adjacency_to_laplacian, residual_norms, max_residual
+//   learn.hpp            KMeansOptions, KMeansResult, kmeans, spectral_cluster,
+//                        misclassification_rate(_permuted)
+//   graphop.hpp:19-22    AdjacencyBackend {Fastsum, Direct}
 // Differences a caller sees: lanczos_largest takes the AdjacencyOperator itself
 // (the Krylov basis stays in HBM; the reference's std::function handle would
 // copy every vector through the host), and the vector types are Eigen's when
@@ -19,6 +22,8 @@
 // below (Eigen is not installed in this build image).
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <complex>
 #include <cstdint>
 #include <stdexcept>
@@ -384,6 +389,83 @@ inline EigenPairs adjacency_to_laplacian(const EigenPairs& pairs) {
     for (Index r = 0; r < pairs.vectors.rows(); ++r) out.vectors(r, i) = pairs.vectors(r, k - 1 - i);
   }
   return out;
+}
+
+/// spectral.cpp:258-275: ||A v_j - lambda_j v_j||_2 per pair, A applied on
+/// the device (one block apply of all pairs).
+inline VectorXd residual_norms(const AdjacencyOperator& op, const EigenPairs& pairs) {
+  const Index n = op.size(), k = pairs.count();
+  if (k > 0 && pairs.vectors.rows() != n) throw ShapeError("eigenvector length does not match operator dimension");
+  VectorXd norms(k);
+  if (k == 0) return norms;
+  MatrixXd av(n, k);
+  detail::check(fgs_adjacency_apply(op.handle(), FGS_OP_NORMALIZED, pairs.vectors.data(), av.data(),
+                                    static_cast<int>(k), n));
+  for (Index j = 0; j < k; ++j) {
+    double s = 0.0;
+    for (Index i = 0; i < n; ++i) {
+      const double r = av(i, j) - pairs.values(j) * pairs.vectors(i, j);
+      s += r * r;
+    }
+    norms(j) = std::sqrt(s);
+  }
+  return norms;
+}
+
+inline double max_residual(const AdjacencyOperator& op, const EigenPairs& pairs) {
+  if (pairs.count() == 0) return 0.0;
+  VectorXd r = residual_norms(op, pairs);
+  double m = r(0);
+  for (Index j = 1; j < r.size(); ++j) m = std::max(m, r(j));
+  return m;
+}
+
+// ---- learn.hpp: k-means / spectral clustering (learn.cpp:17-167) ----------
+struct KMeansOptions {
+  int restarts = 10;
+  int max_iter = 100;
+  std::uint64_t seed = 1;
+};
+
+struct KMeansResult {
+  std::vector<int> labels;
+  MatrixXd centroids;  // k x d
+  double wcss = 0.0;
+};
+
+inline KMeansResult kmeans(const MatrixXd& points, int k, const KMeansOptions& opts = {}, int device = 0) {
+  KMeansResult r;
+  r.labels.resize(static_cast<size_t>(points.rows()));
+  r.centroids = MatrixXd(k > 0 ? k : 0, points.cols());
+  detail::check(fgs_kmeans(points.data(), points.rows(), static_cast<int>(points.cols()), k, opts.restarts,
+                           opts.max_iter, opts.seed, device, r.labels.data(), k > 0 ? r.centroids.data() : nullptr,
+                           &r.wcss));
+  return r;
+}
+
+inline std::vector<int> spectral_cluster(const EigenPairs& pairs, int k_clusters, const KMeansOptions& opts = {},
+                                         int device = 0) {
+  std::vector<int> labels(static_cast<size_t>(pairs.vectors.rows()));
+  detail::check(fgs_spectral_cluster(pairs.vectors.data(), pairs.vectors.rows(),
+                                     static_cast<int>(pairs.vectors.cols()), k_clusters, opts.restarts,
+                                     opts.max_iter, opts.seed, device, 0, labels.data()));
+  return labels;
+}
+
+inline double misclassification_rate(const std::vector<int>& predicted, const std::vector<int>& truth) {
+  if (predicted.size() != truth.size()) throw ShapeError("label vectors differ in length");
+  double r;
+  detail::check(fgs_misclassification_rate(predicted.data(), truth.data(), static_cast<std::int64_t>(predicted.size()),
+                                           0, &r));
+  return r;
+}
+
+inline double misclassification_rate_permuted(const std::vector<int>& predicted, const std::vector<int>& truth) {
+  if (predicted.size() != truth.size()) throw ShapeError("label vectors differ in length");
+  double r;
+  detail::check(fgs_misclassification_rate(predicted.data(), truth.data(), static_cast<std::int64_t>(predicted.size()),
+                                           1, &r));
+  return r;
 }
 
 }  // namespace fgs

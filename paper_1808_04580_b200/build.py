@@ -48,6 +48,7 @@ def _compile(src: str, verbose: bool) -> str:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _deps():
+        build_cli(verbose)
         return OUT
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
@@ -57,7 +58,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.run(link, check=True)
+    build_cli(verbose)
     return OUT
+
+
+CLI_SRC = os.path.join(HERE, "cli", "fgs_b200_cli.cpp")
+CLI_OUT = os.path.join(HERE, "fgs-b200")
+
+
+def build_cli(verbose: bool = False) -> str:
+    """The command-line drivers (tools/commands.cpp analogue) linked against
+    the in-tree library with an $ORIGIN rpath."""
+    if (os.path.exists(CLI_OUT) and os.path.getmtime(CLI_OUT) >= os.path.getmtime(OUT)
+            and os.path.getmtime(CLI_OUT) >= max(os.path.getmtime(CLI_SRC),
+                                                 os.path.getmtime(os.path.join(ROOT, "include", "fgs", "b200.hpp")))):
+        return CLI_OUT
+    cmd = ["g++", "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"), CLI_SRC, "-L", HERE, "-lfgs_b200",
+           "-Wl,-rpath,$ORIGIN", "-o", CLI_OUT]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return CLI_OUT
 
 
 if __name__ == "__main__":

@@ -49,7 +49,7 @@ struct Error : std::runtime_error {
 // visible -- and then allow their own successor to be scheduled, so each
 // kernel's CTAs are resident and waiting when its predecessor drains
 // instead of paying the launch gap.  A no-op when launched without the
-// attribute.  FGS_PDL=0 launches everything fully serialised.
+// attribute.  FGS_PDL selects the mode (see pdl_mode).
 // g_pdl_early: 1 = let the successor launch as soon as every CTA of this
 // grid has passed its wait (FGS_PDL=1), 0 = implicit trigger at grid end.
 __device__ int g_pdl_early;
@@ -59,8 +59,8 @@ __device__ __forceinline__ void pdl_wait() {
   if (g_pdl_early) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-// FGS_PDL: 0 off, 1 PDL launches + early trigger, 2 (default) PDL launches,
-// implicit trigger
+// FGS_PDL: 0 off, 1 PDL launches + early trigger, 2 (default) PDL launches
+// with the implicit trigger (validated with FGS_POISON=1 over the GPU suite).
 inline int pdl_mode() {
   static const int mode = [] {
     const char* e = std::getenv("FGS_PDL");

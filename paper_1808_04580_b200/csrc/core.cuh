@@ -7,6 +7,7 @@
 #include <complex>
 #include <map>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -18,6 +19,16 @@ struct Params {
   int N = 32, m = 4, p = 4;
   double eps_b = 0.0, oversampling = 2.0;
 };
+
+// FGS_POISON=1: fill every new device buffer with 0xff bytes (NaN) -- a
+// debugging aid that turns reads of never-written memory into NaNs.
+inline bool poison_allocations() {
+  static const bool on = [] {
+    const char* e = std::getenv("FGS_POISON");
+    return e && std::string(e) == "1";
+  }();
+  return on;
+}
 
 // RAII device buffer
 template <class T>
@@ -53,6 +64,10 @@ struct DBuf {
     if (count == 0) return;
     FGS_CUDA(cudaMalloc(&p, count * sizeof(T)));
     n = count;
+    if (poison_allocations()) {  // NaN bytes: exposes reads of unwritten memory
+      FGS_CUDA(cudaMemset(p, 0xff, count * sizeof(T)));
+      FGS_CUDA(cudaDeviceSynchronize());  // legacy-stream memset vs the non-blocking handle streams
+    }
   }
   void upload(const T* h, size_t count, cudaStream_t s) {
     alloc(count);

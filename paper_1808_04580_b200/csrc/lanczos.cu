@@ -100,7 +100,8 @@ __global__ void reduce_partials_kernel(const double* __restrict__ partial, int n
 // column-wise first index of the largest |v| (make_eigenpairs' convention,
 // spectral.cpp:120-124): per block (max, first index), then ordered fold
 __global__ void colmax_partial_kernel(const double* __restrict__ V, int64_t ldv, int64_t n, int chunk,
-                                      double* __restrict__ pval, int64_t* __restrict__ pidx) {
+                                      double* __restrict__ pval, int64_t* __restrict__ pidx,
+                                      double* __restrict__ psigned) {
   __shared__ double sv[256];
   __shared__ int64_t si[256];
   const int col = blockIdx.y;
@@ -130,27 +131,30 @@ __global__ void colmax_partial_kernel(const double* __restrict__ V, int64_t ldv,
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    pval[static_cast<int64_t>(col) * gridDim.x + blockIdx.x] = sv[0];
-    pidx[static_cast<int64_t>(col) * gridDim.x + blockIdx.x] = si[0];
+    const int64_t slot = static_cast<int64_t>(col) * gridDim.x + blockIdx.x;
+    pval[slot] = sv[0];
+    pidx[slot] = si[0];
+    psigned[slot] = si[0] >= 0 ? V[col * ldv + si[0]] : 0.0;  // the entry itself, before any scaling
   }
 }
 
-// sign[col] = -1 if V[first argmax |.|] < 0; then V[:, col] *= sign
+// sign[col] = -1 if V[first argmax |.|] < 0; then V[:, col] *= sign.  The
+// signed entry comes from colmax_partial_kernel: every block of a column
+// scales V in place, so no block may read V to decide the sign.
 __global__ void colsign_kernel(double* __restrict__ V, int64_t ldv, int64_t n, const double* __restrict__ pval,
-                               const int64_t* __restrict__ pidx, int nparts) {
+                               const double* __restrict__ psigned, int nparts) {
   const int col = blockIdx.y;
   __shared__ double sgn;
   if (threadIdx.x == 0) {
-    double best = -1.0;
-    int64_t bi = 0;
+    double best = -1.0, at = 0.0;
     for (int p = 0; p < nparts; ++p) {  // parts in row order: first index wins ties
       const double v = pval[static_cast<int64_t>(col) * nparts + p];
       if (v > best) {
         best = v;
-        bi = pidx[static_cast<int64_t>(col) * nparts + p];
+        at = psigned[static_cast<int64_t>(col) * nparts + p];
       }
     }
-    sgn = (n > 0 && V[col * ldv + bi] < 0.0) ? -1.0 : 1.0;
+    sgn = (n > 0 && at < 0.0) ? -1.0 : 1.0;
   }
   __syncthreads();
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
@@ -534,12 +538,13 @@ void lanczos_finish_vectors(Core& c, LanczosResult& r, const std::vector<int>& o
   unpermute_cols_kernel<<<dim3(gx, cnt), 256, 0, st>>>(r.vectors_dev.p, n, Vc.p, n, c.perm.p, dorder.p, n);
   const int chunk = 1 << 16;
   const int parts = std::max(1, ceil_div(n, chunk));
-  DBuf<double> pval;
+  DBuf<double> pval, psigned;
   DBuf<int64_t> pidx;
   pval.alloc(static_cast<size_t>(parts) * cnt);
+  psigned.alloc(static_cast<size_t>(parts) * cnt);
   pidx.alloc(static_cast<size_t>(parts) * cnt);
-  colmax_partial_kernel<<<dim3(parts, cnt), 256, 0, st>>>(Vc.p, n, n, chunk, pval.p, pidx.p);
-  colsign_kernel<<<dim3(gx, cnt), 256, 0, st>>>(Vc.p, n, n, pval.p, pidx.p, parts);
+  colmax_partial_kernel<<<dim3(parts, cnt), 256, 0, st>>>(Vc.p, n, n, chunk, pval.p, pidx.p, psigned.p);
+  colsign_kernel<<<dim3(gx, cnt), 256, 0, st>>>(Vc.p, n, n, pval.p, psigned.p, parts);
   c.launches += 3;
   FGS_CUDA(cudaMemcpyAsync(host_out, Vc.p, sizeof(double) * n * cnt, cudaMemcpyDeviceToHost, st));
   FGS_CUDA(cudaStreamSynchronize(st));

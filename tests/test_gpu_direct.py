@@ -79,3 +79,22 @@ def test_direct_nonpositive_degree_names_node(orc):
     with pytest.raises(fgs.NumericalError) as e:
         fgs.AdjacencyOperator(X, fgs.KernelSpec.gaussian(0.01), backend=fgs.BACKEND_DIRECT)
     assert e.value.bad_node == 0
+
+
+def test_block_residuals_after_lanczos_fast_and_direct(orc):
+    # regression: fast-op Lanczos, then block applies (nvec = 6) on the fast
+    # and on a freshly created direct handle must read back fully written
+    # results (stale-memory columns were once observed with PDL launches)
+    rng = np.random.default_rng(4)
+    t = rng.uniform(0, 1, 2000)
+    X = np.stack([2 * t * np.cos(6 * t), 2 * t * np.sin(6 * t), 10 * t], 1) + rng.normal(0, 0.2, (2000, 3))
+    k = fgs.KernelSpec.gaussian(3.5)
+    op = fgs.AdjacencyOperator(X, k, fgs.FastsumParams.preset(2))
+    pairs = fgs.lanczos_largest(op, 6, fgs.LanczosOptions(tol=1e-12, seed=1))
+    for _ in range(3):
+        r = np.linalg.norm(op.apply_normalized(pairs.vectors) - pairs.vectors * pairs.values, axis=0)
+        assert np.max(r) <= 1e-10
+        ex = fgs.AdjacencyOperator(X, k, backend=fgs.BACKEND_DIRECT)
+        r = np.linalg.norm(ex.apply_normalized(pairs.vectors) - pairs.vectors * pairs.values, axis=0)
+        assert np.max(r) <= 1e-5
+        del ex

@@ -259,3 +259,18 @@ def test_cpp_dropin_program_passes():
     exe = g.build_cpp_dropin_test()
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_ritz_vectors_sign_convention_is_race_free():
+    # colsign_kernel scales each column in place over many blocks; the sign
+    # must come from the pre-scaling argmax entry (a partial flip of a column
+    # once slipped through when blocks re-read the entry mid-scaling)
+    X = fgs.workload_nodes(2, 2024)[:60000]
+    op = fgs.AdjacencyOperator(X, fgs.KernelSpec.gaussian(0.05), fgs.FastsumParams(64, 6, 6, 0.0))
+    for _ in range(4):
+        pairs = fgs.lanczos_largest(op, 6, fgs.LanczosOptions(tol=1e-10))
+        AV = op.apply_normalized(pairs.vectors)
+        assert np.max(np.linalg.norm(AV - pairs.vectors * pairs.values, axis=0)) <= 1e-7
+        for j in range(6):
+            col = pairs.vectors[:, j]
+            assert col[np.argmax(np.abs(col))] > 0
