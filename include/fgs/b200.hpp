@@ -13,7 +13,9 @@
 //   spectral.hpp:33-70   EigenPairs, LanczosOptions, LanczosInfo, lanczos_largest,
 //                        adjacency_to_laplacian, residual_norms, max_residual
 //   learn.hpp            KMeansOptions, KMeansResult, kmeans, spectral_cluster,
-//                        misclassification_rate(_permuted)
+//                        misclassification_rate(_permuted), kernel_ssl_solve,
+//                        kernel_ssl_truncated, RidgeModel, krr_fit, krr_predict
+//   spectral.hpp:120-140 CgStatus, CgResult
 //   graphop.hpp:19-22    AdjacencyBackend {Fastsum, Direct}
 // Differences a caller sees: lanczos_largest takes the AdjacencyOperator itself
 // (the Krylov basis stays in HBM; the reference's std::function handle would
@@ -267,6 +269,7 @@ class FastsumPlan {
     detail::check(fgs_fastsum_apply(h_, x.data(), x.size(), y.data()));
     return y;
   }
+  fgs_fastsum_t handle() const { return h_; }
   double kernel_error_estimate(int sample_count, std::uint64_t seed) const {
     double r;
     detail::check(fgs_fastsum_error_estimate(h_, sample_count, seed, &r));
@@ -418,6 +421,100 @@ inline double max_residual(const AdjacencyOperator& op, const EigenPairs& pairs)
   double m = r(0);
   for (Index j = 1; j < r.size(); ++j) m = std::max(m, r(j));
   return m;
+}
+
+// ---- spectral.hpp:120-140 CG, learn.hpp SSL / ridge (learn.cpp:364-445) ----
+enum class CgStatus { Converged, MaxIterations, Indefinite };
+
+struct CgResult {
+  VectorXd x;
+  int iterations = 0;
+  CgStatus status = CgStatus::MaxIterations;
+  bool converged() const { return status == CgStatus::Converged; }
+};
+
+/// (I + beta L_s) u = f by conjugate gradients on the device (beta = 0: u = f)
+inline CgResult kernel_ssl_solve(const AdjacencyOperator& op, const VectorXd& f, double beta, double tol = 1e-4,
+                                 int max_iter = 1000) {
+  CgResult r;
+  r.x = VectorXd(f.size());
+  int it = 0, st = 1;
+  detail::check(fgs_kernel_ssl_solve(op.handle(), f.data(), f.size(), beta, tol, max_iter, r.x.data(), &it, &st));
+  r.iterations = it;
+  r.status = static_cast<CgStatus>(st);
+  return r;
+}
+
+/// learn.cpp:383-394: closed form in a truncated eigenbasis of A
+inline VectorXd kernel_ssl_truncated(const EigenPairs& pairs, const VectorXd& f, double beta) {
+  if (!(beta >= 0.0)) throw ParameterError("beta must be nonnegative");
+  const Index n = f.size(), k = pairs.count();
+  if (k > 0 && pairs.vectors.rows() != n) throw ShapeError("fidelity length does not match eigenvectors");
+  std::vector<double> coords(static_cast<size_t>(k), 0.0);
+  for (Index j = 0; j < k; ++j)
+    for (Index i = 0; i < n; ++i) coords[static_cast<size_t>(j)] += pairs.vectors(i, j) * f(i);
+  VectorXd out(n);
+  for (Index i = 0; i < n; ++i) {
+    double inside = 0.0, projected = 0.0;
+    for (Index j = 0; j < k; ++j) {
+      const double c = coords[static_cast<size_t>(j)];
+      inside += pairs.vectors(i, j) * (c / (1.0 + beta * (1.0 - pairs.values(j))));
+      projected += pairs.vectors(i, j) * c;
+    }
+    out(i) = inside + (f(i) - projected) / (1.0 + beta);
+  }
+  return out;
+}
+
+struct RidgeModel {
+  MatrixXd train_nodes;
+  KernelSpec kernel;
+  FastsumParams params;
+  double beta = 0.0;
+  VectorXd alpha;
+  int cg_iterations = 0;
+  double cg_tol = 0.0;
+};
+
+/// (K + beta I) alpha = f by device CG over a FastsumPlan (learn.cpp:403-430)
+inline RidgeModel krr_fit(const MatrixXd& train_nodes, const KernelSpec& kernel, double beta, const VectorXd& f,
+                          const FastsumParams& params, double tol = 1e-6, int max_iter = 1000, int device = 0) {
+  if (!(beta > 0.0)) throw ParameterError("beta must be positive");
+  if (f.size() != train_nodes.rows()) throw ShapeError("target length does not match training node count");
+  FastsumPlan plan(train_nodes, kernel, params, device);
+  RidgeModel m;
+  m.alpha = VectorXd(f.size());
+  int it = 0, st = 1;
+  detail::check(fgs_fastsum_ridge_solve(plan.handle(), f.data(), f.size(), beta, tol, max_iter, m.alpha.data(), &it,
+                                        &st));
+  if (st == 2)
+    throw NumericalError("regularized Gram operator is indefinite for this kernel; solve dense regularized normal "
+                         "equations instead");
+  m.train_nodes = train_nodes;
+  m.kernel = kernel;
+  m.params = params;
+  m.beta = beta;
+  m.cg_iterations = it;
+  m.cg_tol = tol;
+  return m;
+}
+
+/// learn.cpp:432-445: one fast summation over train + query nodes
+inline VectorXd krr_predict(const RidgeModel& model, const MatrixXd& query, int device = 0) {
+  if (query.cols() != model.train_nodes.cols()) throw ShapeError("query dimension does not match training dimension");
+  const Index nt = model.train_nodes.rows(), nq = query.rows(), d = query.cols();
+  MatrixXd all(nt + nq, d);
+  for (Index t = 0; t < d; ++t) {
+    for (Index i = 0; i < nt; ++i) all(i, t) = model.train_nodes(i, t);
+    for (Index i = 0; i < nq; ++i) all(nt + i, t) = query(i, t);
+  }
+  FastsumPlan plan(all, model.kernel, model.params, device);
+  VectorXd masked(nt + nq);
+  for (Index i = 0; i < nt + nq; ++i) masked(i) = i < nt ? model.alpha(i) : 0.0;
+  const VectorXd y = plan.apply(masked);
+  VectorXd out(nq);
+  for (Index i = 0; i < nq; ++i) out(i) = y(nt + i);
+  return out;
 }
 
 // ---- learn.hpp: k-means / spectral clustering (learn.cpp:17-167) ----------

@@ -188,6 +188,17 @@ fgs_status fgs_workload_info(int config, int64_t* n, int* d, double* sigma, int*
 fgs_status fgs_workload_generate(int config, uint64_t seed, double* nodes_colmajor);
 fgs_status fgs_workload_vectors(int64_t n, int nvec, uint64_t seed, double* out);
 
+/* ---- conjugate gradients (spectral.hpp:120-140, spectral.cpp:446-495) ---- */
+/* status: 0 converged, 1 max iterations, 2 indefinite (CgStatus).  f, x in
+ * caller order, length n.  Convergence on the true relative residual
+ * ||f - Ax|| <= tol ||f||, as the reference. */
+/* kernel_ssl_solve (learn.cpp:364-381): (I + beta L_s) x = f; beta = 0 -> x = f */
+fgs_status fgs_kernel_ssl_solve(fgs_adjacency_t h, const double* f, int64_t len, double beta, double tol,
+                                int max_iter, double* x, int* iterations, int* status);
+/* krr_fit's system (learn.cpp:403-430): (W~ + beta I) alpha = f on a FastsumPlan */
+fgs_status fgs_fastsum_ridge_solve(fgs_fastsum_t h, const double* f, int64_t len, double beta, double tol,
+                                   int max_iter, double* x, int* iterations, int* status);
+
 /* ---- k-means / spectral clustering (learn.hpp, learn.cpp:17-167) --------- */
 /* kmeans(points, k, {restarts, max_iter, seed}) (learn.cpp:140-155): points
  * column-major n x dim; labels[n]; centroids k x dim column-major and wcss

@@ -1104,6 +1104,54 @@ LanczosOut lanczos_largest(int64_t n, const ApplyFn& apply, int k, int max_iter,
 thread_local std::string g_last_error;
 
 // ---------------------------------------------------------------------------
+// cg_solve (spectral.cpp:446-495): status 0 converged, 1 max iterations,
+// 2 indefinite.  Serial dot products (Eigen's are vectorised: rounding-level
+// difference only).
+// ---------------------------------------------------------------------------
+double dotv(const std::vector<double>& a, const std::vector<double>& b) {
+  double s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+
+int cg_serial(const ApplyFn& op, const std::vector<double>& b, double tol, int max_iter, std::vector<double>& x,
+              int* iterations) {
+  if (!(tol > 0.0)) fail(S_PARAM, "tolerance must be positive");
+  if (max_iter < 1) fail(S_PARAM, "max_iter must be positive");
+  const size_t n = b.size();
+  x.assign(n, 0.0);
+  *iterations = 0;
+  const double bn = std::sqrt(dotv(b, b));
+  if (bn == 0.0) return 0;
+  std::vector<double> r = b, p = r;
+  double rs = dotv(r, r);
+  for (int it = 1; it <= max_iter; ++it) {
+    const std::vector<double> ap = op(p);
+    const double curv = dotv(p, ap);
+    *iterations = it;
+    if (!(curv > 0.0)) return 2;
+    const double step = rs / curv;
+    for (size_t i = 0; i < n; ++i) x[i] += step * p[i];
+    for (size_t i = 0; i < n; ++i) r[i] -= step * ap[i];
+    double rs_next = dotv(r, r);
+    if (std::sqrt(rs_next) <= tol * bn) {
+      const std::vector<double> ax = op(x);
+      std::vector<double> tr(n);
+      for (size_t i = 0; i < n; ++i) tr[i] = b[i] - ax[i];
+      if (std::sqrt(dotv(tr, tr)) <= tol * bn) return 0;
+      r = tr;
+      rs_next = dotv(r, r);
+      p = r;
+      rs = rs_next;
+      continue;
+    }
+    for (size_t i = 0; i < n; ++i) p[i] = r[i] + (rs_next / rs) * p[i];
+    rs = rs_next;
+  }
+  return 1;
+}
+
+// ---------------------------------------------------------------------------
 // k-means and spectral clustering (learn.cpp:17-167), label metrics
 // (learn.cpp:441-486).  Points column-major n x dim (Eigen's MatrixXd).
 // Row squared norms are left-to-right sums of squares (Eigen's scalar redux
@@ -1684,6 +1732,47 @@ void orc_blobs(const int* counts, int nb, const double* centers_rowmajor, int di
       for (int t = 0; t < dim; ++t) out_colmajor[t * total + row] = centers_rowmajor[b * dim + t] + gauss(rng);
       labels[row] = b;
     }
+}
+
+// learn.cpp:364-381 kernel_ssl_solve: (I + beta L_s) x = f
+int orc_kernel_ssl_solve(void* h, const double* f, int64_t n, double beta, double tol, int max_iter, double* x,
+                         int* iterations, int* status) {
+  return guarded([&] {
+    auto* a = static_cast<Adjacency*>(h);
+    if (!(beta >= 0.0)) fail(S_PARAM, "beta must be nonnegative");
+    if (n != a->nodes.rows) fail(S_SHAPE, "fidelity length does not match operator dimension");
+    std::vector<double> b(f, f + n), xs;
+    if (beta == 0.0) {
+      std::copy(b.begin(), b.end(), x);
+      *iterations = 0;
+      *status = 0;
+      return;
+    }
+    ApplyFn op = [a, beta, n](const std::vector<double>& v) {
+      std::vector<double> lx = a->apply_sym_laplacian(v.data(), n);
+      for (int64_t i = 0; i < n; ++i) lx[static_cast<size_t>(i)] = v[static_cast<size_t>(i)] + beta * lx[static_cast<size_t>(i)];
+      return lx;
+    };
+    *status = cg_serial(op, b, tol, max_iter, xs, iterations);
+    std::copy(xs.begin(), xs.end(), x);
+  });
+}
+
+// learn.cpp:403-430 krr_fit's system: (W~ + beta I) alpha = f
+int orc_fastsum_ridge_solve(void* h, const double* f, int64_t n, double beta, double tol, int max_iter, double* x,
+                            int* iterations, int* status) {
+  return guarded([&] {
+    auto* fs = static_cast<Fastsum*>(h);
+    if (!(beta > 0.0)) fail(S_PARAM, "beta must be positive");
+    std::vector<double> b(f, f + n), xs;
+    ApplyFn op = [fs, beta, n](const std::vector<double>& v) {
+      std::vector<double> kx = fs->apply(v.data(), n);
+      for (int64_t i = 0; i < n; ++i) kx[static_cast<size_t>(i)] = kx[static_cast<size_t>(i)] + beta * v[static_cast<size_t>(i)];
+      return kx;
+    };
+    *status = cg_serial(op, b, tol, max_iter, xs, iterations);
+    std::copy(xs.begin(), xs.end(), x);
+  });
 }
 
 }  // extern "C"

@@ -423,3 +423,23 @@ def blobs(counts, centers, spread, seed):
     lib().orc_blobs(cts.ctypes.data_as(C.POINTER(C.c_int)), len(cts), _dp(cen), int(dim), C.c_double(spread),
                     C.c_uint64(seed), _dp(out), labels.ctypes.data_as(C.POINTER(C.c_int)))
     return out.reshape(dim, n).T.copy(), labels
+
+
+# ---- conjugate gradients (spectral.cpp:446-495) ------------------------------
+def _cg(fn, h, f, beta, tol, max_iter):
+    fv = _f64(f)
+    x = np.zeros_like(fv)
+    it, st = C.c_int(), C.c_int()
+    _check(fn(h, _dp(fv), C.c_int64(fv.size), C.c_double(beta), C.c_double(tol), int(max_iter), _dp(x),
+              C.byref(it), C.byref(st)))
+    return x, it.value, st.value
+
+
+def kernel_ssl_solve(adj, f, beta, tol=1e-8, max_iter=1000):
+    """learn.cpp:364-381 -> (x, iterations, status 0/1/2)."""
+    return _cg(lib().orc_kernel_ssl_solve, adj._h, f, beta, tol, max_iter)
+
+
+def fastsum_ridge_solve(plan, f, beta, tol=1e-8, max_iter=1000):
+    """(W~ + beta I) alpha = f, krr_fit's system (learn.cpp:403-430)."""
+    return _cg(lib().orc_fastsum_ridge_solve, plan._h, f, beta, tol, max_iter)

@@ -495,6 +495,92 @@ def adjacency_to_laplacian(pairs: EigenPairs) -> EigenPairs:
     return EigenPairs(vals, vecs)
 
 
+# ---- conjugate gradients and its consumers (spectral.hpp:120-140) ---------
+CG_CONVERGED, CG_MAX_ITERATIONS, CG_INDEFINITE = 0, 1, 2  # CgStatus
+
+
+@dataclass
+class CgResult:
+    x: np.ndarray
+    iterations: int = 0
+    status: int = CG_MAX_ITERATIONS
+
+    def converged(self) -> bool:
+        return self.status == CG_CONVERGED
+
+
+def _cg_call(fn, h, f, beta, tol, max_iter, n):
+    fv = np.ascontiguousarray(f, dtype=np.float64)
+    if fv.size != n:
+        raise ShapeError("fidelity length does not match operator dimension")
+    x = np.zeros(n)
+    it, st = C.c_int(), C.c_int()
+    _check(fn(h, _dp(fv), C.c_int64(fv.size), C.c_double(beta), C.c_double(tol), int(max_iter), _dp(x),
+              C.byref(it), C.byref(st)))
+    return CgResult(x, it.value, st.value)
+
+
+def kernel_ssl_solve(op: AdjacencyOperator, f, beta: float, tol: float = 1e-4, max_iter: int = 1000) -> CgResult:
+    """learn.cpp:364-381: (I + beta L_s) x = f by CG on the device."""
+    return _cg_call(lib().fgs_kernel_ssl_solve, op.handle, f, beta, tol, max_iter, op.size())
+
+
+def kernel_ssl_truncated(pairs: "EigenPairs", f, beta: float) -> np.ndarray:
+    """learn.cpp:383-394: the same system solved in a truncated eigenbasis
+    of A (O(n k) host arithmetic on the Lanczos output)."""
+    if not beta >= 0.0:
+        raise ParameterError("beta must be nonnegative")
+    fv = np.asarray(f, dtype=np.float64)
+    V, lam = pairs.vectors, pairs.values
+    if V is not None and V.shape[1] > 0 and V.shape[0] != fv.size:
+        raise ShapeError("fidelity length does not match eigenvectors")
+    coords = V.T @ fv
+    inside = coords / (1.0 + beta * (1.0 - lam))
+    return V @ inside + (fv - V @ coords) / (1.0 + beta)
+
+
+@dataclass
+class RidgeModel:
+    train_nodes: np.ndarray
+    kernel: KernelSpec
+    params: FastsumParams
+    beta: float
+    alpha: np.ndarray
+    cg_iterations: int
+    cg_tol: float
+
+
+def krr_fit(train_nodes, kernel: KernelSpec, beta: float, f, params: FastsumParams = None, tol: float = 1e-6,
+            max_iter: int = 1000, device: int = 0) -> RidgeModel:
+    """learn.cpp:403-430: (W~ + beta I) alpha = f by CG on a device FastsumPlan."""
+    if not beta > 0.0:
+        raise ParameterError("beta must be positive")
+    params = params or FastsumParams()
+    X = np.asarray(train_nodes, dtype=np.float64)
+    X = X[:, None] if X.ndim == 1 else X
+    if np.asarray(f).size != X.shape[0]:
+        raise ShapeError("target length does not match training node count")
+    plan = FastsumPlan(X, kernel, params, device)
+    cg = _cg_call(lib().fgs_fastsum_ridge_solve, plan._h, f, beta, tol, max_iter, X.shape[0])
+    if cg.status == CG_INDEFINITE:
+        raise NumericalError("regularized Gram operator is indefinite for this kernel; solve dense regularized "
+                             "normal equations instead")
+    return RidgeModel(X.copy(), kernel, params, beta, cg.x, cg.iterations, tol)
+
+
+def krr_predict(model: RidgeModel, query_nodes, device: int = 0) -> np.ndarray:
+    """learn.cpp:432-445: one fast summation over train + query nodes."""
+    Q = np.asarray(query_nodes, dtype=np.float64)
+    Q = Q[:, None] if Q.ndim == 1 else Q
+    if Q.shape[1] != model.train_nodes.shape[1]:
+        raise ShapeError("query dimension does not match training dimension")
+    allx = np.concatenate([model.train_nodes, Q])
+    plan = FastsumPlan(allx, model.kernel, model.params, device)
+    masked = np.zeros(allx.shape[0])
+    masked[:model.train_nodes.shape[0]] = model.alpha
+    return plan.apply(masked)[model.train_nodes.shape[0]:]
+
+
 # ---- k-means / spectral clustering (learn.hpp, learn.cpp:17-167) ----------
 @dataclass
 class KMeansOptions:

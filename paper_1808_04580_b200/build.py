@@ -20,7 +20,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
-SOURCES = ["core.cu", "lanczos.cu", "capi.cu", "peak.cu", "kmeans.cu", "workload.cpp"]
+SOURCES = ["core.cu", "lanczos.cu", "capi.cu", "peak.cu", "kmeans.cu", "cg.cu", "workload.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 NVFLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-O3"]

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "core.cuh"
+#include "cg.hpp"
 #include "kmeans.hpp"
 #include "fgs_b200.h"
 #include "lanczos.cuh"
@@ -513,6 +514,31 @@ fgs_status fgs_lanczos_largest(fgs_adjacency_t h, int which, int k, int max_iter
     if (iterations) *iterations = r.iterations;
     if (converged) *converged = r.converged ? 1 : 0;
   });
+}
+
+// ---- conjugate gradients (spectral.cpp:446-495) ---------------------------
+static fgs_status cg_impl(Core* c, int system, double beta, const double* f, int64_t len, double tol, int max_iter,
+                          double* x, int* iterations, int* status) {
+  return guard([&] {
+    need(c, "handle");
+    need(f, "f");
+    need(x, "x");
+    if (len != c->n) fail(FGS_ESHAPE, "fidelity length does not match operator dimension");
+    FGS_CUDA(cudaSetDevice(c->device));
+    const fgsb::CgOutcome o = fgsb::cg_solve(*c, system == 0 ? fgsb::CG_SSL : fgsb::CG_KRR, beta, f, tol, max_iter, x);
+    if (iterations) *iterations = o.iterations;
+    if (status) *status = static_cast<int>(o.status);
+  });
+}
+
+fgs_status fgs_kernel_ssl_solve(fgs_adjacency_t h, const double* f, int64_t len, double beta, double tol,
+                                int max_iter, double* x, int* iterations, int* status) {
+  return cg_impl(h ? h->core.get() : nullptr, 0, beta, f, len, tol, max_iter, x, iterations, status);
+}
+
+fgs_status fgs_fastsum_ridge_solve(fgs_fastsum_t h, const double* f, int64_t len, double beta, double tol,
+                                   int max_iter, double* x, int* iterations, int* status) {
+  return cg_impl(h ? h->core.get() : nullptr, 1, beta, f, len, tol, max_iter, x, iterations, status);
 }
 
 // ---- k-means / spectral clustering (learn.cpp:17-167, 441-486) -----------

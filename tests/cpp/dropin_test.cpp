@@ -128,6 +128,46 @@ int main() {
     }
     CHECK(threw);
   }
+  // Direct backend, residual norms, clustering, SSL and ridge (graphop.hpp:19-22,
+  // spectral.cpp:258-275, learn.cpp:17-167, 364-445)
+  {
+    MatrixXd pts(400, 2);
+    for (int i = 0; i < 400; ++i) {
+      const double cx = (i < 200) ? -0.15 : 0.15;
+      pts(i, 0) = cx + 0.01 * std::sin(0.37 * i);
+      pts(i, 1) = 0.01 * std::cos(0.91 * i);
+    }
+    const KernelSpec k = KernelSpec::gaussian(0.05);
+    AdjacencyOperator fast(pts, k, FastsumParams::preset(3));
+    AdjacencyOperator exact(pts, k, FastsumParams::preset(3), AdjacencyBackend::Direct);
+    CHECK(exact.backend() == AdjacencyBackend::Direct);
+    EigenPairs pf = lanczos_largest(fast, 2);
+    EigenPairs pe = lanczos_largest(exact, 2);
+    CHECK(std::abs(pf.values(0) - pe.values(0)) <= 1e-8 && std::abs(pf.values(1) - pe.values(1)) <= 1e-6);
+    CHECK(max_residual(fast, pf) <= 1e-9);
+    CHECK(max_residual(exact, pf) <= 1e-5);
+    std::vector<int> labels = spectral_cluster(pf, 2);
+    std::vector<int> truth(400);
+    for (int i = 0; i < 400; ++i) truth[static_cast<size_t>(i)] = i < 200 ? 0 : 1;
+    CHECK(misclassification_rate_permuted(labels, truth) == 0.0);
+    KMeansResult km = kmeans(pts, 2);
+    CHECK(misclassification_rate_permuted(km.labels, truth) == 0.0 && km.centroids.rows() == 2);
+    VectorXd f(400);
+    for (int i = 0; i < 400; ++i) f(i) = (i % 3) - 1.0;
+    CgResult ssl = kernel_ssl_solve(fast, f, 10.0, 1e-10, 500);
+    CHECK(ssl.converged());
+    VectorXd lx = fast.apply_sym_laplacian(ssl.x);
+    double rn = 0.0, fn = 0.0;
+    for (int i = 0; i < 400; ++i) {
+      const double r = f(i) - (ssl.x(i) + 10.0 * lx(i));
+      rn += r * r;
+      fn += f(i) * f(i);
+    }
+    CHECK(std::sqrt(rn) <= 1e-10 * std::sqrt(fn));
+    RidgeModel rm = krr_fit(pts, k, 1e-2, f, FastsumParams::preset(3, 0.125), 1e-10, 500);
+    VectorXd pred = krr_predict(rm, pts);
+    CHECK(pred.size() == 400 && std::isfinite(pred(7)));
+  }
   std::printf("dropin_test: %d failure(s)\n", failures);
   return failures;
 }
