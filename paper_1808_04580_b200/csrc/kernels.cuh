@@ -264,7 +264,19 @@ __global__ void assemble_kernel(AssembleArgs a) {
   for (int v = 0; v < a.nvec; ++v) {
     const double* pv = a.priv + v * a.priv_stride;
     double acc = 0.0;
-    for (int l = b; l < e; ++l) acc += pv[a.idx[l]];
+    // batches of 4: the index loads, then the value loads, are issued
+    // back to back (two dependent latencies per batch, not per entry);
+    // the sum stays in entry order
+    int l = b;
+    for (; l + 4 <= e; l += 4) {
+      const int i0 = __ldg(a.idx + l), i1 = __ldg(a.idx + l + 1), i2 = __ldg(a.idx + l + 2), i3 = __ldg(a.idx + l + 3);
+      const double v0 = pv[i0], v1 = pv[i1], v2 = pv[i2], v3 = pv[i3];
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
+    }
+    for (; l < e; ++l) acc += pv[__ldg(a.idx + l)];
 #pragma unroll
     for (int off = 1; off < kAsmLanes; off <<= 1) acc += __shfl_down_sync(0xffffffffu, acc, off, kAsmLanes > 1 ? kAsmLanes : 32);
     if (valid && sub == 0) a.grid[v * a.grid_stride + g] = acc;
