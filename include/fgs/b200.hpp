@@ -16,6 +16,7 @@
 //                        misclassification_rate(_permuted), kernel_ssl_solve,
 //                        kernel_ssl_truncated, RidgeModel, krr_fit, krr_predict
 //   spectral.hpp:120-140 CgStatus, CgResult
+//   spectral.hpp:81-86   NystromOptions, nystrom_gaussian
 //   graphop.hpp:19-22    AdjacencyBackend {Fastsum, Direct}
 // Differences a caller sees: lanczos_largest takes the AdjacencyOperator itself
 // (the Krylov basis stays in HBM; the reference's std::function handle would
@@ -421,6 +422,31 @@ inline double max_residual(const AdjacencyOperator& op, const EigenPairs& pairs)
   double m = r(0);
   for (Index j = 1; j < r.size(); ++j) m = std::max(m, r(j));
   return m;
+}
+
+// ---- spectral.hpp:81-86 Nystrom (spectral.cpp:384-444) ---------------------
+struct NystromOptions {
+  int k = 10;
+  int L = 100;
+  int M = 10;
+  std::uint64_t seed = 1;
+};
+
+/// nystrom_gaussian(adjacency_handle(op), opts): the 2L operator applies run
+/// as block applies on the device
+inline EigenPairs nystrom_gaussian(const AdjacencyOperator& op, const NystromOptions& opts = {}) {
+  const Index n = op.size();
+  std::vector<double> vals(static_cast<size_t>(opts.k > 0 ? opts.k : 1));
+  MatrixXd vecs(n, opts.k > 0 ? opts.k : 1);
+  detail::check(fgs_nystrom_gaussian(op.handle(), opts.k, opts.L, opts.M, opts.seed, vals.data(), vecs.data()));
+  EigenPairs out;
+  out.values = VectorXd(opts.k);
+  out.vectors = MatrixXd(n, opts.k);
+  for (int i = 0; i < opts.k; ++i) {
+    out.values(i) = vals[static_cast<size_t>(i)];
+    for (Index r = 0; r < n; ++r) out.vectors(r, i) = vecs(r, i);
+  }
+  return out;
 }
 
 // ---- spectral.hpp:120-140 CG, learn.hpp SSL / ridge (learn.cpp:364-445) ----

@@ -199,6 +199,15 @@ fgs_status fgs_kernel_ssl_solve(fgs_adjacency_t h, const double* f, int64_t len,
 fgs_status fgs_fastsum_ridge_solve(fgs_fastsum_t h, const double* f, int64_t len, double beta, double tol,
                                    int max_iter, double* x, int* iterations, int* status);
 
+/* ---- Nystrom (spectral.hpp:81-86, spectral.cpp:384-444) ------------------ */
+/* nystrom_gaussian(adjacency_handle(op), {k, L, M, seed}): k approximate
+ * eigenpairs of A from a Gaussian sketch of L columns (2L fast applies) with
+ * inversion rank M; 1 <= k <= M <= L <= n.  values[k] descending, vectors
+ * n x k column-major (caller order, first-max-entry positive).  Fewer than M
+ * positive sketch eigenvalues -> FGS_ENUMERIC. */
+fgs_status fgs_nystrom_gaussian(fgs_adjacency_t h, int k, int L, int M, uint64_t seed, double* values,
+                                double* vectors);
+
 /* ---- k-means / spectral clustering (learn.hpp, learn.cpp:17-167) --------- */
 /* kmeans(points, k, {restarts, max_iter, seed}) (learn.cpp:140-155): points
  * column-major n x dim; labels[n]; centroids k x dim column-major and wcss

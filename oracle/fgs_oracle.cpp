@@ -1152,6 +1152,196 @@ int cg_serial(const ApplyFn& op, const std::vector<double>& b, double tol, int m
 }
 
 // ---------------------------------------------------------------------------
+// nystrom_gaussian (spectral.cpp:384-444).  Dense helpers standing in for
+// Eigen: Householder QR with Eigen's makeHouseholder convention (beta =
+// -sign(x0)|x|), Q formed explicitly (thin); the symmetric eigensolver is
+// Householder tridiagonalisation followed by the implicit-QL tridiag_eig,
+// ascending as SelfAdjointEigenSolver.
+// ---------------------------------------------------------------------------
+// thin QR of the r x c column-major A: Q (r x c) and R (c x c upper)
+void householder_qr(const Mat& A, Mat& Q, Mat& R) {
+  const int64_t r = A.rows, c = A.cols;
+  Mat W = A;
+  std::vector<std::vector<double>> vs;
+  std::vector<double> taus;
+  const int64_t steps = std::min(r, c);
+  for (int64_t j = 0; j < steps; ++j) {
+    double sq = 0.0;
+    for (int64_t i = j + 1; i < r; ++i) sq += W(i, j) * W(i, j);
+    const double c0 = W(j, j);
+    std::vector<double> v(static_cast<size_t>(r - j), 0.0);
+    double tau = 0.0, beta = c0;
+    if (sq > 0.0) {
+      beta = std::sqrt(c0 * c0 + sq);
+      if (c0 >= 0.0) beta = -beta;
+      v[0] = 1.0;
+      for (int64_t i = j + 1; i < r; ++i) v[static_cast<size_t>(i - j)] = W(i, j) / (c0 - beta);
+      tau = (beta - c0) / beta;
+    } else {
+      v[0] = 1.0;
+    }
+    W(j, j) = beta;
+    for (int64_t i = j + 1; i < r; ++i) W(i, j) = 0.0;
+    for (int64_t k = j + 1; k < c; ++k) {  // apply H = I - tau v v^T to the trailing columns
+      double dot = 0.0;
+      for (int64_t i = j; i < r; ++i) dot += v[static_cast<size_t>(i - j)] * W(i, k);
+      dot *= tau;
+      for (int64_t i = j; i < r; ++i) W(i, k) -= dot * v[static_cast<size_t>(i - j)];
+    }
+    vs.push_back(std::move(v));
+    taus.push_back(tau);
+  }
+  R = Mat(c, c);
+  for (int64_t k = 0; k < c; ++k)
+    for (int64_t i = 0; i <= std::min(k, r - 1); ++i) R(i, k) = W(i, k);
+  Q = Mat(r, c);  // Q = H_0 ... H_{s-1} [I; 0]
+  for (int64_t k = 0; k < std::min(r, c); ++k) Q(k, k) = 1.0;
+  for (int64_t j = steps - 1; j >= 0; --j) {
+    const std::vector<double>& v = vs[static_cast<size_t>(j)];
+    const double tau = taus[static_cast<size_t>(j)];
+    for (int64_t k = 0; k < c; ++k) {
+      double dot = 0.0;
+      for (int64_t i = j; i < r; ++i) dot += v[static_cast<size_t>(i - j)] * Q(i, k);
+      dot *= tau;
+      for (int64_t i = j; i < r; ++i) Q(i, k) -= dot * v[static_cast<size_t>(i - j)];
+    }
+  }
+}
+
+// symmetric s x s: ascending eigenvalues, eigenvectors as columns
+void dense_sym_eig(const Mat& A, std::vector<double>& vals, Mat& vecs) {
+  const int64_t s = A.rows;
+  Mat T = A, Qt(s, s);
+  for (int64_t i = 0; i < s; ++i) Qt(i, i) = 1.0;
+  // Householder tridiagonalisation: T <- H T H, Qt <- Qt H
+  for (int64_t j = 0; j + 2 < s; ++j) {
+    double sq = 0.0;
+    for (int64_t i = j + 2; i < s; ++i) sq += T(i, j) * T(i, j);
+    if (sq == 0.0) continue;
+    const double c0 = T(j + 1, j);
+    double beta = std::sqrt(c0 * c0 + sq);
+    if (c0 >= 0.0) beta = -beta;
+    std::vector<double> v(static_cast<size_t>(s), 0.0);
+    v[static_cast<size_t>(j + 1)] = 1.0;
+    for (int64_t i = j + 2; i < s; ++i) v[static_cast<size_t>(i)] = T(i, j) / (c0 - beta);
+    const double tau = (beta - c0) / beta;
+    for (int64_t k = 0; k < s; ++k) {  // T <- H T
+      double dot = 0.0;
+      for (int64_t i = j + 1; i < s; ++i) dot += v[static_cast<size_t>(i)] * T(i, k);
+      dot *= tau;
+      for (int64_t i = j + 1; i < s; ++i) T(i, k) -= dot * v[static_cast<size_t>(i)];
+    }
+    for (int64_t k = 0; k < s; ++k) {  // T <- T H, Qt <- Qt H
+      double dot = 0.0, dq = 0.0;
+      for (int64_t i = j + 1; i < s; ++i) {
+        dot += T(k, i) * v[static_cast<size_t>(i)];
+        dq += Qt(k, i) * v[static_cast<size_t>(i)];
+      }
+      dot *= tau;
+      dq *= tau;
+      for (int64_t i = j + 1; i < s; ++i) {
+        T(k, i) -= dot * v[static_cast<size_t>(i)];
+        Qt(k, i) -= dq * v[static_cast<size_t>(i)];
+      }
+    }
+  }
+  std::vector<double> diag(static_cast<size_t>(s)), sub(static_cast<size_t>(std::max<int64_t>(s - 1, 0)));
+  for (int64_t i = 0; i < s; ++i) diag[static_cast<size_t>(i)] = T(i, i);
+  for (int64_t i = 0; i + 1 < s; ++i) sub[static_cast<size_t>(i)] = T(i + 1, i);
+  std::vector<double> z;
+  tridiag_eig(static_cast<int>(s), diag, sub, z);
+  vals = diag;
+  vecs = Mat(s, s);
+  for (int64_t k = 0; k < s; ++k)
+    for (int64_t i = 0; i < s; ++i) {
+      double acc = 0.0;
+      for (int64_t t = 0; t < s; ++t) acc += Qt(i, t) * z[static_cast<size_t>(k * s + t)];
+      vecs(i, k) = acc;
+    }
+}
+
+// spectral.cpp:384-444 over any operator
+void nystrom_gaussian_serial(int64_t n, const ApplyFn& op, int k, int L, int M, uint64_t seed, std::vector<double>& values,
+                             Mat& vectors) {
+  if (k < 1 || M < k || L < M || L > n) fail(S_PARAM, "need 1 <= k <= M <= L <= n");
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss;
+  Mat probes(n, L);
+  for (int64_t c = 0; c < L; ++c)
+    for (int64_t r = 0; r < n; ++r) probes(r, c) = gauss(rng);
+  Mat sketch(n, L);
+  for (int64_t c = 0; c < L; ++c) {
+    std::vector<double> x(probes.col(c), probes.col(c) + n);
+    const std::vector<double> y = op(x);
+    std::copy(y.begin(), y.end(), sketch.col(c));
+  }
+  Mat q, r;
+  householder_qr(sketch, q, r);
+  Mat b1(n, L);
+  for (int64_t c = 0; c < L; ++c) {
+    std::vector<double> x(q.col(c), q.col(c) + n);
+    const std::vector<double> y = op(x);
+    std::copy(y.begin(), y.end(), b1.col(c));
+  }
+  Mat b2(L, L);
+  for (int64_t j = 0; j < L; ++j)
+    for (int64_t i = 0; i < L; ++i) {
+      double acc = 0.0;
+      for (int64_t t = 0; t < n; ++t) acc += q(t, i) * b1(t, j);
+      b2(i, j) = acc;
+    }
+  Mat b2s(L, L);
+  for (int64_t j = 0; j < L; ++j)
+    for (int64_t i = 0; i < L; ++i) b2s(i, j) = 0.5 * (b2(i, j) + b2(j, i));
+  std::vector<double> ev;
+  Mat evec;
+  dense_sym_eig(b2s, ev, evec);
+  int positives = 0;
+  for (double v : ev) positives += v > 0.0;
+  if (positives < M)
+    fail(S_NUMERIC, "sketch captured fewer than the requested number of positive eigenvalues; increase the sketch size");
+  std::vector<double> sigma(static_cast<size_t>(M));
+  Mat um(L, M);
+  for (int i = 0; i < M; ++i) {
+    sigma[static_cast<size_t>(i)] = ev[static_cast<size_t>(L - 1 - i)];
+    for (int64_t t = 0; t < L; ++t) um(t, i) = evec(t, L - 1 - i);
+  }
+  Mat bu(n, M);
+  for (int64_t j = 0; j < M; ++j)
+    for (int64_t i = 0; i < n; ++i) {
+      double acc = 0.0;
+      for (int64_t t = 0; t < L; ++t) acc += b1(i, t) * um(t, j);
+      bu(i, j) = acc;
+    }
+  Mat qh, rh;
+  householder_qr(bu, qh, rh);
+  Mat mid(M, M);
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t j = 0; j < M; ++j) {
+      double acc = 0.0;
+      for (int64_t t = 0; t < M; ++t) acc += rh(i, t) / sigma[static_cast<size_t>(t)] * rh(j, t);
+      mid(i, j) = acc;
+    }
+  Mat mids(M, M);
+  for (int64_t j = 0; j < M; ++j)
+    for (int64_t i = 0; i < M; ++i) mids(i, j) = 0.5 * (mid(i, j) + mid(j, i));
+  std::vector<double> mv;
+  Mat mvec;
+  dense_sym_eig(mids, mv, mvec);
+  values.assign(static_cast<size_t>(k), 0.0);
+  Mat raw(n, k);
+  for (int i = 0; i < k; ++i) {
+    values[static_cast<size_t>(i)] = mv[static_cast<size_t>(M - 1 - i)];
+    for (int64_t row = 0; row < n; ++row) {
+      double acc = 0.0;
+      for (int64_t t = 0; t < M; ++t) acc += qh(row, t) * mvec(t, M - 1 - i);
+      raw(row, i) = acc;
+    }
+  }
+  vectors = raw;
+}
+
+// ---------------------------------------------------------------------------
 // k-means and spectral clustering (learn.cpp:17-167), label metrics
 // (learn.cpp:441-486).  Points column-major n x dim (Eigen's MatrixXd).
 // Row squared norms are left-to-right sums of squares (Eigen's scalar redux
@@ -1773,6 +1963,39 @@ int orc_fastsum_ridge_solve(void* h, const double* f, int64_t n, double beta, do
     *status = cg_serial(op, b, tol, max_iter, xs, iterations);
     std::copy(xs.begin(), xs.end(), x);
   });
+}
+
+static int nystrom_out(int64_t n, const ApplyFn& fn, int k, int L, int M, uint64_t seed, double* values,
+                       double* vectors) {
+  return guarded([&] {
+    std::vector<double> v;
+    Mat vec;
+    nystrom_gaussian_serial(n, fn, k, L, M, seed, v, vec);
+    const EigenPairs p = make_eigenpairs(v, vec);  // spectral.cpp:105-127
+    std::copy(p.values.begin(), p.values.end(), values);
+    std::copy(p.vectors.a.begin(), p.vectors.a.end(), vectors);
+  });
+}
+
+int orc_nystrom_dense(const double* A, int64_t n, int k, int L, int M, uint64_t seed, double* values, double* vectors) {
+  std::vector<double> mat(A, A + n * n);
+  ApplyFn fn = [&mat, n](const std::vector<double>& x) {
+    std::vector<double> y(static_cast<size_t>(n), 0.0);
+    for (int64_t j = 0; j < n; ++j) {
+      const double xj = x[j];
+      const double* c = mat.data() + j * n;
+      for (int64_t i = 0; i < n; ++i) y[i] += c[i] * xj;
+    }
+    return y;
+  };
+  return nystrom_out(n, fn, k, L, M, seed, values, vectors);
+}
+
+int orc_nystrom_adjacency(void* h, int k, int L, int M, uint64_t seed, double* values, double* vectors) {
+  auto* a = static_cast<Adjacency*>(h);
+  const int64_t n = a->nodes.rows;
+  ApplyFn fn = [a, n](const std::vector<double>& x) { return a->apply_normalized(x.data(), n); };
+  return nystrom_out(n, fn, k, L, M, seed, values, vectors);
 }
 
 }  // extern "C"

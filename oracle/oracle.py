@@ -443,3 +443,22 @@ def kernel_ssl_solve(adj, f, beta, tol=1e-8, max_iter=1000):
 def fastsum_ridge_solve(plan, f, beta, tol=1e-8, max_iter=1000):
     """(W~ + beta I) alpha = f, krr_fit's system (learn.cpp:403-430)."""
     return _cg(lib().orc_fastsum_ridge_solve, plan._h, f, beta, tol, max_iter)
+
+
+# ---- nystrom_gaussian (spectral.cpp:384-444) ----------------------------------
+def _nystrom(fn, head, n, k, L, M, seed):
+    vals = np.zeros(k)
+    vecs = np.zeros(n * k)
+    _check(fn(*head, int(k), int(L), int(M), C.c_uint64(seed), _dp(vals), _dp(vecs)))
+    return vals, vecs.reshape(k, n).T.copy()
+
+
+def nystrom_dense(A, k, L, M, seed=1):
+    A = np.asfortranarray(np.asarray(A, dtype=np.float64))
+    n = A.shape[0]
+    flat = A.ravel(order="F").copy()
+    return _nystrom(lib().orc_nystrom_dense, (_dp(flat), C.c_int64(n)), n, k, L, M, seed)
+
+
+def nystrom_adjacency(adj, n, k, L, M, seed=1):
+    return _nystrom(lib().orc_nystrom_adjacency, (adj._h,), n, k, L, M, seed)

@@ -495,6 +495,27 @@ def adjacency_to_laplacian(pairs: EigenPairs) -> EigenPairs:
     return EigenPairs(vals, vecs)
 
 
+# ---- Nystrom (spectral.hpp:81-86, spectral.cpp:384-444) -------------------
+@dataclass
+class NystromOptions:
+    k: int = 10
+    L: int = 100
+    M: int = 10
+    seed: int = 1
+
+
+def nystrom_gaussian(op: AdjacencyOperator, opts: NystromOptions = None) -> EigenPairs:
+    """k approximate eigenpairs of A from a Gaussian sketch (2L fast applies,
+    as block applies on the device)."""
+    opts = opts or NystromOptions()
+    n = op.size()
+    vals = np.zeros(max(opts.k, 1))
+    vecs = np.zeros((n, max(opts.k, 1)), order="F")
+    _check(lib().fgs_nystrom_gaussian(op.handle, int(opts.k), int(opts.L), int(opts.M), C.c_uint64(opts.seed),
+                                      _dp(vals), _dp(vecs)))
+    return EigenPairs(vals[:opts.k].copy(), vecs[:, :opts.k].copy())
+
+
 # ---- conjugate gradients and its consumers (spectral.hpp:120-140) ---------
 CG_CONVERGED, CG_MAX_ITERATIONS, CG_INDEFINITE = 0, 1, 2  # CgStatus
 

@@ -20,7 +20,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
-SOURCES = ["core.cu", "lanczos.cu", "capi.cu", "peak.cu", "kmeans.cu", "cg.cu", "workload.cpp"]
+SOURCES = ["core.cu", "lanczos.cu", "capi.cu", "peak.cu", "kmeans.cu", "cg.cu", "nystrom.cu", "workload.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 NVFLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-O3"]
@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     link = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs + [
-        "-L", os.path.join(CUDA, "lib64"), "-lcufft", "-lcudart", "-ldl",
+        "-L", os.path.join(CUDA, "lib64"), "-lcufft", "-lcusolver", "-lcublas", "-lcudart", "-ldl",
         "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64")]
     if verbose:
         print(" ".join(link), flush=True)

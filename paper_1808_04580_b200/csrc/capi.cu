@@ -8,6 +8,7 @@
 
 #include "core.cuh"
 #include "cg.hpp"
+#include "nystrom.hpp"
 #include "kmeans.hpp"
 #include "fgs_b200.h"
 #include "lanczos.cuh"
@@ -539,6 +540,19 @@ fgs_status fgs_kernel_ssl_solve(fgs_adjacency_t h, const double* f, int64_t len,
 fgs_status fgs_fastsum_ridge_solve(fgs_fastsum_t h, const double* f, int64_t len, double beta, double tol,
                                    int max_iter, double* x, int* iterations, int* status) {
   return cg_impl(h ? h->core.get() : nullptr, 1, beta, f, len, tol, max_iter, x, iterations, status);
+}
+
+// ---- nystrom_gaussian (spectral.cpp:384-444) --------------------------------
+fgs_status fgs_nystrom_gaussian(fgs_adjacency_t h, int k, int L, int M, uint64_t seed, double* values, double* vectors) {
+  return guard([&] {
+    need(h, "handle");
+    need(values, "values");
+    need(vectors, "vectors");
+    Core& c = *h->core;
+    FGS_CUDA(cudaSetDevice(c.device));
+    const std::vector<double> v = fgsb::nystrom_gaussian(c, k, L, M, seed, vectors);
+    std::copy(v.begin(), v.end(), values);
+  });
 }
 
 // ---- k-means / spectral clustering (learn.cpp:17-167, 441-486) -----------

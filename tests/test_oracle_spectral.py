@@ -120,3 +120,49 @@ def test_perron_identity(orc):
     direction /= np.linalg.norm(direction)
     assert abs(vals[0] - 1.0) <= 1e-8
     assert np.linalg.norm(op.apply_normalized(direction) - direction) <= 1e-8
+
+
+# ---- nystrom_gaussian (test_spectral.cpp:265-316) ----------------------------
+def _signed_top(A, k):
+    w, V = np.linalg.eigh(A)
+    out = []
+    for i in range(k):
+        v = V[:, -1 - i]
+        out.append(v if v[np.argmax(np.abs(v))] > 0 else -v)
+    return w[::-1][:k], np.stack(out, 1)
+
+
+def test_gaussian_sketch_recovers_low_rank_operator(orc):
+    spectrum = np.zeros(40)
+    spectrum[:3] = [3.0, 2.0, 1.0]
+    A = with_spectrum(spectrum, 83)
+    vals, vecs = orc.nystrom_dense(A, 3, 6, 3, seed=5)
+    ev, V = _signed_top(A, 3)
+    for i in range(3):
+        assert approx(vals[i], ev[i], 1e-8)
+        assert np.linalg.norm(vecs[:, i] - V[:, i]) <= 1e-6
+    assert np.max(np.abs(vecs.T @ vecs - np.eye(3))) <= 1e-8
+
+
+def test_gaussian_sketch_deterministic_and_rank_deficiency(orc):
+    A = with_spectrum(0.7 ** np.arange(30), 91)
+    a = orc.nystrom_dense(A, 4, 12, 6, seed=17)
+    b = orc.nystrom_dense(A, 4, 12, 6, seed=17)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    with pytest.raises(orc.OracleError) as e:
+        orc.nystrom_dense(np.zeros((20, 20)), 2, 6, 3)
+    assert e.value.kind == "NumericalError"
+    for args in ((0, 6, 3), (4, 6, 3), (2, 6, 7), (2, 30, 3)):
+        with pytest.raises(orc.OracleError) as e:
+            orc.nystrom_dense(np.eye(20), *args)
+        assert e.value.kind == "ParameterError"
+
+
+def test_householder_qr_and_dense_eig_helpers(orc):
+    # full sketch (L = n) of a full-rank operator reproduces its top pairs
+    rng = np.random.default_rng(3)
+    A = with_spectrum(np.linspace(2.0, 0.1, 25), 4)
+    vals, vecs = orc.nystrom_dense(A, 5, 25, 25, seed=2)
+    ev, V = _signed_top(A, 5)
+    assert np.max(np.abs(vals - ev)) <= 1e-10
+    assert np.max(np.abs(vecs - V)) <= 1e-8
