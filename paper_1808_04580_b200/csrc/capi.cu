@@ -360,6 +360,10 @@ fgs_status fgs_adjacency_apply(fgs_adjacency_t h, fgs_op op, const double* x, do
     bool scale = false;
     const int epi = epilogue_of(op, &scale);
     FGS_CUDA(cudaSetDevice(c.device));
+    if (c.apply_host_graph(epi, x, y, ld, nvec, scale)) {  // pinned x / y: copies inside the graph
+      FGS_CUDA(cudaStreamSynchronize(c.stream));
+      return;
+    }
     upload_block(c, c.xbuf, x, c.n, nvec, ld);
     c.ybuf.alloc(static_cast<size_t>(c.n) * nvec);
     c.apply(epi, c.xbuf.p, c.n, c.ybuf.p, c.n, nvec, true, scale);

@@ -1036,6 +1036,73 @@ void Core::apply(int epilogue, const double* x, int64_t ldx, double* y, int64_t 
   launches += graphs_.back().launches;
 }
 
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+bool Core::apply_host_graph(int epilogue, const double* hx, double* hy, int64_t ld, int nvec, bool scale_input) {
+  static const bool graphs_on = [] {
+    const char* e = std::getenv("FGS_GRAPHS");
+    const char* h = std::getenv("FGS_HOST_GRAPH");
+    return !(e && std::string(e) == "0") && !(h && std::string(h) == "0");
+  }();
+  if (!graphs_on || profile_ || stream == nullptr || sharded || world > 1) return false;
+  if (!is_pinned(hx) || !is_pinned(hy)) return false;  // checked every call: an address may be reused
+  xbuf.alloc(static_cast<size_t>(n) * nvec);
+  ybuf.alloc(static_cast<size_t>(n) * nvec);
+  GraphKey key{epilogue, xbuf.p, n, ybuf.p, n, nvec, true, scale_input};
+  key.hx = hx;
+  key.hy = hy;
+  key.hld = ld;
+  for (auto& g : graphs_) {
+    if (g.key == key) {
+      FGS_CUDA(cudaGraphLaunch(g.exec, stream));
+      launches += g.launches;
+      return true;
+    }
+  }
+  workspace(nvec);
+  const int64_t before = launches;
+  FGS_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    if (ld == n)
+      FGS_CUDA(cudaMemcpyAsync(xbuf.p, hx, sizeof(double) * n * nvec, cudaMemcpyHostToDevice, stream));
+    else
+      FGS_CUDA(cudaMemcpy2DAsync(xbuf.p, sizeof(double) * n, hx, sizeof(double) * ld, sizeof(double) * n, nvec,
+                                 cudaMemcpyHostToDevice, stream));
+    apply_launches(epilogue, xbuf.p, n, ybuf.p, n, nvec, true, scale_input);
+    if (ld == n)
+      FGS_CUDA(cudaMemcpyAsync(hy, ybuf.p, sizeof(double) * n * nvec, cudaMemcpyDeviceToHost, stream));
+    else
+      FGS_CUDA(cudaMemcpy2DAsync(hy, sizeof(double) * ld, ybuf.p, sizeof(double) * n, sizeof(double) * n, nvec,
+                                 cudaMemcpyDeviceToHost, stream));
+  } catch (...) {
+    cudaGraph_t broken = nullptr;
+    cudaStreamEndCapture(stream, &broken);
+    if (broken) cudaGraphDestroy(broken);
+    throw;
+  }
+  cudaGraph_t graph = nullptr;
+  FGS_CUDA(cudaStreamEndCapture(stream, &graph));
+  cudaGraphExec_t exec = nullptr;
+  FGS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  if (graphs_.size() >= 8) {
+    cudaGraphExecDestroy(graphs_.front().exec);
+    graphs_.erase(graphs_.begin());
+  }
+  graphs_.push_back({key, exec, launches - before});
+  launches = before;
+  FGS_CUDA(cudaGraphLaunch(exec, stream));
+  launches += graphs_.back().launches;
+  return true;
+}
+
 void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
                           bool caller_order, bool scale_input) {
   Workspace& w = workspace(nvec);

@@ -145,6 +145,10 @@ class Core {
   // indexing), else local-slice internal order.
   void apply(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
              bool caller_order, bool scale_input);
+  // y_host = op(x_host) as ONE graph (H2D into xbuf, the apply, D2H from
+  // ybuf) when both host buffers are pinned; false -> caller stages itself.
+  // Does not synchronise.
+  bool apply_host_graph(int epilogue, const double* hx, double* hy, int64_t ld, int nvec, bool scale_input);
   void compute_degrees(int64_t* bad_node);
 
   // complex NFFT transforms (NfftPlan), interleaved complex on device
@@ -173,9 +177,12 @@ class Core {
     int64_t ldy;
     int nvec;
     bool caller_order, scale;
+    const double* hx = nullptr;  // host-vector graphs: pinned x / y with their leading dimension
+    double* hy = nullptr;
+    int64_t hld = 0;
     bool operator==(const GraphKey& o) const {
       return epi == o.epi && x == o.x && ldx == o.ldx && y == o.y && ldy == o.ldy && nvec == o.nvec &&
-             caller_order == o.caller_order && scale == o.scale;
+             caller_order == o.caller_order && scale == o.scale && hx == o.hx && hy == o.hy && hld == o.hld;
     }
   };
   struct GraphEntry {
