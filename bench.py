@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--nvec", type=int, default=0, help="vectors per step (0: 16 for config 5, else 1)")
     p.add_argument("--no-lanczos", action="store_true")
+    p.add_argument("--force-sharded", action="store_true",
+                   help=argparse.SUPPRESS)  # run the sharded (NCCL) path even at world size 1 (under torchrun)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--also", default="4", help="comma list of extra configs measured after the main line "
@@ -261,15 +263,16 @@ def run_b200(args, rank, world, local_rank):
     params = fgs.FastsumParams(info["N"], info["m"], info["p"], 0.0)
     kernel = fgs.KernelSpec.gaussian(info["sigma"])
 
+    sharded = world > 1 or args.force_sharded
     dist = None
-    if world > 1:
+    if sharded:
         import torch.distributed as dist
         nid = [fgs.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(nid, src=0)
         nccl_id = nid[0]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    if world > 1:
+    if sharded:
         op = fgs.AdjacencyOperator(X, kernel, params, device=dev, rank=rank, world=world, nccl_id=nccl_id)
     else:
         op = fgs.AdjacencyOperator(X, kernel, params, device=dev)
@@ -370,7 +373,7 @@ def run_b200(args, rank, world, local_rank):
 
     # ---- end to end through the public API with pinned host buffers ---------
     e2e = None
-    if world == 1:
+    if not sharded:
         hx = torch.from_numpy(np.asfortranarray(xs_host)).pin_memory()
         hy = torch.empty_like(hx).pin_memory()
         import ctypes as C
@@ -392,9 +395,38 @@ def run_b200(args, rank, world, local_rank):
                "d2h_bytes_per_step": 8 * n * nvec, "ms_per_step": e2e_ms,
                "path": "fgs_adjacency_apply (C ABI) with pinned host x/y, caller order"}
 
+    else:
+        # sharded handles take device vectors in the internal order (the
+        # public multi-GPU API, fgs_adjacency_apply_device): each rank uploads
+        # its slice from pinned memory, applies, downloads; max over ranks
+        hx = x_int.cpu().pin_memory()
+        hy = torch.empty_like(hx).pin_memory()
+        for _ in range(args.warmup):
+            x_int.copy_(hx, non_blocking=True)
+            step()
+            hy.copy_(y_int, non_blocking=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            x_int.copy_(hx, non_blocking=True)
+            step()
+            hy.copy_(y_int, non_blocking=True)
+            stream.synchronize()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        e2e = {"value": nvec / (e2e_ms / 1000.0), "unit": "matvecs/s", "h2d_bytes_per_step": 8 * n * nvec,
+               "d2h_bytes_per_step": 8 * n * nvec, "ms_per_step": e2e_ms,
+               "path": "per rank: pinned slice H2D + fgs_adjacency_apply_device (sharded, internal order) + D2H; "
+                       "max over ranks"}
+
     # ---- Lanczos time-to-k (spectral.cpp:141-256 via the device path) -------
     lanczos = None
-    if world == 1 and not args.no_lanczos and args.config <= 4:
+    if not sharded and not args.no_lanczos and args.config <= 4:
         li = fgs.LanczosInfo()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -407,13 +439,13 @@ def run_b200(args, rank, world, local_rank):
 
     # ---- CPU baseline (rank 0, N=1) ----------------------------------------
     cpu = None
-    if world == 1 and not args.no_cpu:
+    if not sharded and not args.no_cpu:
         rate, desc, csetup = cpu_matvecs_per_s(args.config, X, info, nvec, args.cpu_seconds)
         cpu = {"value": rate, "unit": "matvecs/s", "cores": 1, "kind": "port", "sample": desc,
                "cpu": cpu_model(), "host_cores": os.cpu_count(), "setup_s": csetup}
 
     also = []
-    if world == 1 and args.also:
+    if not sharded and args.also:
         for cfg in [int(c) for c in args.also.split(",") if c.strip()]:
             if cfg != args.config:
                 try:
@@ -429,7 +461,7 @@ def run_b200(args, rank, world, local_rank):
             "data": "synthetic (seeded stand-in for the paper's datasets)",
             "config": {"workload": f"config{args.config}", "n": n, "d": info["d"], "sigma": info["sigma"],
                        "N": info["N"], "m": info["m"], "p": info["p"], "nvec": nvec, "op": "L_s x",
-                       "parallelism": f"points sharded x{world}" if world > 1 else "single GPU",
+                       "parallelism": f"points sharded x{world}" if sharded else "single GPU",
                        "l2": "flushed (256 MB write) between timed steps, outside the events"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(w0, w1), "lanczos": lanczos, "setup_s": setup_s, "also": also,
@@ -442,7 +474,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and args.impl == "b200":
+    if (world > 1 or args.force_sharded) and args.impl == "b200":
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
@@ -451,7 +483,7 @@ def main():
         run_reference(args, rank, world)
     else:
         run_b200(args, rank, world, local_rank)
-    if world > 1 and args.impl == "b200":
+    if (world > 1 or args.force_sharded) and args.impl == "b200":
         import torch.distributed as dist
         dist.destroy_process_group()
 
