@@ -230,6 +230,26 @@ size_t v4_stage_doubles(V4Var v) {
   return one(Blk4<T, INTERP, 0, 0>{});
 }
 
+// private spread boxes of the variant in use (P when P >= 4, else one shared box)
+int v4_spread_groups(int T) {
+  const V4Var v = v4_variant(false);
+  auto pick = [&](auto tag) -> int {
+    constexpr int TT = decltype(tag)::value;
+#define FGS_V4P(PP, QQ) \
+  if (v.p == PP && v.qs == QQ) return Blk4<TT, false, PP, QQ>::P >= 4 ? Blk4<TT, false, PP, QQ>::P : 1;
+    FGS_V4P(0, 0) FGS_V4P(0, 32) FGS_V4P(0, 64) FGS_V4P(1, 32) FGS_V4P(1, 64) FGS_V4P(2, 32) FGS_V4P(2, 64)
+    FGS_V4P(4, 32) FGS_V4P(4, 64)
+#undef FGS_V4P
+    return Blk4<TT, false, 0, 0>::P >= 4 ? Blk4<TT, false, 0, 0>::P : 1;
+  };
+  switch (T) {
+    case 8: return pick(std::integral_constant<int, 8>{});
+    case 12: return pick(std::integral_constant<int, 12>{});
+    case 16: return pick(std::integral_constant<int, 16>{});
+    default: return 1;
+  }
+}
+
 template <int T, bool INTERP>
 void v4_launch(V4Var v, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
 #define FGS_V4L(PP, QQ)                                                               \
@@ -947,7 +967,9 @@ Workspace& Core::workspace(int nvec) {
 size_t Core::smem_bytes(bool interp) const {
   const bool dense = mean_run >= kDenseRun;
   const LaunchShape sh = d == 3 ? shape_of<3>(T, dense) : (d == 2 ? shape_of<2>(T, dense) : shape_of<1>(T, dense));
-  return (static_cast<size_t>(box_stride) + (interp ? sh.extra_interp : sh.extra_spread)) * sizeof(double);
+  size_t boxes = static_cast<size_t>(box_stride);
+  if (d == 3 && !interp && dense && use_v4()) boxes *= static_cast<size_t>(v4_spread_groups(T));  // per-group boxes
+  return (boxes + (interp ? sh.extra_interp : sh.extra_spread)) * sizeof(double);
 }
 
 void Core::launch_spread(const PassArgs& a) {

@@ -239,8 +239,13 @@ __global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE;
   constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, NE = B::NE;
   extern __shared__ __align__(16) double smem[];
+  // P >= 4 groups: one private box per group (flushes need no barrier; the
+  // boxes are summed in group order at the end of the item).  Fewer groups:
+  // one shared box, groups flush in turn (the extra box costs occupancy).
+  constexpr bool PRIV = P >= 4;
+  constexpr int NB = PRIV ? P : 1;
   double* S = smem;
-  double* stg = smem + box_stride_smem;
+  double* stg = smem + NB * box_stride_smem;
   double* xs = stg + 2 * QS * SR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = warp / B::G, wg = warp % B::G;
@@ -256,7 +261,8 @@ __global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(
 
   for (int vec = 0; vec < a.nvec; ++vec) {
     const double* xv = a.x + vec * a.ldx;
-    for (int v = tid; v < V; v += NT) S[v] = 0.0;
+    for (int g = 0; g < NB; ++g)
+      for (int v = tid; v < V; v += NT) S[g * box_stride_smem + v] = 0.0;
     v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
     cp_async_commit();
     if (tid < QS && p_begin + tid < p_end) xs[tid] = v2_x(a, xv, p_begin + tid);
@@ -268,27 +274,34 @@ __global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(
 #pragma unroll
       for (int ne = 0; ne < NE; ++ne) C[t][ne][0] = C[t][ne][1] = 0.0;
 
-    // flush this group's accumulators of `run` into the box, groups in turn
-    auto flush = [&]() {
+    // flush this group's accumulators of `run`: into its own box (PRIV: the
+    // G warps of a group own disjoint a-rows, lanes disjoint (c, e), so no
+    // barrier), else into the shared box with the groups in turn
+    auto flush_into = [&](double* Sg) {
       const int o0 = run.off & 1023, o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
-      for (int g = 0; g < P; ++g) {
-        if (g == grp) {
 #pragma unroll
-          for (int t = 0; t < TW; ++t) {
-            const int ta = ta0 + t / TC, tc = t % TC;
-            const int aa = 2 * ta + (r8 >> 2), cc = 4 * tc + (r8 & 3);
-            double* row = S + ((o0 + aa) * bx1 + (o1 + cc)) * bx2 + o2;
+      for (int t = 0; t < TW; ++t) {
+        const int ta = ta0 + t / TC, tc = t % TC;
+        const int aa = 2 * ta + (r8 >> 2), cc = 4 * tc + (r8 & 3);
+        double* row = Sg + ((o0 + aa) * bx1 + (o1 + cc)) * bx2 + o2;
 #pragma unroll
-            for (int ne = 0; ne < NE; ++ne)
+        for (int ne = 0; ne < NE; ++ne)
 #pragma unroll
-              for (int i = 0; i < 2; ++i) {
-                const int e = 8 * ne + 2 * q + i;
-                if (e < T) row[e] += C[t][ne][i];
-                C[t][ne][i] = 0.0;
-              }
+          for (int i = 0; i < 2; ++i) {
+            const int e = 8 * ne + 2 * q + i;
+            if (e < T) row[e] += C[t][ne][i];
+            C[t][ne][i] = 0.0;
           }
+      }
+    };
+    auto flush = [&]() {
+      if constexpr (PRIV) {
+        flush_into(S + grp * box_stride_smem);
+      } else {
+        for (int g = 0; g < P; ++g) {
+          if (g == grp) flush_into(S);
+          __syncthreads();
         }
-        __syncthreads();
       }
     };
 
@@ -350,7 +363,12 @@ __global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(
     }
     __syncthreads();
     double* out = a.priv + (static_cast<int64_t>(vec) * gridDim.x + blockIdx.x) * a.box_stride;
-    for (int v = tid; v < V; v += NT) out[v] = S[v];
+    for (int v = tid; v < V; v += NT) {
+      double sum = S[v];
+#pragma unroll
+      for (int g = 1; g < NB; ++g) sum += S[g * box_stride_smem + v];
+      out[v] = sum;
+    }
     __syncthreads();
   }
 }
