@@ -219,7 +219,7 @@ template <int T, bool INTERP>
 size_t v4_stage_doubles(V4Var v) {
   auto one = [](auto tag) -> size_t {
     using B = decltype(tag);
-    return INTERP ? 2 * static_cast<size_t>(B::QS) * B::STRIDE + static_cast<size_t>(B::P) * B::G * 8
+    return INTERP ? 2 * static_cast<size_t>(B::QS) * B::STRIDE + 2 * static_cast<size_t>(B::QS) * (B::G + 3)
                   : 2 * static_cast<size_t>(B::QS) * B::STRIDE + 2 * B::QS;
   };
 #define FGS_V4V(PP, QQ) \

@@ -71,10 +71,12 @@ __device__ __forceinline__ void v4_issue_chunk(double* buf, const double* taps, 
 }
 
 // ---------------------------------------------------------------------------
-// interpolation.  smem: box | stage[2][QS*TAPS] | red[P][G][8]
+// interpolation.  smem: box | stage[2][QS*STRIDE] | red[2][QS][G] | x, s, index [2][QS]
 // ---------------------------------------------------------------------------
 template <int T, int PS, int QSZ>
-__global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT) interp_v4_kernel(PassArgs a, int box_stride_smem) {
+// 2m = 12: keep 4 CTAs (16 warps) per SM resident (<= 128 registers)
+__global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT, (T == 12 && Blk4<T, true, PS, QSZ>::NT == 128) ? 4 : 1)
+    interp_v4_kernel(PassArgs a, int box_stride_smem) {
   pdl_wait();
   using B = Blk4<T, true, PS, QSZ>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, G = B::G, P = B::P, SR = B::STRIDE;
@@ -82,7 +84,12 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT) interp_v4_kernel(P
   extern __shared__ __align__(16) double smem[];
   double* S = smem;
   double* stg = smem + box_stride_smem;
-  double* red = stg + 2 * QS * SR;
+  // per staged chunk (double-buffered): partial sums of the G warps per
+  // point and the epilogue operands, reduced after the next chunk barrier
+  double* red = stg + 2 * QS * SR;        // [2][QS][G]
+  double* ex = red + 2 * QS * G;           // [2][QS] x
+  double* es = ex + 2 * QS;                // [2][QS] s
+  long long* eix = reinterpret_cast<long long*>(es + 2 * QS);  // [2][QS] caller index
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = warp / G, wg = warp % G;
   const int q = lane & 3, r8 = lane >> 2;
@@ -111,12 +118,42 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT) interp_v4_kernel(P
     int loaded = -1;
     double gB[TW][KS];  // B fragments of the run's grid block: g[pair(lane/4)][4 ks + lane%4]
 
+    // y of chunk kk's points: the G partials in warp order, then the epilogue
+    auto finish_chunk = [&](int kk) {
+      const int64_t f0 = p_begin + static_cast<int64_t>(kk) * QS;
+      const int cnt = static_cast<int>(lmin(QS, p_end - f0));
+      const int fb = kk & 1;
+      for (int pt = tid; pt < cnt; pt += NT) {
+        double val = red[(fb * QS + pt) * G];
+#pragma unroll
+        for (int w2 = 1; w2 < G; ++w2) val += red[(fb * QS + pt) * G + w2];
+        const int64_t ipt = f0 + pt;
+        if (a.epilogue == EPI_DEGREE) {
+          const double dg = val - a.k0;  // graphop.cpp:55-56
+          a.degrees[ipt] = dg;
+          a.inv_sqrt[ipt] = 1.0 / sqrt(dg);
+          if (!(dg > 0.0)) atomicMin(a.bad_flag, static_cast<unsigned long long>(a.caller[ipt]));
+        } else {
+          const double xin = ex[fb * QS + pt], sin_ = es[fb * QS + pt];
+          double out;
+          switch (a.epilogue) {
+            case EPI_KERNEL: out = val; break;
+            case EPI_WEIGHT: out = val - a.k0 * xin; break;
+            case EPI_NORMALIZED: out = sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
+            default: out = xin - sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
+          }
+          yv[eix[fb * QS + pt]] = out;
+        }
+      }
+    };
+
     for (int k = 0; k < nch; ++k) {
       const int64_t c0 = p_begin + static_cast<int64_t>(k) * QS;
       const int64_t c1 = lmin(c0 + QS, p_end);
       const int buf = k & 1;
       cp_async_wait_0();
       __syncthreads();
+      if (k > 0) finish_chunk(k - 1);
       if (k + 1 < nch) {
         v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, static_cast<int>(lmin(QS, p_end - c1)), tid, NT);
         cp_async_commit();
@@ -192,39 +229,24 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT) interp_v4_kernel(P
           }
           break;
         }
-        // sum the 4 lanes of each point, then the G warps of the group
+        // sum the 4 lanes of each point; the G warps' partials meet in
+        // shared memory (reduced in finish_chunk after the next barrier)
         yacc += __shfl_xor_sync(0xffffffffu, yacc, 1);
         yacc += __shfl_xor_sync(0xffffffffu, yacc, 2);
-        if (G > 1) {
-          double* rg = red + grp * G * 8;
-          if (wg > 0 && q == 0) rg[wg * 8 + r8] = yacc;
-          asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(32 * G) : "memory");
-          if (wg == 0 && q == 0)
-#pragma unroll
-            for (int w2 = 1; w2 < G; ++w2) yacc += rg[w2 * 8 + r8];
-          asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(32 * G) : "memory");
-        }
-        if (wg == 0 && q == 0 && in_chunk) {
-          const double val = yacc;
-          if (a.epilogue == EPI_DEGREE) {
-            const double dg = val - a.k0;  // graphop.cpp:55-56
-            a.degrees[ipt] = dg;
-            a.inv_sqrt[ipt] = 1.0 / sqrt(dg);
-            if (!(dg > 0.0)) atomicMin(a.bad_flag, static_cast<unsigned long long>(a.caller[ipt]));
-          } else {
-            double out;
-            switch (a.epilogue) {
-              case EPI_KERNEL: out = val; break;
-              case EPI_WEIGHT: out = val - a.k0 * xin; break;
-              case EPI_NORMALIZED: out = sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
-              default: out = xin - sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
-            }
-            yv[ix] = out;
+        if (q == 0 && in_chunk) {
+          const int pt = static_cast<int>(ipt - c0);
+          red[(buf * QS + pt) * G + wg] = yacc;
+          if (wg == 0) {
+            ex[buf * QS + pt] = xin;
+            es[buf * QS + pt] = sin_;
+            eix[buf * QS + pt] = ix;
           }
         }
       }
     }
     cp_async_wait_0();
+    __syncthreads();
+    if (nch > 0) finish_chunk(nch - 1);
     __syncthreads();
   }
 }
