@@ -47,7 +47,7 @@ __device__ unsigned long long g_conv2_trace[16];
   } while (0)
 #endif
 
-constexpr int kClusterCtas = 8;
+constexpr int kClusterCtas = 16;  // non-portable cluster size (B200 allows 16)
 constexpr int kConvThreads = 256;
 
 struct Conv2Args {
@@ -264,21 +264,30 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kConvThre
   CONV2_MARK(8);
 }
 
-// Host dispatch over the supported grid sizes (M = 16 ... 256).
-inline bool conv2_supported(int M) { return M == 16 || M == 32 || M == 64 || M == 128 || M == 256; }
+// Host dispatch over the supported grid sizes (M = 32 ... 256).
+inline bool conv2_supported(int M) { return M == 32 || M == 64 || M == 128 || M == 256; }  // M / 16 rows, paired
 inline const void* conv2_kernel_ptr(int M) {
   switch (M) {
-    case 16: return reinterpret_cast<const void*>(conv2_cluster_kernel<16>);
     case 32: return reinterpret_cast<const void*>(conv2_cluster_kernel<32>);
     case 64: return reinterpret_cast<const void*>(conv2_cluster_kernel<64>);
     case 128: return reinterpret_cast<const void*>(conv2_cluster_kernel<128>);
     default: return reinterpret_cast<const void*>(conv2_cluster_kernel<256>);
   }
 }
+inline void conv2_allow_cluster(const void* k) {
+  FGS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
 inline void conv2_launch(const Conv2Args& a, size_t smem, cudaStream_t stream) {
+  static const bool allowed = [] {
+    conv2_allow_cluster(reinterpret_cast<const void*>(conv2_cluster_kernel<32>));
+    conv2_allow_cluster(reinterpret_cast<const void*>(conv2_cluster_kernel<64>));
+    conv2_allow_cluster(reinterpret_cast<const void*>(conv2_cluster_kernel<128>));
+    conv2_allow_cluster(reinterpret_cast<const void*>(conv2_cluster_kernel<256>));
+    return true;
+  }();
+  (void)allowed;
   const dim3 grid(kClusterCtas * a.nvec), block(kConvThreads);
   switch (a.M) {
-    case 16: launch_ex(conv2_cluster_kernel<16>, grid, block, smem, stream, a); break;
     case 32: launch_ex(conv2_cluster_kernel<32>, grid, block, smem, stream, a); break;
     case 64: launch_ex(conv2_cluster_kernel<64>, grid, block, smem, stream, a); break;
     case 128: launch_ex(conv2_cluster_kernel<128>, grid, block, smem, stream, a); break;

@@ -25,6 +25,7 @@ int main() {
   Conv2Args a{g, g, mult, tw, M, logM, N, 1, M * M};
   const size_t smem = conv2_smem(M, N);
   cudaFuncSetAttribute(conv2_cluster_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(conv2_cluster_kernel<128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
