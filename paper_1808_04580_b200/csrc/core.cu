@@ -1019,8 +1019,14 @@ void Core::apply(int epilogue, const double* x, int64_t ldx, double* y, int64_t 
     const char* e = std::getenv("FGS_GRAPHS");
     return !(e && std::string(e) == "0");
   }();
-  // sharded handles launch directly: NCCL inside stream capture is not exercised on this 1-GPU pool
-  if (!graphs_on || profile_ || stream == nullptr || epilogue == EPI_DEGREE || sharded) {
+  // sharded handles capture their ncclAllReduce into the graph as well (NCCL
+  // supports stream capture; every rank replays the same sequence);
+  // FGS_SHARDED_GRAPHS=0 launches them directly
+  static const bool sharded_graphs = [] {
+    const char* e = std::getenv("FGS_SHARDED_GRAPHS");
+    return !(e && std::string(e) == "0");
+  }();
+  if (!graphs_on || profile_ || stream == nullptr || epilogue == EPI_DEGREE || (sharded && !sharded_graphs)) {
     apply_launches(epilogue, x, ldx, y, ldy, nvec, caller_order, scale_input);
     return;
   }
@@ -1165,7 +1171,14 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
   if (profile_) mark(evs);
   if (use_conv2d()) {
     // d = 2: one cluster launch (row FFTs / kept-column FFT + multiply +
-    // inverse through DSMEM / inverse row FFTs), conv2d.cuh
+    // inverse through DSMEM / inverse row FFTs), conv2d.cuh.  Sharded: the
+    // ranks' partial real grids (M^2 doubles) are summed first, then every
+    // rank convolves the full grid (the exchange of SURVEY 8e on the grid
+    // instead of the spectrum window: one launch instead of four)
+    if (sharded)
+      nccl_check(nccl().all_reduce(w.grid.p, w.grid.p, static_cast<size_t>(grid_elems) * nvec, ncclDouble, ncclSum,
+                                   comm, stream),
+                 "ncclAllReduce of the partial grids");
     int logM = 0;
     while ((1 << logM) < M) ++logM;
     Conv2Args ca{w.grid.p, w.grid.p, mult.p, tw2.p, M, logM, N, nvec, grid_elems};
@@ -1251,7 +1264,7 @@ bool Core::use_conv2d() const {
     const char* e = std::getenv("FGS_CONV2D");
     return !(e && std::string(e) == "0");
   }();
-  return on && d == 2 && !sharded && kind == FASTSUM && conv2_supported(M) &&
+  return on && d == 2 && kind == FASTSUM && conv2_supported(M) &&
          conv2_smem(M, N) <= 200 * 1024 && tw2.p != nullptr;
 }
 
