@@ -137,6 +137,7 @@ struct PassArgs {
   double* inv_sqrt;
   unsigned long long* bad_flag;  // EPI_DEGREE: min caller index with d <= 0
   const int* caller;   // internal -> caller index of this shard's slice (always set)
+  int defer_epilogue;  // v4 interp, one warp per footprint: epilogue per staged chunk (large plans)
 };
 
 }  // namespace fgsb

@@ -265,6 +265,12 @@ void v4_launch(V4Var v, const PassArgs& a, int nitems, size_t smem, int box_stri
     }                                                                                 \
     return;                                                                           \
   }
+  if (INTERP && v.p == 0 && v.qs == 0 && a.defer_epilogue) {  // default interp variant, large plan
+    auto k = interp_v4_kernel<T, 0, 0, true>;
+    set_smem(reinterpret_cast<const void*>(k), smem);
+    launch_ex(k, nitems, Blk4<T, true, 0, 0>::NT, smem, s, a, box_stride);
+    return;
+  }
   FGS_V4L(0, 0) FGS_V4L(0, 32) FGS_V4L(0, 64) FGS_V4L(1, 32) FGS_V4L(1, 64) FGS_V4L(2, 32) FGS_V4L(2, 64) FGS_V4L(4, 32)
   FGS_V4L(4, 64)
 #undef FGS_V4L
@@ -829,6 +835,43 @@ void Core::build_plan(const double* nodes_colmajor) {
     }
     asm_ptr.upload(cnt.data(), cnt.size(), stream);
     asm_idx.upload(idx.data(), idx.size(), stream);
+    // lanes per cell by list length: clustered data concentrates most entries
+    // in a few long lists (C3-C5: ~85 % of the entries sit in lists > 64),
+    // which one lane per cell walks serially.  Split only when the mean list
+    // is short (one lane per cell would be chosen) and the plan is large
+    // enough to amortise two more launches; otherwise one launch with lanes
+    // by the mean.  FGS_ASM_STATS=1 prints the distribution.
+    asm_split = false;
+    asm_class_n[0] = asm_class_n[1] = asm_class_n[2] = 0;
+    {
+      const double mean_list = static_cast<double>(cnt.back()) / static_cast<double>(std::max<int64_t>(grid_elems, 1));
+      static const bool split_on = [] {
+        const char* e = std::getenv("FGS_ASM_CLASSES");
+        return !(e && std::string(e) == "0");
+      }();
+      std::vector<int> cls[3];
+      int64_t entries[3] = {0, 0, 0};
+      int maxlen = 0;
+      for (int64_t g = 0; g < grid_elems; ++g) {
+        const int len = cnt[static_cast<size_t>(g) + 1] - cnt[static_cast<size_t>(g)];
+        const int c = len <= 8 ? 0 : (len <= 64 ? 1 : 2);
+        cls[c].push_back(static_cast<int>(g));
+        entries[c] += len;
+        maxlen = std::max(maxlen, len);
+      }
+      if (std::getenv("FGS_ASM_STATS"))
+        std::fprintf(stderr, "[asm] cells %lld entries %lld mean %.2f max %d | entries in lists <=8 %lld, 9..64 %lld, >64 %lld\n",
+                     static_cast<long long>(grid_elems), static_cast<long long>(cnt.back()), mean_list, maxlen,
+                     static_cast<long long>(entries[0]), static_cast<long long>(entries[1]),
+                     static_cast<long long>(entries[2]));
+      if (split_on && mean_list < 4.0 && n_local >= 100000) {
+        asm_split = true;
+        for (int c = 0; c < 3; ++c) {
+          asm_class_n[c] = static_cast<int64_t>(cls[c].size());
+          if (!cls[c].empty()) asm_cells[c].upload(cls[c].data(), cls[c].size(), stream);
+        }
+      }
+    }
   }
   if (ditems.empty()) {
     ditems.push_back(DItem{0, 0, 0, 0, 0, 1, 1, 1});
@@ -996,17 +1039,32 @@ void Core::launch_interp(const PassArgs& a) {
 }
 
 void Core::launch_assemble(Workspace& w, int nvec) {
-  AssembleArgs aa{asm_ptr.p, asm_idx.p, w.priv.p, static_cast<int64_t>(std::max(nitems, 1)) * box_stride, w.grid.p,
-                  grid_elems, grid_elems, nvec};
-  // lanes per grid cell from the mean CSR list length
-  const double mean_list = static_cast<double>(asm_idx.n) / static_cast<double>(std::max<int64_t>(grid_elems, 1));
-  if (mean_list >= 16.0)
-    launch_ex(assemble_kernel<8>, ceil_div(grid_elems * 8, 256), 256, 0, stream, aa);
-  else if (mean_list >= 4.0)
-    launch_ex(assemble_kernel<4>, ceil_div(grid_elems * 4, 256), 256, 0, stream, aa);
-  else
-    launch_ex(assemble_kernel<1>, ceil_div(grid_elems, 256), 256, 0, stream, aa);
-  ++launches;
+  const int64_t pstride = static_cast<int64_t>(std::max(nitems, 1)) * box_stride;
+  if (!asm_split) {  // lanes per cell from the mean list length, one launch
+    AssembleArgs aa{asm_ptr.p, asm_idx.p, w.priv.p, pstride, w.grid.p, grid_elems, grid_elems, nvec, nullptr};
+    const double mean_list = static_cast<double>(asm_idx.n) / static_cast<double>(std::max<int64_t>(grid_elems, 1));
+    if (mean_list >= 16.0)
+      launch_ex(assemble_kernel<8>, dim3(ceil_div(grid_elems * 8, 256)), 256, 0, stream, aa);
+    else if (mean_list >= 4.0)
+      launch_ex(assemble_kernel<4>, dim3(ceil_div(grid_elems * 4, 256)), 256, 0, stream, aa);
+    else
+      launch_ex(assemble_kernel<1>, dim3(ceil_div(grid_elems, 256)), 256, 0, stream, aa);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+    return;
+  }
+  // one launch per nonempty list-length class: 1, 8 or 32 lanes per cell
+  for (int c = 0; c < 3; ++c) {
+    if (asm_class_n[c] == 0) continue;
+    AssembleArgs aa{asm_ptr.p, asm_idx.p, w.priv.p, pstride, w.grid.p, grid_elems, asm_class_n[c], nvec,
+                    asm_cells[c].p};
+    const int lanes = c == 0 ? 1 : (c == 1 ? 8 : 32);
+    const dim3 blocks(static_cast<unsigned>(ceil_div(asm_class_n[c] * lanes, 256)));
+    if (c == 0) launch_ex(assemble_kernel<1>, blocks, 256, 0, stream, aa);
+    if (c == 1) launch_ex(assemble_kernel<8>, blocks, 256, 0, stream, aa);
+    if (c == 2) launch_ex(assemble_kernel<32>, blocks, 256, 0, stream, aa);
+    ++launches;
+  }
   FGS_CUDA(cudaGetLastError());
 }
 
@@ -1162,6 +1220,7 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
   a.inv_sqrt = inv_sqrt.p;
   a.bad_flag = flag.p;
   a.caller = perm.p + offset;
+  a.defer_epilogue = n_local >= 100000 ? 1 : 0;
 
   std::vector<cudaEvent_t> evs;
   if (profile_) mark(evs);

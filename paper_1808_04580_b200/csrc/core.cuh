@@ -119,6 +119,9 @@ class Core {
   DBuf<DItem> items;
   DBuf<DRun> runs;
   DBuf<int> asm_ptr, asm_idx;  // grid cell -> private-box entries (CSR, item order)
+  DBuf<int> asm_cells[3];      // cells by list-length class (<= 8, 9..64, > 64 entries)
+  int64_t asm_class_n[3] = {0, 0, 0};
+  bool asm_split = false;
   DBuf<cufftDoubleComplex> mult;  // compact Hermitian multiplier (FASTSUM)
   DBuf<double> deconv_d;
   DBuf<double2> tw2;  // d = 2 pruned-convolution twiddles

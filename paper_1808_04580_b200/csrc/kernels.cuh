@@ -240,20 +240,22 @@ struct AssembleArgs {
   int64_t priv_stride;  // per vector
   double* grid;
   int64_t grid_stride;
-  int64_t cells;
+  int64_t cells;       // cells handled by this launch
   int nvec;
+  const int* cell_ids; // this launch's cells (nullable: cells 0 .. cells-1)
 };
 
-// L lanes per grid cell (1, 4 or 8 by the mean list length): each sums a
-// contiguous slice of the cell's entry list in order, then the slices are
-// combined by a fixed shuffle tree, so the result is bitwise reproducible.
+// L lanes per grid cell (1, 8 or 32 by the cell's list-length class, plan
+// time): each sums a contiguous slice of the cell's entry list in order, then
+// the slices are combined by a fixed shuffle tree -> bitwise reproducible.
 template <int kAsmLanes>
 __global__ void assemble_kernel(AssembleArgs a) {
   pdl_wait();
   const int64_t gt = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t g = gt / kAsmLanes;
+  const int64_t gi = gt / kAsmLanes;
   const int sub = static_cast<int>(gt % kAsmLanes);
-  const bool valid = g < a.cells;
+  const bool valid = gi < a.cells;
+  const int64_t g = (valid && a.cell_ids) ? static_cast<int64_t>(a.cell_ids[gi]) : gi;
   int b = 0, e = 0;
   if (valid) {
     const int b0 = a.ptr[g], e0 = a.ptr[g + 1];
