@@ -93,6 +93,7 @@ struct DItem {
   int run_begin, run_end;
   int a0, a1, a2;
   int e0, e1, e2;
+  int p_begin, p_end;  // the item's points [p_begin, p_end) (first tap prefetch needs no run load)
 };
 
 // A run = consecutive points (in the internal order) that share the same

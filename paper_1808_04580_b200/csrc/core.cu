@@ -791,6 +791,8 @@ void Core::build_plan(const double* nodes_colmajor) {
       druns.push_back(dr);
     }
     it.run_end = static_cast<int>(druns.size());
+    it.p_begin = h.runs.front().pstart;
+    it.p_end = h.runs.back().pstart + h.runs.back().pcount;
     int ext[3], org[3];
     for (int t = 0; t < 3; ++t) {
       const bool used = t >= 3 - d;
@@ -874,7 +876,7 @@ void Core::build_plan(const double* nodes_colmajor) {
     }
   }
   if (ditems.empty()) {
-    ditems.push_back(DItem{0, 0, 0, 0, 0, 1, 1, 1});
+    ditems.push_back(DItem{0, 0, 0, 0, 0, 1, 1, 1, 0, 0});
     nitems = 0;
   }
   items.upload(ditems.data(), ditems.size(), stream);

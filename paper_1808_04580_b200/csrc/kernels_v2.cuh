@@ -104,9 +104,7 @@ __global__ void __launch_bounds__(Blk<D, T>::NT) spread_v2_kernel(PassArgs a, in
   const int bx1 = it.e1, bx2 = it.e2;
   const int V = it.e0 * it.e1 * it.e2;
   const V2Geom ug = v2_unit<D, T>(tid);
-  const int64_t p_begin = a.runs[it.run_begin].pstart;
-  const DRun last = a.runs[it.run_end - 1];
-  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int64_t p_begin = it.p_begin, p_end = it.p_end;
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
 
   for (int vec = 0; vec < a.nvec; ++vec) {
@@ -226,9 +224,7 @@ __global__ void __launch_bounds__(Blk<D, T>::NT) interp_v2_kernel(PassArgs a, in
   const int V = it.e0 * it.e1 * it.e2;
   const int Md0 = D == 3 ? a.M : 1, Md1 = D >= 2 ? a.M : 1, Md2 = a.M;
   const V2Geom ug = v2_unit<D, T>(tid);
-  const int64_t p_begin = a.runs[it.run_begin].pstart;
-  const DRun last = a.runs[it.run_end - 1];
-  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int64_t p_begin = it.p_begin, p_end = it.p_end;
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
   int rb = 0;  // red double buffer
 

@@ -55,9 +55,7 @@ __global__ void __launch_bounds__(Blk3<T>::NT) interp_v3_kernel(PassArgs a, int 
   const int bx1 = it.e1, bx2 = it.e2;
   const int V = it.e0 * it.e1 * it.e2;
   const int M = a.M;
-  const int64_t p_begin = a.runs[it.run_begin].pstart;
-  const DRun last = a.runs[it.run_end - 1];
-  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int64_t p_begin = it.p_begin, p_end = it.p_end;
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
 
   for (int vec = 0; vec < a.nvec; ++vec) {

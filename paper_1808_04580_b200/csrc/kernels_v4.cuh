@@ -103,9 +103,7 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT, (T == 12 && Blk4<T
   const int bx1 = it.e1, bx2 = it.e2;
   const int V = it.e0 * it.e1 * it.e2;
   const int M = a.M;
-  const int64_t p_begin = a.runs[it.run_begin].pstart;
-  const DRun last = a.runs[it.run_end - 1];
-  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int64_t p_begin = it.p_begin, p_end = it.p_end;
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
 
   for (int vec = 0; vec < a.nvec; ++vec) {
@@ -302,9 +300,7 @@ __global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(
   const DItem it = a.items[blockIdx.x];
   const int bx1 = it.e1, bx2 = it.e2;
   const int V = it.e0 * it.e1 * it.e2;
-  const int64_t p_begin = a.runs[it.run_begin].pstart;
-  const DRun last = a.runs[it.run_end - 1];
-  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int64_t p_begin = it.p_begin, p_end = it.p_end;
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
 
   for (int vec = 0; vec < a.nvec; ++vec) {
@@ -458,9 +454,7 @@ __global__ void __launch_bounds__(Blk4d2<T>::NT) interp_v4_2d_kernel(PassArgs a,
   const int bx2 = it.e2;
   const int V = it.e1 * it.e2;
   const int M = a.M;
-  const int64_t p_begin = a.runs[it.run_begin].pstart;
-  const DRun last = a.runs[it.run_end - 1];
-  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int64_t p_begin = it.p_begin, p_end = it.p_end;
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
 
   for (int vec = 0; vec < a.nvec; ++vec) {
@@ -581,9 +575,7 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) spread_v4_2d_kernel(PassArg
   const DItem it = a.items[blockIdx.x];
   const int bx2 = it.e2;
   const int V = it.e1 * it.e2;
-  const int64_t p_begin = a.runs[it.run_begin].pstart;
-  const DRun last = a.runs[it.run_end - 1];
-  const int64_t p_end = static_cast<int64_t>(last.pstart) + last.pcount;
+  const int64_t p_begin = it.p_begin, p_end = it.p_end;
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
 
   for (int vec = 0; vec < a.nvec; ++vec) {
