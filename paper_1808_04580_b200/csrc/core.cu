@@ -363,9 +363,29 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
   if constexpr (has_v4_2d<D, T>()) {
     if (use_v4() && (interp || dense)) {
       if (interp) {
-        auto k = interp_v4_2d_kernel<T>;
-        set_smem(reinterpret_cast<const void*>(k), smem);
-        launch_ex(k, nitems, Blk4d2<T>::NT, smem, s, a, box_stride);
+        // point-stream warps per CTA (FGS_INTERP2D_P; 2 measured best on C2:
+        // 22.8 k vs 22.2 k with 4, 21.7 k with 1)
+        static const int pi = [] {
+          const char* e = std::getenv("FGS_INTERP2D_P");
+          return e ? std::atoi(e) : 2;
+        }();
+        if (pi == 1) {
+          auto k = interp_v4_2d_kernel<T, 1>;
+          set_smem(reinterpret_cast<const void*>(k), smem);
+          launch_ex(k, nitems, Blk4d2<T, 1>::NT, smem, s, a, box_stride);
+        } else if (pi == 2) {
+          auto k = interp_v4_2d_kernel<T, 2>;
+          set_smem(reinterpret_cast<const void*>(k), smem);
+          launch_ex(k, nitems, Blk4d2<T, 2>::NT, smem, s, a, box_stride);
+        } else if (pi == 8) {
+          auto k = interp_v4_2d_kernel<T, 8>;
+          set_smem(reinterpret_cast<const void*>(k), smem);
+          launch_ex(k, nitems, Blk4d2<T, 8>::NT, smem, s, a, box_stride);
+        } else {
+          auto k = interp_v4_2d_kernel<T, 4>;
+          set_smem(reinterpret_cast<const void*>(k), smem);
+          launch_ex(k, nitems, Blk4d2<T, 4>::NT, smem, s, a, box_stride);
+        }
       } else {
         static const int ps = [] {
           const char* e = std::getenv("FGS_SPREAD2D_P");

@@ -440,10 +440,10 @@ struct Blk4d2 {
                               : (TAPS % 16 == 0 ? TAPS + 4 : TAPS + ((12 - TAPS % 16 + 16) % 16));
 };
 
-template <int T>
-__global__ void __launch_bounds__(Blk4d2<T>::NT) interp_v4_2d_kernel(PassArgs a, int box_stride_smem) {
+template <int T, int PS = 4>
+__global__ void __launch_bounds__(Blk4d2<T, PS>::NT) interp_v4_2d_kernel(PassArgs a, int box_stride_smem) {
   pdl_wait();
-  using B = Blk4d2<T>;
+  using B = Blk4d2<T, PS>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE, NC = B::NC, KS = B::KS;
   extern __shared__ __align__(16) double smem[];
   double* S = smem;
