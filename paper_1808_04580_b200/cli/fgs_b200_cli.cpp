@@ -1,5 +1,5 @@
 // fgs_b200_cli.cpp -- the reference's command-line drivers for the hot path
-// (tools/commands.cpp: gen, eigs, cluster, bench) on the B200 library, with
+// (tools/commands.cpp: gen, eigs, cluster, bench, ssl-kernel, krr) on the B200 library, with
 // the same flags, defaults, exit codes and `fgs-report-v1` JSON report
 // (report.cpp:97-112, schema/report.schema.json).
 //
@@ -11,8 +11,10 @@
 // Methods: nfft-lanczos (Fastsum backend), direct (Direct backend) and
 // nystrom-gauss-nfft (Gaussian sketch over the fast operator).  The sampled
 // "nystrom" method (dense kernel blocks, spectral.cpp:277-382) is not part of
-// this build and is rejected as a usage error.  Commands segment / ssl-pf / ssl-kernel / krr
-// are likewise out of scope.
+// this build and is rejected as a usage error, as are the commands segment
+// (image I/O) and ssl-pf (Allen-Cahn phase field).
+// ssl-kernel and krr (commands.cpp:531-713) run the device CG.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -882,9 +884,211 @@ int run_bench(Args& a) {
   });
 }
 
+// ---- learn.cpp:169-216 training selection / fidelity -----------------------
+std::vector<int> require_labels(const PointCloud& c) {
+  if (!c.has_labels()) throw fgs::ParameterError("this command needs a labeled input CSV (final `label` column)");
+  return c.labels;
+}
+
+int count_classes(const std::vector<int>& labels) {
+  int k = 0;
+  for (int l : labels) {
+    if (l < 0) throw fgs::RangeError("labels must be nonnegative");
+    k = std::max(k, l + 1);
+  }
+  return k;
+}
+
+// per_class_count indices per class, uniformly without replacement: each
+// class's member list shuffled by one std::mt19937_64(seed) in class order
+std::vector<std::vector<Index>> select_training(const std::vector<int>& labels, int n_classes, int per_class_count,
+                                                std::uint64_t seed) {
+  if (n_classes < 1) throw fgs::ParameterError("need at least one class");
+  if (per_class_count < 1) throw fgs::ParameterError("need at least one sample per class");
+  std::vector<std::vector<Index>> members(static_cast<size_t>(n_classes));
+  for (size_t i = 0; i < labels.size(); ++i) {
+    const int l = labels[i];
+    if (l < 0 || l >= n_classes)
+      throw fgs::RangeError("label " + std::to_string(l) + " at position " + std::to_string(i) +
+                            " is outside [0, n_classes)");
+    members[static_cast<size_t>(l)].push_back(static_cast<Index>(i));
+  }
+  std::mt19937_64 rng(seed);
+  std::vector<std::vector<Index>> out(static_cast<size_t>(n_classes));
+  for (int c = 0; c < n_classes; ++c) {
+    auto& pool = members[static_cast<size_t>(c)];
+    if (static_cast<int>(pool.size()) < per_class_count)
+      throw fgs::ParameterError("class " + std::to_string(c) + " has only " + std::to_string(pool.size()) +
+                                " members; cannot draw " + std::to_string(per_class_count));
+    std::shuffle(pool.begin(), pool.end(), rng);
+    out[static_cast<size_t>(c)].assign(pool.begin(), pool.begin() + per_class_count);
+  }
+  return out;
+}
+
+VectorXd fidelity_vector(const std::vector<std::vector<Index>>& sel, Index n, int positive) {
+  VectorXd f(n);
+  for (size_t c = 0; c < sel.size(); ++c)
+    for (Index i : sel[c]) f(i) = static_cast<int>(c) == positive ? 1.0 : -1.0;
+  return f;
+}
+
+std::vector<int> argmax_labels(const std::vector<VectorXd>& fields, Index n) {
+  std::vector<int> out(static_cast<size_t>(n));
+  for (Index i = 0; i < n; ++i) {
+    if (fields.size() == 1) {
+      out[static_cast<size_t>(i)] = fields[0](i) >= 0.0 ? 0 : 1;
+    } else {
+      int best = 0;
+      for (size_t c = 1; c < fields.size(); ++c)
+        if (fields[c](i) > fields[static_cast<size_t>(best)](i)) best = static_cast<int>(c);
+      out[static_cast<size_t>(i)] = best;
+    }
+  }
+  return out;
+}
+
+// ---- ssl-kernel (commands.cpp:531-652) -------------------------------------
+int run_ssl_kernel(Args& a) {
+  CommonOpts o;
+  int per_class = 25, truncate_k = 0, max_iter = 1000;
+  double beta = 1e4;
+  io_flags(a, &o, true);
+  kernel_flags(a, &o);
+  fastsum_flags(a, &o);
+  a.get("method", &o.method);
+  if (o.method != "nfft-lanczos" && o.method != "direct")
+    throw UsageError("--method: " + o.method + " not in {nfft-lanczos, direct}");
+  a.get("samples-per-class", &per_class);
+  a.get("beta", &beta);
+  a.get("k", &truncate_k);
+  a.get("tol", &o.tol);
+  a.get("max-iter", &max_iter);
+  a.finish();
+  Report rep;
+  rep.command = "ssl-kernel";
+  rep.method = truncate_k > 0 ? "truncated-eig" : "cg";
+  rep.seed = o.seed;
+  rep.parameters = echo_common(o);
+  rep.parameters["samples_per_class"] = per_class;
+  rep.parameters["beta"] = beta;
+  rep.parameters["truncate_k"] = truncate_k;
+  rep.parameters["max_iter"] = max_iter;
+  return guarded(rep, o.out, [&] {
+    const PointCloud cloud = load_points_csv(o.in);
+    const std::vector<int> truth = require_labels(cloud);
+    const int n_classes = count_classes(truth);
+    if (n_classes < 2) throw fgs::ParameterError("kernel SSL needs at least two classes");
+    const double tol = o.tol > 0.0 ? o.tol : 1e-4;
+    const auto sel = select_training(truth, n_classes, per_class, o.seed);
+    Timer setup;
+    AdjacencyOperator op(cloud.coordinates, make_kernel(o), make_params(o),
+                         o.method == "direct" ? AdjacencyBackend::Direct : AdjacencyBackend::Fastsum, o.device);
+    rep.add_timing("setup", setup.seconds());
+    std::optional<EigenPairs> basis;
+    fgs::LanczosInfo binfo;
+    if (truncate_k > 0) {  // commands.cpp:573-587
+      fgs::LanczosOptions lo;
+      lo.seed = o.seed;
+      lo.tol = 1e-8;
+      lo.max_iter = 6000;
+      Timer eig;
+      basis = fgs::lanczos_largest(op, truncate_k, lo, &binfo);
+      rep.add_timing("eig", eig.seconds());
+    }
+    const int channels = n_classes == 2 ? 1 : n_classes;
+    std::vector<VectorXd> fields;
+    int max_its = 0;
+    bool all_conv = true;
+    Timer solve;
+    for (int ch = 0; ch < channels; ++ch) {
+      const VectorXd f = fidelity_vector(sel, cloud.size(), ch);
+      if (basis) {
+        fields.push_back(fgs::kernel_ssl_truncated(*basis, f, beta));
+      } else {
+        fgs::CgResult r = fgs::kernel_ssl_solve(op, f, beta, tol, max_iter);
+        max_its = std::max(max_its, r.iterations);
+        all_conv = all_conv && r.converged();
+        fields.push_back(r.x);
+      }
+    }
+    rep.add_timing("solve", solve.seconds());
+    const std::vector<int> pred = argmax_labels(fields, cloud.size());
+    save_labels_csv(pred, o.out + ".labels.csv");
+    const double rate = fgs::misclassification_rate(pred, truth);
+    rep.add_metric("misclassification_rate", rate,
+                   "fraction of points labeled differently from the ground-truth labels of the input");
+    if (!basis) {
+      rep.add_metric("cg_iterations", max_its, "largest conjugate-gradient iteration count over channels");
+      rep.add_metric("cg_converged", all_conv ? 1.0 : 0.0, "1 if every channel met the CG tolerance");
+      if (!all_conv) {
+        rep.status = "numerical-failure";
+        rep.diagnostic = "conjugate gradients hit the iteration cap before meeting the tolerance";
+      }
+    } else {
+      rep.add_metric("basis_iterations", binfo.iterations, "Krylov steps spent computing the truncated eigenbasis");
+      rep.add_metric("basis_converged", binfo.converged ? 1.0 : 0.0,
+                     "1 if every basis pair met the residual tolerance");
+      if (!binfo.converged) {
+        rep.status = "numerical-failure";
+        rep.diagnostic = "the truncated eigenbasis hit the iteration cap before meeting the residual tolerance";
+      }
+    }
+    return finish(rep, o.out, "ssl-kernel: misclassification " + std::to_string(rate) + '\n');
+  });
+}
+
+// ---- krr (commands.cpp:654-713) --------------------------------------------
+int run_krr(Args& a) {
+  CommonOpts o;
+  double beta = 1e-3;
+  int max_iter = 1000;
+  io_flags(a, &o, true);
+  kernel_flags(a, &o);
+  fastsum_flags(a, &o);
+  a.get("beta", &beta);
+  a.get("tol", &o.tol);
+  a.get("max-iter", &max_iter);
+  a.finish();
+  Report rep;
+  rep.command = "krr";
+  rep.method = "krr";
+  rep.seed = o.seed;
+  rep.parameters = echo_common(o);
+  rep.parameters["beta"] = beta;
+  rep.parameters["max_iter"] = max_iter;
+  return guarded(rep, o.out, [&] {
+    const PointCloud cloud = load_points_csv(o.in);
+    const std::vector<int> truth = require_labels(cloud);
+    const int n_classes = count_classes(truth);
+    if (n_classes < 2) throw fgs::ParameterError("classification needs at least two classes");
+    const double tol = o.tol > 0.0 ? o.tol : 1e-6;
+    const int channels = n_classes == 2 ? 1 : n_classes;
+    std::vector<VectorXd> scores;
+    int max_its = 0;
+    Timer fit;
+    for (int ch = 0; ch < channels; ++ch) {
+      VectorXd t(cloud.size());
+      const int positive = channels == 1 ? 0 : ch;
+      for (Index i = 0; i < cloud.size(); ++i) t(i) = truth[static_cast<size_t>(i)] == positive ? 1.0 : -1.0;
+      const fgs::RidgeModel model =
+          fgs::krr_fit(cloud.coordinates, make_kernel(o), beta, t, make_params(o), tol, max_iter, o.device);
+      max_its = std::max(max_its, model.cg_iterations);
+      scores.push_back(fgs::krr_predict(model, cloud.coordinates, o.device));
+    }
+    rep.add_timing("fit_and_predict", fit.seconds());
+    const std::vector<int> pred = argmax_labels(scores, cloud.size());
+    save_labels_csv(pred, o.out + ".labels.csv");
+    const double acc = 1.0 - fgs::misclassification_rate(pred, truth);
+    rep.add_metric("train_accuracy", acc, "fraction of training points whose predicted class matches the label");
+    rep.add_metric("cg_iterations", max_its, "largest conjugate-gradient iteration count over channels");
+    return finish(rep, o.out, "krr: train accuracy " + std::to_string(acc) + '\n');
+  });
+}
+
 const char* kUsage =
     "fgs-b200: matrix-free spectral toolkit for fully connected kernel graphs (B200 build)\n"
-    "usage: fgs-b200 <gen|eigs|cluster|bench> [--options]\n";
+    "usage: fgs-b200 <gen|eigs|cluster|bench|ssl-kernel|krr> [--options]\n";
 
 int run(int argc, char** argv) {
   if (argc < 2) {
@@ -902,7 +1106,9 @@ int run(int argc, char** argv) {
     if (cmd == "eigs") return run_eigs(a);
     if (cmd == "cluster") return run_cluster(a);
     if (cmd == "bench") return run_bench(a);
-    if (cmd == "segment" || cmd == "ssl-pf" || cmd == "ssl-kernel" || cmd == "krr")
+    if (cmd == "ssl-kernel") return run_ssl_kernel(a);
+    if (cmd == "krr") return run_krr(a);
+    if (cmd == "segment" || cmd == "ssl-pf")
       throw UsageError("command '" + cmd + "' is not part of the B200 build");
     throw UsageError("unknown command '" + cmd + "'");
   } catch (const UsageError& e) {  // CLI11::ParseError -> 2

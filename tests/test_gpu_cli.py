@@ -90,3 +90,45 @@ def test_numerical_failure_writes_report(tmp_path):
     assert r.returncode == 1
     rep = json.loads(rep_path.read_text())
     assert rep["status"] == "numerical-failure" and "node 0" in rep["diagnostic"]
+
+
+def test_ssl_kernel_cg_and_truncated(tmp_path):
+    # commands.cpp:531-652: CG on (I + beta L_s) per one-vs-rest channel, or
+    # the truncated-eigenbasis closed form
+    pts = tmp_path / "cm.csv"
+    assert run(EXE, "gen", "--crescent-fullmoon", "--n", 2000, "--out", pts, "--seed", 3).returncode == 0
+    rates = {}
+    for extra, method in (((), "cg"), (("--k", 16), "truncated-eig")):
+        rep_path = tmp_path / f"ssl_{method}.json"
+        r = run(EXE, "ssl-kernel", "--in", pts, "--out", rep_path, "--sigma", 2.0, "--beta", 10,
+                "--samples-per-class", 10, "--tol", 1e-8, *extra)
+        assert r.returncode == 0, r.stderr
+        rep = json.loads(rep_path.read_text())
+        check_report(rep)
+        assert rep["method"] == method and rep["status"] == "ok"
+        rates[method] = rep["metrics"]["misclassification_rate"]["value"]
+        labels = np.loadtxt(str(rep_path) + ".labels.csv", skiprows=1, dtype=int)
+        assert labels.shape == (2000,) and set(labels.tolist()) <= {0, 1}
+    assert rates["cg"] <= 0.05
+    cg = json.loads((tmp_path / "ssl_cg.json").read_text())
+    assert cg["metrics"]["cg_converged"]["value"] == 1.0
+    # too narrow a kernel for setup 2: the reference's nonpositive-degree
+    # failure, reported with status numerical-failure and exit 1
+    r = run(EXE, "ssl-kernel", "--in", pts, "--out", tmp_path / "bad.json", "--sigma", 0.5, "--beta", 10)
+    assert r.returncode == 1
+    assert json.loads((tmp_path / "bad.json").read_text())["status"] == "numerical-failure"
+
+
+def test_krr_command(tmp_path):
+    pts = tmp_path / "cm.csv"
+    assert run(EXE, "gen", "--crescent-fullmoon", "--n", 800, "--out", pts, "--seed", 3).returncode == 0
+    rep_path = tmp_path / "krr.json"
+    r = run(EXE, "krr", "--in", pts, "--out", rep_path, "--sigma", 1.0, "--beta", 1e-2, "--setup", 3)
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(rep_path.read_text())
+    check_report(rep)
+    assert rep["metrics"]["train_accuracy"]["value"] >= 0.95
+    # unlabeled input is a usage error (commands.cpp:279-285)
+    bare = tmp_path / "bare.csv"
+    bare.write_text("x0,x1\n0.1,0.2\n0.3,0.1\n0.5,0.5\n")
+    assert run(EXE, "krr", "--in", bare, "--out", tmp_path / "x.json").returncode == 2
