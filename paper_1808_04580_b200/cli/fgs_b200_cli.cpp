@@ -11,10 +11,13 @@
 // Methods: nfft-lanczos (Fastsum backend), direct (Direct backend) and
 // nystrom-gauss-nfft (Gaussian sketch over the fast operator).  The sampled
 // "nystrom" method (dense kernel blocks, spectral.cpp:277-382) is not part of
-// this build and is rejected as a usage error, as are the commands segment
-// (image I/O) and ssl-pf (Allen-Cahn phase field).
+// this build and is rejected as a usage error, as is the command ssl-pf
+// (Allen-Cahn phase field).  segment reads and writes
+// binary PPM (PNG needs libpng, absent here).
 // ssl-kernel and krr (commands.cpp:531-713) run the device CG.
 #include <algorithm>
+#include <cctype>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -948,6 +951,191 @@ std::vector<int> argmax_labels(const std::vector<VectorXd>& fields, Index n) {
   return out;
 }
 
+// ---- images (dataset.cpp:84-130, 340-460): binary PPM; PNG needs libpng ----
+struct ImageBuffer {
+  int width = 0, height = 0;
+  std::vector<unsigned char> rgb;
+};
+
+std::string ppm_token(std::istream& in) {
+  std::string tok;
+  int c = in.get();
+  while (c != EOF) {
+    if (c == '#') {
+      while (c != EOF && c != '\n') c = in.get();
+    } else if (std::isspace(c)) {
+      c = in.get();
+    } else {
+      break;
+    }
+  }
+  while (c != EOF && !std::isspace(c)) {
+    tok.push_back(static_cast<char>(c));
+    c = in.get();
+  }
+  return tok;
+}
+
+ImageBuffer load_image(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw ParseError(path + ": cannot open");
+  unsigned char magic[8] = {};
+  in.read(reinterpret_cast<char*>(magic), 8);
+  static const unsigned char png_sig[8] = {0x89, 'P', 'N', 'G', '\r', '\n', 0x1a, '\n'};
+  if (std::equal(magic, magic + 8, png_sig))
+    throw FormatError(path + ": PNG input needs libpng, which is not part of this build (use binary PPM)");
+  if (!(magic[0] == 'P' && magic[1] == '6'))
+    throw FormatError(path + ": unsupported image format (expected PNG or binary PPM)");
+  in.clear();
+  in.seekg(0);
+  ppm_token(in);
+  ImageBuffer img;
+  try {
+    img.width = std::stoi(ppm_token(in));
+    img.height = std::stoi(ppm_token(in));
+    if (std::stoi(ppm_token(in)) != 255) throw FormatError(path + ": only 8-bit images are supported");
+  } catch (const std::logic_error&) {
+    throw ParseError(path + ": malformed header");
+  }
+  if (img.width <= 0 || img.height <= 0) throw ParseError(path + ": malformed header");
+  const size_t bytes = 3u * static_cast<size_t>(img.width) * static_cast<size_t>(img.height);
+  img.rgb.resize(bytes);
+  in.read(reinterpret_cast<char*>(img.rgb.data()), static_cast<std::streamsize>(bytes));
+  if (static_cast<size_t>(in.gcount()) != bytes) throw ParseError(path + ": truncated pixel data");
+  return img;
+}
+
+bool ends_with(const std::string& s, const std::string& suf) {
+  return s.size() >= suf.size() && s.compare(s.size() - suf.size(), suf.size(), suf) == 0;
+}
+
+void save_image(const ImageBuffer& img, const std::string& path) {
+  if (ends_with(path, ".png")) throw FormatError(path + ": PNG output needs libpng, which is not part of this build");
+  if (!ends_with(path, ".ppm")) throw FormatError(path + ": unsupported image extension (expected .png or .ppm)");
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw ParseError(path + ": cannot open for writing");
+  out << "P6\n" << img.width << ' ' << img.height << "\n255\n";
+  out.write(reinterpret_cast<const char*>(img.rgb.data()), static_cast<std::streamsize>(img.rgb.size()));
+  if (!out) throw ParseError(path + ": write failed");
+}
+
+// pixels as RGB feature points, raster order (dataset.cpp:368-382)
+PointCloud image_to_nodes(const std::string& path, int* w, int* h) {
+  const ImageBuffer img = load_image(path);
+  *w = img.width;
+  *h = img.height;
+  const Index n = static_cast<Index>(img.width) * img.height;
+  PointCloud c;
+  c.coordinates = MatrixXd(n, 3);
+  for (Index p = 0; p < n; ++p)
+    for (int t = 0; t < 3; ++t) c.coordinates(p, t) = static_cast<double>(img.rgb[static_cast<size_t>(3 * p + t)]);
+  return c;
+}
+
+// dataset.cpp:384-410
+std::vector<std::array<double, 3>> default_palette(int k) {
+  if (k < 1) throw fgs::ParameterError("palette needs at least one color");
+  static const int base[10][3] = {{31, 119, 180}, {255, 127, 14}, {44, 160, 44},   {214, 39, 40}, {148, 103, 189},
+                                  {140, 86, 75},  {227, 119, 194}, {127, 127, 127}, {188, 189, 34}, {23, 190, 207}};
+  std::vector<std::array<double, 3>> pal(static_cast<size_t>(k));
+  for (int i = 0; i < k; ++i) {
+    if (i < 10) {
+      for (int c = 0; c < 3; ++c) pal[static_cast<size_t>(i)][static_cast<size_t>(c)] = base[i][c];
+    } else {
+      const double hue = 6.0 * (i - 10) / std::max(1, k - 10);
+      const int sector = static_cast<int>(hue) % 6;
+      const double frac = hue - std::floor(hue);
+      const double table[6][3] = {{1, frac, 0}, {1 - frac, 1, 0}, {0, 1, frac},
+                                  {0, 1 - frac, 1}, {frac, 0, 1}, {1, 0, 1 - frac}};
+      for (int c = 0; c < 3; ++c) pal[static_cast<size_t>(i)][static_cast<size_t>(c)] = std::round(255.0 * table[sector][c]);
+    }
+  }
+  return pal;
+}
+
+void labels_to_image(const std::vector<int>& labels, int w, int h, const std::vector<std::array<double, 3>>& pal,
+                     const std::string& path) {
+  if (labels.size() != static_cast<size_t>(w) * static_cast<size_t>(h))
+    throw fgs::ShapeError("label count does not fill the raster");
+  ImageBuffer img;
+  img.width = w;
+  img.height = h;
+  img.rgb.resize(labels.size() * 3u);
+  for (size_t p = 0; p < labels.size(); ++p) {
+    const int l = labels[p];
+    if (l < 0 || l >= static_cast<int>(pal.size())) throw fgs::RangeError("label " + std::to_string(l) + " has no palette entry");
+    for (int c = 0; c < 3; ++c)
+      img.rgb[3 * p + static_cast<size_t>(c)] =
+          static_cast<unsigned char>(std::clamp(pal[static_cast<size_t>(l)][static_cast<size_t>(c)], 0.0, 255.0));
+  }
+  save_image(img, path);
+}
+
+void difference_image(const std::vector<int>& a, const std::vector<int>& b, int w, int h, const std::string& path) {
+  ImageBuffer img;
+  img.width = w;
+  img.height = h;
+  img.rgb.assign(a.size() * 3u, 0);
+  for (size_t p = 0; p < a.size(); ++p)
+    if (a[p] != b[p]) img.rgb[3 * p] = img.rgb[3 * p + 1] = img.rgb[3 * p + 2] = 255;
+  save_image(img, path);
+}
+
+std::string with_suffix(const std::string& path, const std::string& suffix) {
+  const size_t dot = path.find_last_of('.');
+  if (dot == std::string::npos) return path + suffix;
+  return path.substr(0, dot) + suffix + path.substr(dot);
+}
+
+// ---- segment (commands.cpp:400-448) ----------------------------------------
+int run_segment(Args& a) {
+  CommonOpts o;
+  o.sigma = 90.0;
+  o.k = 4;
+  io_flags(a, &o, true);
+  kernel_flags(a, &o);
+  fastsum_flags(a, &o);
+  method_flags(a, &o);
+  a.finish();
+  Report rep;
+  rep.command = "segment";
+  rep.method = o.method;
+  rep.seed = o.seed;
+  rep.parameters = echo_common(o);
+  const std::string rpath = o.out + ".report.json";
+  return guarded(rep, rpath, [&] {
+    int w = 0, h = 0;
+    const PointCloud cloud = image_to_nodes(o.in, &w, &h);
+    const KernelSpec kernel = make_kernel(o);
+    const EigenPairs pairs = solve_pairs(cloud, kernel, make_params(o), o, &rep);
+    fgs::KMeansOptions ko;
+    ko.seed = o.seed;
+    Timer t;
+    const std::vector<int> labels = fgs::spectral_cluster(pairs, o.k, ko, o.device);
+    rep.add_timing("cluster", t.seconds());
+    labels_to_image(labels, w, h, default_palette(o.k), o.out);
+    std::string summary = "segment: " + std::to_string(w) + "x" + std::to_string(h) + " -> " + o.out + '\n';
+    if (o.with_reference) {
+      if (cloud.size() > kReferenceBudget) {
+        rep.extra["reference_skipped"] = "pixel count exceeds the dense-reference budget";
+      } else {
+        AdjacencyOperator exact(cloud.coordinates, kernel, FastsumParams{}, AdjacencyBackend::Direct, o.device);
+        const EigenPairs dense = dense_reference_eig(exact, o.k);
+        const std::vector<int> dl = fgs::spectral_cluster(dense, o.k, ko, o.device);
+        double diff = 0.0;
+        for (size_t p = 0; p < labels.size(); ++p) diff += labels[p] != dl[p];
+        const double frac = diff / static_cast<double>(labels.size());
+        rep.add_metric("label_difference_fraction", frac,
+                       "fraction of pixels labeled differently from the dense-reference segmentation (same clustering "
+                       "seed)");
+        difference_image(labels, dl, w, h, with_suffix(o.out, ".diff"));
+        summary += "difference vs dense reference: " + std::to_string(frac) + '\n';
+      }
+    }
+    return finish(rep, rpath, summary);
+  });
+}
+
 // ---- ssl-kernel (commands.cpp:531-652) -------------------------------------
 int run_ssl_kernel(Args& a) {
   CommonOpts o;
@@ -1088,7 +1276,7 @@ int run_krr(Args& a) {
 
 const char* kUsage =
     "fgs-b200: matrix-free spectral toolkit for fully connected kernel graphs (B200 build)\n"
-    "usage: fgs-b200 <gen|eigs|cluster|bench|ssl-kernel|krr> [--options]\n";
+    "usage: fgs-b200 <gen|eigs|cluster|segment|bench|ssl-kernel|krr> [--options]\n";
 
 int run(int argc, char** argv) {
   if (argc < 2) {
@@ -1108,7 +1296,8 @@ int run(int argc, char** argv) {
     if (cmd == "bench") return run_bench(a);
     if (cmd == "ssl-kernel") return run_ssl_kernel(a);
     if (cmd == "krr") return run_krr(a);
-    if (cmd == "segment" || cmd == "ssl-pf")
+    if (cmd == "segment") return run_segment(a);
+    if (cmd == "ssl-pf")
       throw UsageError("command '" + cmd + "' is not part of the B200 build");
     throw UsageError("unknown command '" + cmd + "'");
   } catch (const UsageError& e) {  // CLI11::ParseError -> 2

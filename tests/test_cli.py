@@ -90,3 +90,27 @@ def test_csv_input_errors_exit_2(exe, tmp_path):
         assert r.returncode == 2 and "input error" in r.stderr, (name, r.stderr)
     r = run(exe, "eigs", "--in", tmp_path / "missing.csv", "--out", tmp_path / "r.json")
     assert r.returncode == 2 and "cannot open" in r.stderr
+
+
+def write_ppm(path, rgb):
+    h, w, _ = rgb.shape
+    with open(path, "wb") as f:
+        f.write(b"P6\n%d %d\n255\n" % (w, h))
+        f.write(np.ascontiguousarray(rgb, dtype=np.uint8).tobytes())
+
+
+def test_segment_image_input_errors(exe, tmp_path):
+    png = tmp_path / "a.png"
+    png.write_bytes(b"\x89PNG\r\n\x1a\n" + b"\0" * 32)
+    r = run(exe, "segment", "--in", png, "--out", tmp_path / "o.ppm")
+    assert r.returncode == 2 and "libpng" in r.stderr
+    bad = tmp_path / "b.ppm"
+    bad.write_bytes(b"P3\n2 2\n255\n")
+    assert run(exe, "segment", "--in", bad, "--out", tmp_path / "o.ppm").returncode == 2
+    trunc = tmp_path / "t.ppm"
+    trunc.write_bytes(b"P6\n4 4\n255\n" + b"\0" * 10)
+    r = run(exe, "segment", "--in", trunc, "--out", tmp_path / "o.ppm")
+    assert r.returncode == 2 and "truncated" in r.stderr
+    deep = tmp_path / "d.ppm"
+    deep.write_bytes(b"P6\n1 1\n65535\n" + b"\0" * 6)
+    assert run(exe, "segment", "--in", deep, "--out", tmp_path / "o.ppm").returncode == 2

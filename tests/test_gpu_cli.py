@@ -132,3 +132,53 @@ def test_krr_command(tmp_path):
     bare = tmp_path / "bare.csv"
     bare.write_text("x0,x1\n0.1,0.2\n0.3,0.1\n0.5,0.5\n")
     assert run(EXE, "krr", "--in", bare, "--out", tmp_path / "x.json").returncode == 2
+
+
+def _voronoi_image(w, h, sites, seed):
+    rng = np.random.default_rng(seed)
+    pts = rng.uniform(0, 1, (sites, 2)) * [w, h]
+    cols = rng.uniform(0, 255, (sites, 3))
+    yy, xx = np.mgrid[0:h, 0:w]
+    d = (xx[..., None] - pts[:, 0]) ** 2 + (yy[..., None] - pts[:, 1]) ** 2
+    img = cols[np.argmin(d, axis=-1)] + rng.normal(0, 5, (h, w, 3))
+    return np.clip(np.rint(img), 0, 255).astype(np.uint8)
+
+
+def test_segment_small_image_with_reference(tmp_path):
+    from test_cli import write_ppm
+    img = _voronoi_image(80, 60, 4, 2)
+    src = tmp_path / "img.ppm"
+    write_ppm(src, img)
+    out = tmp_path / "seg.ppm"
+    r = run(EXE, "segment", "--in", src, "--out", out, "--with-reference")
+    assert r.returncode == 0, r.stderr
+    rep = json.loads((tmp_path / "seg.ppm.report.json").read_text())
+    check_report(rep)
+    assert rep["command"] == "segment" and rep["parameters"]["sigma"] == 90.0 and rep["parameters"]["k"] == 4
+    assert rep["metrics"]["label_difference_fraction"]["value"] <= 0.01
+    data = out.read_bytes()
+    assert data.startswith(b"P6\n80 60\n255\n") and len(data) == len(b"P6\n80 60\n255\n") + 80 * 60 * 3
+    assert (tmp_path / "seg.diff.ppm").exists()
+
+
+def test_segment_config3_image_matches_api(tmp_path):
+    # BASELINE config 3: the 800 x 600 synthetic image, k = 4, then k-means
+    from test_cli import write_ppm
+    X = fgs.workload_nodes(3, 2024)
+    assert X.shape == (480000, 3)
+    src = tmp_path / "c3.ppm"
+    write_ppm(src, X.reshape(600, 800, 3))
+    out = tmp_path / "c3_seg.ppm"
+    r = run(EXE, "segment", "--in", src, "--out", out, "--N", 32, "--m", 4, "--p", 4)
+    assert r.returncode == 0, r.stderr
+    rep = json.loads((tmp_path / "c3_seg.ppm.report.json").read_text())
+    assert rep["metrics"]["lanczos_converged"]["value"] == 1.0
+    # the same pipeline through the library: identical labels
+    op = fgs.AdjacencyOperator(X, fgs.KernelSpec.gaussian(90.0), fgs.FastsumParams(32, 4, 4, 0.0))
+    pairs = fgs.lanczos_largest(op, 4, fgs.LanczosOptions(tol=1e-12, seed=1))
+    assert np.array_equal(np.array(rep["eigenvalues"]), pairs.values)
+    labels = fgs.spectral_cluster(pairs, 4, fgs.KMeansOptions(seed=1))
+    pal = np.array([[31, 119, 180], [255, 127, 14], [44, 160, 44], [214, 39, 40]], dtype=np.uint8)
+    raw = out.read_bytes()
+    pix = np.frombuffer(raw[len(b"P6\n800 600\n255\n"):], dtype=np.uint8).reshape(-1, 3)
+    assert np.array_equal(pix, pal[labels])
