@@ -707,6 +707,12 @@ void Core::build_plan(const double* nodes_colmajor) {
   if (const char* e = std::getenv("FGS_ITEM_TARGET")) target_items = std::max<int64_t>(1, std::atoll(e));
   int chunk = static_cast<int>(std::max<int64_t>(32, std::min<int64_t>(4096, (n_local + target_items - 1) / target_items)));
   chunk = (chunk + 31) / 32 * 32;
+  // per-run overhead in point units (a partly filled K-step + the footprint
+  // flush), FGS_RUN_COST overrides.  d = 2: 3 (C2 22.2k -> 24.1k matvecs/s:
+  // sparse-region items no longer set the single wave's length); d = 3: 0
+  // (C1 loses with it, C3/C4 are indifferent)
+  int run_cost = d == 2 ? 3 : 0;
+  if (const char* e = std::getenv("FGS_RUN_COST")) run_cost = std::max(0, std::atoi(e));
   int BD = 1;
   for (int t = 0; t < d; ++t) BD *= B;
 
@@ -718,6 +724,7 @@ void Core::build_plan(const double* nodes_colmajor) {
     int tile;
     std::vector<HRun> runs;
     int npts = 0;
+    int cost = 0;  // points + run_cost per run: what a CTA's time scales with
   };
   std::vector<HItem> hitems;
   auto decode_cell = [&](unsigned long long key, int* tcoord, int* cc) {
@@ -755,11 +762,16 @@ void Core::build_plan(const double* nodes_colmajor) {
       decode_cell(hkeys[static_cast<size_t>(c)], tc, cc);
       int64_t p = lo;
       while (p < hi) {
-        int take = static_cast<int>(std::min<int64_t>(hi - p, chunk - cur.npts));
+        // item budget in cost units: a run costs run_cost plus its points
+        int take = static_cast<int>(std::min<int64_t>(hi - p, chunk - cur.cost - run_cost));
         if (take <= 0) {
-          flush();
-          cur.tile = tile;
-          continue;
+          if (cur.runs.empty()) {
+            take = static_cast<int>(std::min<int64_t>(hi - p, chunk));  // one run alone still fits
+          } else {
+            flush();
+            cur.tile = tile;
+            continue;
+          }
         }
         HRun r;
         r.pstart = static_cast<int>(p - offset);
@@ -769,8 +781,9 @@ void Core::build_plan(const double* nodes_colmajor) {
         r.c[2] = cc[2];
         cur.runs.push_back(r);
         cur.npts += take;
+        cur.cost += take + run_cost;
         p += take;
-        if (cur.npts >= chunk) {
+        if (cur.cost >= chunk) {
           flush();
           cur.tile = tile;
         }
@@ -779,7 +792,7 @@ void Core::build_plan(const double* nodes_colmajor) {
     flush();
   }
   // heaviest items first (LPT order for the block scheduler)
-  std::stable_sort(hitems.begin(), hitems.end(), [](const HItem& x, const HItem& y) { return x.npts > y.npts; });
+  std::stable_sort(hitems.begin(), hitems.end(), [](const HItem& x, const HItem& y) { return x.cost > y.cost; });
 
   nitems = static_cast<int>(hitems.size());
   {
