@@ -707,6 +707,7 @@ void Core::build_plan(const double* nodes_colmajor) {
   if (const char* e = std::getenv("FGS_ITEM_TARGET")) target_items = std::max<int64_t>(1, std::atoll(e));
   int chunk = static_cast<int>(std::max<int64_t>(32, std::min<int64_t>(4096, (n_local + target_items - 1) / target_items)));
   chunk = (chunk + 31) / 32 * 32;
+  if (const char* e = std::getenv("FGS_CHUNK")) chunk = std::max(8, std::atoi(e));  // tuning override (cost units)
   // per-run overhead in point units (a partly filled K-step + the footprint
   // flush), FGS_RUN_COST overrides.  d = 2: 3 (C2 22.2k -> 24.1k matvecs/s:
   // sparse-region items no longer set the single wave's length); d = 3: 0
