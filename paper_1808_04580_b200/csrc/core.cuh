@@ -139,6 +139,8 @@ class Core {
 
   // staging buffers for host-vector calls
   DBuf<double> xbuf, ybuf;
+  // Lanczos workspace, reused across solves (lanczos.cu)
+  DBuf<double> lz_basis, lz_z, lz_partial, lz_hbuf, lz_scal, lz_qin;
 
   void set_stream(cudaStream_t s);
   Workspace& workspace(int nvec);

@@ -325,8 +325,17 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   for (int64_t p = 0; p < nl; ++p) local[static_cast<size_t>(p)] = start[static_cast<size_t>(c.host_perm[static_cast<size_t>(c.offset + p)])] / sn;
 
   int64_t cap = std::min<int64_t>(n, 64);
-  DBuf<double> basis, z, partial, hbuf, scal, qin;
+  // workspace kept on the handle between solves: no re-allocation, and the
+  // apply's input/output addresses stay fixed, so its cached CUDA graph is
+  // replayed instead of re-captured on every call
+  DBuf<double>& basis = c.lz_basis;
+  DBuf<double>& z = c.lz_z;
+  DBuf<double>& partial = c.lz_partial;
+  DBuf<double>& hbuf = c.lz_hbuf;
+  DBuf<double>& scal = c.lz_scal;
+  DBuf<double>& qin = c.lz_qin;
   basis.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)) * cap);
+  cap = std::max<int64_t>(cap, std::min<int64_t>(n, static_cast<int64_t>(basis.n) / std::max<int64_t>(nl, 1)));
   z.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)));
   qin.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)));  // fixed apply input -> graph-cached apply
   const int nblk = std::max(1, ceil_div(nl, kRowsPerBlock));
