@@ -593,6 +593,7 @@ Core::~Core() {
   for (auto& evs : ev_pending_)
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  for (cudaEvent_t e : lz_events) cudaEventDestroy(e);
   if (comm) nccl().comm_destroy(comm);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }

@@ -141,6 +141,8 @@ class Core {
   DBuf<double> xbuf, ybuf;
   // Lanczos workspace, reused across solves (lanczos.cu)
   DBuf<double> lz_basis, lz_z, lz_partial, lz_hbuf, lz_scal, lz_qin;
+  DBuf<double> lz_alpha, lz_nrm, lz_beta, lz_st;  // run-ahead recurrence scalars
+  std::vector<cudaEvent_t> lz_events;              // per-step timing events
 
   void set_stream(cudaStream_t s);
   Workspace& workspace(int nvec);

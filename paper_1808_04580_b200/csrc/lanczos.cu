@@ -196,15 +196,44 @@ __global__ void update_kernel(const double* __restrict__ Q, int64_t ldq, int m, 
   z[r] -= acc;
 }
 
-// z -= alpha q_{m-1} + beta q_{m-2}  (spectral.cpp:186-191)
+// z -= alpha q_{m-1} + beta q_{m-2}  (spectral.cpp:186-191); alpha and the
+// previous beta are read from device memory (the host runs ahead)
 __global__ void three_term_kernel(double* __restrict__ z, const double* __restrict__ qcur,
-                                  const double* __restrict__ qprev, const double* __restrict__ alpha, double beta,
-                                  int64_t n) {
+                                  const double* __restrict__ qprev, const double* __restrict__ alpha,
+                                  const double* __restrict__ beta, int64_t n) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (r >= n) return;
   double v = z[r] - alpha[0] * qcur[r];
-  if (qprev) v -= beta * qprev[r];
+  if (qprev) v -= beta[0] * qprev[r];
   z[r] = v;
+}
+
+// step m's scalars on the device: beta = sqrt(|z|^2), the running scale
+// max(|alpha| + beta + beta_prev) and the breakdown test
+// beta > 1e-14 max(scale, 1) (spectral.cpp:197-199, 225); inv = 1 / beta.
+// st[0] = scale, st[1] = 1 / beta (0 on breakdown), st[2] = first
+// breakdown step (+1) or 0.
+__global__ void lanczos_scalars_kernel(const double* __restrict__ alpha, const double* __restrict__ nrm2,
+                                       double* __restrict__ beta, double* __restrict__ st, int m) {
+  const double a = alpha[m - 1];
+  const double b = sqrt(nrm2[m - 1]);
+  const double bp = m >= 2 ? beta[m - 2] : 0.0;
+  const double scale = fmax(st[0], fabs(a) + b + bp);
+  st[0] = scale;
+  if (b > 1e-14 * fmax(scale, 1.0) && st[2] == 0.0) {
+    beta[m - 1] = b;
+    st[1] = 1.0 / b;
+  } else {
+    beta[m - 1] = b;  // the raw value, for the convergence estimate
+    st[1] = 0.0;
+    if (st[2] == 0.0) st[2] = static_cast<double>(m);
+  }
+}
+
+__global__ void scale_dev_kernel(const double* __restrict__ z, const double* __restrict__ inv,
+                                 double* __restrict__ out, int64_t n) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r < n) out[r] = z[r] * inv[0];
 }
 
 __global__ void scale_kernel(const double* __restrict__ z, double inv, double* __restrict__ out, int64_t n) {
@@ -383,9 +412,35 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     tri_size = m;
   };
 
+  // Run-ahead recurrence: alpha_m, |z|^2 and beta_m live in device arrays
+  // and step m's 1/beta is formed on the device (lanczos_scalars_kernel), so
+  // the host enqueues steps without waiting and synchronises only where the
+  // reference needs host values: its geometric convergence checks
+  // (spectral.cpp:200-215), the iteration cap, basis growth, or a
+  // breakdown -- which rolls the run back to that step and takes the
+  // reference's random restart (spectral.cpp:225-238) on the host.
+  const int64_t amax = std::min<int64_t>(n, max_iter) + 2;
+  DBuf<double>& dalpha = c.lz_alpha;
+  DBuf<double>& dnrm = c.lz_nrm;
+  DBuf<double>& dbeta = c.lz_beta;
+  DBuf<double>& dst = c.lz_st;
+  dalpha.alloc(static_cast<size_t>(amax));
+  dnrm.alloc(static_cast<size_t>(amax));
+  dbeta.alloc(static_cast<size_t>(amax));
+  dst.alloc(4);
+  FGS_CUDA(cudaMemsetAsync(dst.p, 0, 4 * sizeof(double), st));
+  const int gsz = ceil_div(std::max<int64_t>(nl, 1), 256);
+
   // per-phase device timing (operator applies vs reorthogonalisation)
-  cudaEvent_t ev[3];
-  for (auto& e : ev) FGS_CUDA(cudaEventCreate(&e));
+  std::vector<cudaEvent_t>& evpool = c.lz_events;  // kept on the handle: no create/destroy per solve
+  auto ev_at = [&](size_t i) {
+    while (evpool.size() <= i) {
+      cudaEvent_t e;
+      FGS_CUDA(cudaEventCreate(&e));
+      evpool.push_back(e);
+    }
+    return evpool[i];
+  };
   double apply_ms = 0.0, reorth_ms = 0.0;
   const auto wall0 = std::chrono::steady_clock::now();
   static const bool trace = std::getenv("FGS_LANCZOS_TRACE") != nullptr;
@@ -393,43 +448,75 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
   };
   double t_launch = 0.0, t_sync = 0.0, t_tri = 0.0;
-  while (true) {
-    const int m = static_cast<int>(alphas.size()) + 1;
-    const double* qcur = basis.p + static_cast<int64_t>(m - 1) * nl;
-    const double h0 = now_ms();
-    FGS_CUDA(cudaEventRecord(ev[0], st));
+  int syncs = 0;
+
+  // enqueue step mm (1-based): z = A q_mm, alpha, three-term, CGS2, |z|^2,
+  // scalars, q_{mm+1} = z / beta (when the basis has room)
+  auto enqueue_step = [&](int mm, size_t evbase) {
+    const double* qcur = basis.p + static_cast<int64_t>(mm - 1) * nl;
+    FGS_CUDA(cudaEventRecord(ev_at(evbase), st));
     FGS_CUDA(cudaMemcpyAsync(qin.p, qcur, sizeof(double) * nl, cudaMemcpyDeviceToDevice, st));
     c.apply(epi, qin.p, nl, z.p, nl, 1, false, true);
-    FGS_CUDA(cudaEventRecord(ev[1], st));
-    ++iterations;
-    // alpha = q . z
-    multidot(qcur, 1, z.p, scal.p);
-    const double beta_prev = m >= 2 ? betas[static_cast<size_t>(m - 2)] : 0.0;
-    three_term_kernel<<<ceil_div(std::max<int64_t>(nl, 1), 256), 256, 0, st>>>(
-        z.p, qcur, m >= 2 ? basis.p + static_cast<int64_t>(m - 2) * nl : nullptr, scal.p, beta_prev, nl);
-    ++c.launches;
-    cgs_pass(m, z.p);
-    cgs_pass(m, z.p);
-    multidot(z.p, 1, z.p, scal.p + 1);
-    FGS_CUDA(cudaEventRecord(ev[2], st));
+    FGS_CUDA(cudaEventRecord(ev_at(evbase + 1), st));
+    multidot(qcur, 1, z.p, dalpha.p + (mm - 1));
+    three_term_kernel<<<gsz, 256, 0, st>>>(z.p, qcur, mm >= 2 ? basis.p + static_cast<int64_t>(mm - 2) * nl : nullptr,
+                                           dalpha.p + (mm - 1), mm >= 2 ? dbeta.p + (mm - 2) : dbeta.p, nl);
+    cgs_pass(mm, z.p);
+    cgs_pass(mm, z.p);
+    multidot(z.p, 1, z.p, dnrm.p + (mm - 1));
+    lanczos_scalars_kernel<<<1, 1, 0, st>>>(dalpha.p, dnrm.p, dbeta.p, dst.p, mm);
+    if (mm < cap) scale_dev_kernel<<<gsz, 256, 0, st>>>(z.p, dst.p + 1, basis.p + static_cast<int64_t>(mm) * nl, nl);
+    c.launches += 3;
+    FGS_CUDA(cudaEventRecord(ev_at(evbase + 2), st));
+  };
+
+  while (true) {
+    const int m0 = static_cast<int>(alphas.size()) + 1;  // first step of this batch
+    // last step before the host must look: check point, cap, basis room, n
+    int mt = m0;
+    while (true) {
+      const bool check = mt >= k && mt >= next_check;
+      const bool stop = iterations + (mt - m0 + 1) >= max_iter || mt == static_cast<int>(n) || mt == cap;
+      if (check || stop) break;
+      ++mt;
+    }
+    const double h0 = now_ms();
+    for (int mm = m0; mm <= mt; ++mm) enqueue_step(mm, 3 * static_cast<size_t>(mm - m0));
     const double h1 = now_ms();
-    double ab[2];
-    FGS_CUDA(cudaMemcpyAsync(ab, scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    const int cnt = mt - m0 + 1;
+    std::vector<double> ha(static_cast<size_t>(cnt)), hb(static_cast<size_t>(cnt)), hs(3);
+    FGS_CUDA(cudaMemcpyAsync(ha.data(), dalpha.p + (m0 - 1), sizeof(double) * cnt, cudaMemcpyDeviceToHost, st));
+    FGS_CUDA(cudaMemcpyAsync(hb.data(), dbeta.p + (m0 - 1), sizeof(double) * cnt, cudaMemcpyDeviceToHost, st));
+    FGS_CUDA(cudaMemcpyAsync(hs.data(), dst.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
     FGS_CUDA(cudaStreamSynchronize(st));
+    ++syncs;
     const double h2 = now_ms();
     t_launch += h1 - h0;
     t_sync += h2 - h1;
-    {
+    const int mb = static_cast<int>(hs[2]);  // first breakdown step of the batch, or 0
+    const int last_valid = mb > 0 ? mb : mt;  // steps after a breakdown ran on garbage
+    for (int mm = m0; mm <= last_valid; ++mm) {
       float t01 = 0.f, t12 = 0.f;
-      FGS_CUDA(cudaEventElapsedTime(&t01, ev[0], ev[1]));
-      FGS_CUDA(cudaEventElapsedTime(&t12, ev[1], ev[2]));
+      const size_t e = 3 * static_cast<size_t>(mm - m0);
+      FGS_CUDA(cudaEventElapsedTime(&t01, ev_at(e), ev_at(e + 1)));
+      FGS_CUDA(cudaEventElapsedTime(&t12, ev_at(e + 1), ev_at(e + 2)));
       apply_ms += t01;
       reorth_ms += t12;
     }
-    const double alpha = ab[0], beta = std::sqrt(ab[1]);
+    iterations += last_valid - m0 + 1;
+    // steps m0 .. last_valid - 1 continue normally: alpha and beta accepted
+    for (int mm = m0; mm < last_valid; ++mm) {
+      const double beta_prev = mm >= 2 ? betas[static_cast<size_t>(mm - 2)] : 0.0;
+      alphas.push_back(ha[static_cast<size_t>(mm - m0)]);
+      scale = std::max(scale, std::abs(alphas.back()) + hb[static_cast<size_t>(mm - m0)] + beta_prev);
+      betas.push_back(hb[static_cast<size_t>(mm - m0)]);
+    }
+    // the batch's last valid step: the reference's per-step decisions
+    const int m = last_valid;
+    const double alpha = ha[static_cast<size_t>(m - m0)], beta = hb[static_cast<size_t>(m - m0)];
+    const double beta_prev = m >= 2 ? betas[static_cast<size_t>(m - 2)] : 0.0;
     alphas.push_back(alpha);
     scale = std::max(scale, std::abs(alpha) + beta + beta_prev);
-
     const bool last = iterations >= max_iter || m == static_cast<int>(n);
     const double h3 = now_ms();
     if (m >= k && (m >= next_check || last)) {  // spectral.cpp:200-215
@@ -451,7 +538,8 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
       converged = true;
       break;
     }
-    if (m == cap) {  // geometric growth (conservativeResize)
+    const bool grew = m == cap;
+    if (grew) {  // geometric growth (conservativeResize)
       const int64_t ncap = std::min<int64_t>(n, cap * 2);
       DBuf<double> nb;
       nb.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)) * ncap);
@@ -464,12 +552,14 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     const double h4 = now_ms();
     t_tri += h4 - h3;
     double* qnext = basis.p + static_cast<int64_t>(m) * nl;
-    if (beta > 1e-14 * std::max(scale, 1.0)) {
+    if (mb == 0 && beta > 1e-14 * std::max(scale, 1.0)) {
       betas.push_back(beta);
-      scale_kernel<<<ceil_div(std::max<int64_t>(nl, 1), 256), 256, 0, st>>>(z.p, 1.0 / beta, qnext, nl);
-      ++c.launches;
-      // reference divides z / beta; multiplying by the reciprocal differs by
-      // one rounding (<= 1 ulp per entry)
+      if (grew) {  // q_{m+1} was not formed before the basis had room
+        scale_dev_kernel<<<gsz, 256, 0, st>>>(z.p, dst.p + 1, qnext, nl);
+        ++c.launches;
+      }
+      // the reference divides z / beta; multiplying by the reciprocal
+      // differs by one rounding (<= 1 ulp per entry)
     } else {
       // breakdown: fresh random direction orthogonal to the basis
       // (spectral.cpp:59-75, 225-238), same RNG stream as the start vector
@@ -483,7 +573,7 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
         cgs_pass(m, z.p);
         const double nv = norm_of(z.p);
         if (nv > 1e-8) {
-          scale_kernel<<<ceil_div(std::max<int64_t>(nl, 1), 256), 256, 0, st>>>(z.p, 1.0 / nv, qnext, nl);
+          scale_kernel<<<gsz, 256, 0, st>>>(z.p, 1.0 / nv, qnext, nl);
           ++c.launches;
           found = true;
         }
@@ -493,10 +583,17 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
         break;
       }
       betas.push_back(0.0);
+      // device state for the next step: beta_m = 0 (the three-term's
+      // beta_prev), breakdown flag cleared, scale as on the host
+      const double zero = 0.0, reset[3] = {scale, 0.0, 0.0};
+      FGS_CUDA(cudaMemcpyAsync(dbeta.p + (m - 1), &zero, sizeof(double), cudaMemcpyHostToDevice, st));
+      FGS_CUDA(cudaMemcpyAsync(dst.p, reset, 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+      FGS_CUDA(cudaStreamSynchronize(st));
     }
   }
 
-  for (auto& e : ev) cudaEventDestroy(e);
+  if (trace)
+    std::fprintf(stderr, "[lanczos] host syncs %d\n", syncs);
   if (trace)
     std::fprintf(stderr,
                  "[lanczos] iters %d  device apply %.2f ms  reorth %.2f ms | host launch %.2f ms  sync-wait %.2f ms  "

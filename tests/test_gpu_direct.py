@@ -98,3 +98,20 @@ def test_block_residuals_after_lanczos_fast_and_direct(orc):
         r = np.linalg.norm(ex.apply_normalized(pairs.vectors) - pairs.vectors * pairs.values, axis=0)
         assert np.max(r) <= 1e-5
         del ex
+
+
+def test_lanczos_breakdown_restart_matches_oracle(orc):
+    # A = three 2x2 swap blocks (three far-apart pairs of coincident nodes):
+    # the Krylov space is exhausted after 2 steps, so k = 4 forces the
+    # reference's random restart (spectral.cpp:225-238) -- on the device the
+    # run-ahead recurrence must roll back to the breakdown step
+    X = np.array([[0.0, 0.0], [0.0, 0.0], [5.0, 0.0], [5.0, 0.0], [0.0, 5.0], [0.0, 5.0]])
+    op = fgs.AdjacencyOperator(X, fgs.KernelSpec.gaussian(0.1), backend=fgs.BACKEND_DIRECT)
+    ref = orc.AdjacencyOperator(X, 0, 0.1, direct=True)
+    li = fgs.LanczosInfo()
+    pairs = fgs.lanczos_largest(op, 4, fgs.LanczosOptions(tol=1e-10, seed=3), li)
+    rv, rV, rit, rconv = ref.lanczos_largest(4, tol=1e-10, seed=3)
+    assert np.allclose(pairs.values, rv, atol=1e-12) and np.allclose(np.abs(pairs.values), 1.0, atol=1e-12)
+    assert li.iterations == rit
+    res = np.linalg.norm(op.apply_normalized(pairs.vectors) - pairs.vectors * pairs.values, axis=0)
+    assert np.max(res) <= 1e-10
