@@ -282,6 +282,28 @@ bool use_v4() {
   return v4;
 }
 
+// d = 2 tensor-core kernels: point-stream warps per CTA.  Interp 2 measured
+// best on C2 (22.8 k vs 22.2 k with 4, 21.7 k with 1), FGS_INTERP2D_P
+// overrides; spread 1, FGS_SPREAD2D_P overrides.
+int interp2d_p() {
+  static const int p = [] {
+    const char* e = std::getenv("FGS_INTERP2D_P");
+    const int v = e ? std::atoi(e) : 2;
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 2;
+  }();
+  return p;
+}
+int spread2d_p() {
+  static const int p = [] {
+    const char* e = std::getenv("FGS_SPREAD2D_P");
+    const int v = e ? std::atoi(e) : 1;
+    return v == 1 || v == 2 || v == 4 ? v : 1;
+  }();
+  return p;
+}
+// staged input window (Blk4d2::XW) of the d = 2 variant with P streams
+size_t xw2d(int p) { return static_cast<size_t>(std::max(64, 32 * p)); }
+
 template <int D, int T>
 constexpr int e_of() {
   return D == 3 ? T : (D == 2 ? (T >= 2 ? T / 2 : 1) : (T >= 2 ? 2 : 1));
@@ -319,8 +341,9 @@ LaunchShape shape_t(bool dense) {
   if constexpr (has_v4_2d<D, T>()) {
     using B4 = Blk4d2<T>;
     if (use_v4()) {
-      interp = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE;
-      if (dense) spread = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE + 2 * B4::QS;
+      // taps double buffer + staged inputs (interp: x and caller index)
+      interp = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE + 2 * xw2d(interp2d_p());
+      if (dense) spread = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE + xw2d(spread2d_p());
     }
   }
   return {B::NT, spread, interp};
@@ -363,12 +386,7 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
   if constexpr (has_v4_2d<D, T>()) {
     if (use_v4() && (interp || dense)) {
       if (interp) {
-        // point-stream warps per CTA (FGS_INTERP2D_P; 2 measured best on C2:
-        // 22.8 k vs 22.2 k with 4, 21.7 k with 1)
-        static const int pi = [] {
-          const char* e = std::getenv("FGS_INTERP2D_P");
-          return e ? std::atoi(e) : 2;
-        }();
+        const int pi = interp2d_p();
         if (pi == 1) {
           auto k = interp_v4_2d_kernel<T, 1>;
           set_smem(reinterpret_cast<const void*>(k), smem);
@@ -387,10 +405,7 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
           launch_ex(k, nitems, Blk4d2<T, 4>::NT, smem, s, a, box_stride);
         }
       } else {
-        static const int ps = [] {
-          const char* e = std::getenv("FGS_SPREAD2D_P");
-          return e ? std::atoi(e) : 1;
-        }();
+        const int ps = spread2d_p();
         if (ps == 4) {
           auto k = spread_v4_2d_kernel<T, 4>;
           set_smem(reinterpret_cast<const void*>(k), smem);
@@ -844,6 +859,19 @@ void Core::build_plan(const double* nodes_colmajor) {
     ditems.push_back(it);
   }
   box_stride = (box_stride + 1) / 2 * 2;  // keep the staging area 16-byte aligned
+  if (std::getenv("FGS_PLAN_STATS")) {  // tuning aid: item sizes and the per-CTA shared memory
+    int64_t box_sum = 0, pts_max = 0, runs_max = 0;
+    for (const DItem& it : ditems) {
+      box_sum += static_cast<int64_t>(it.e0) * it.e1 * it.e2;
+      pts_max = std::max<int64_t>(pts_max, it.p_end - it.p_begin);
+      runs_max = std::max<int64_t>(runs_max, it.run_end - it.run_begin);
+    }
+    std::fprintf(stderr, "[plan] n_local %lld items %d chunk %d run_cost %d mean_run %.2f | box max %lld mean %.1f | "
+                 "item points max %lld runs max %lld\n", static_cast<long long>(n_local), nitems, chunk, run_cost,
+                 mean_run, static_cast<long long>(box_stride),
+                 nitems ? static_cast<double>(box_sum) / nitems : 0.0, static_cast<long long>(pts_max),
+                 static_cast<long long>(runs_max));
+  }
   if (static_cast<double>(std::max(nitems, 1)) * static_cast<double>(box_stride) > 2.0e9)
     fail(FGS_ERESOURCE, "spread workspace exceeds 2^31 entries");
   // Deterministic assembly map: for every grid cell, the private-box entries
@@ -1049,12 +1077,16 @@ size_t Core::smem_bytes(bool interp) const {
   const LaunchShape sh = d == 3 ? shape_of<3>(T, dense) : (d == 2 ? shape_of<2>(T, dense) : shape_of<1>(T, dense));
   size_t boxes = static_cast<size_t>(box_stride);
   if (d == 3 && !interp && dense && use_v4()) boxes *= static_cast<size_t>(v4_spread_groups(T));  // per-group boxes
+  if (d == 2 && !interp && dense && use_v4() && (T == 8 || T == 12 || T == 16))
+    boxes *= static_cast<size_t>(spread2d_p());  // per-stream boxes
   return (boxes + (interp ? sh.extra_interp : sh.extra_spread)) * sizeof(double);
 }
 
 void Core::launch_spread(const PassArgs& a) {
   if (nitems == 0) return;
   const size_t smem = smem_bytes(false);
+  if (std::getenv("FGS_PLAN_STATS") && launches == 0)
+    std::fprintf(stderr, "[plan] smem per CTA: spread %zu B, interp %zu B\n", smem, smem_bytes(true));
   if (smem > 227 * 1024) fail(FGS_ERESOURCE, "tile box exceeds shared memory (cutoff too large for d = 3)");
   const bool dense = mean_run >= kDenseRun;
   if (d == 3) dispatch<3>(false, dense, T, a, nitems, smem, static_cast<int>(box_stride), stream);

@@ -143,6 +143,7 @@ class Core {
   DBuf<double> lz_basis, lz_z, lz_partial, lz_hbuf, lz_scal, lz_qin;
   DBuf<double> lz_alpha, lz_nrm, lz_beta, lz_st;  // run-ahead recurrence scalars
   std::vector<cudaEvent_t> lz_events;              // per-step timing events
+  DBuf<unsigned> lz_ticket;                        // last-block reduction tickets (reset by their kernels)
 
   void set_stream(cudaStream_t s);
   Workspace& workspace(int nvec);

@@ -438,16 +438,71 @@ struct Blk4d2 {
   static constexpr int TAPS = 2 * T;
   static constexpr int STRIDE = (TAPS % 16 == 4 || TAPS % 16 == 12) ? TAPS
                               : (TAPS % 16 == 0 ? TAPS + 4 : TAPS + ((12 - TAPS % 16 + 16) % 16));
+  // points whose caller-order inputs are staged at once (a multiple of QS)
+  static constexpr int XW = NT > 64 ? NT : 64;
 };
+
+// Per-point inputs of a window of internal points [w0, min(w0 + XW, p_end))
+// staged in shared memory with every load of the window in flight at once:
+// the caller-order gather x[perm[j]] is a two-load dependent chain, and
+// fetched one chunk at a time it stalled the 2-D kernels for ~30 % (spread)
+// and ~11 % (interp) of their samples (ncu source page, r01_c2_full).
+//   xs[o]  spread: x (times s when the pass scales its input), as v2_x
+//   xs[o], ixs[o]  interp: epilogue input x and the caller index of the store
+template <int NT, int XW>
+__device__ __forceinline__ void v4_stage_spread_x(const PassArgs& a, const double* xv, int64_t w0, int64_t p_end,
+                                                  double* xs, int tid) {
+  constexpr int U = XW / NT;
+  int64_t ix[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = w0 + u * NT + tid;
+    ix[u] = j < p_end ? (a.perm ? static_cast<int64_t>(a.perm[j]) : j) : -1;
+  }
+  double xr[U], sr[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    xr[u] = ix[u] >= 0 ? xv[ix[u]] : 0.0;
+    sr[u] = ix[u] >= 0 && a.scale_input ? a.s[w0 + u * NT + tid] : 1.0;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (ix[u] >= 0) xs[u * NT + tid] = a.scale_input ? __dmul_rn(sr[u], xr[u]) : xr[u];
+}
+
+template <int NT, int XW>
+__device__ __forceinline__ void v4_stage_interp_x(const PassArgs& a, const double* xv, int64_t w0, int64_t p_end,
+                                                  double* xs, int64_t* ixs, int tid) {
+  constexpr int U = XW / NT;
+  const bool need_x = xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE;
+  int64_t ix[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = w0 + u * NT + tid;
+    ix[u] = j < p_end ? (a.perm ? static_cast<int64_t>(a.perm[j]) : j) : -1;
+  }
+  double xr[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) xr[u] = need_x && ix[u] >= 0 ? xv[ix[u]] : 0.0;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (ix[u] >= 0) {
+      xs[u * NT + tid] = xr[u];
+      ixs[u * NT + tid] = ix[u];
+    }
+}
 
 template <int T, int PS = 4>
 __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) interp_v4_2d_kernel(PassArgs a, int box_stride_smem) {
   pdl_wait();
   using B = Blk4d2<T, PS>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE, NC = B::NC, KS = B::KS;
+  constexpr int XW = B::XW;
   extern __shared__ __align__(16) double smem[];
   double* S = smem;
   double* stg = smem + box_stride_smem;
+  double* xs = stg + 2 * QS * SR;
+  int64_t* ixs = reinterpret_cast<int64_t*>(xs + XW);
   const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
   const int q = lane & 3, r8 = lane >> 2;
   const DItem it = a.items[blockIdx.x];
@@ -463,6 +518,7 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) interp_v4_2d_kernel(PassArg
     double* yv = a.y ? a.y + vec * a.ldy : nullptr;
     v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
     cp_async_commit();
+    v4_stage_interp_x<NT, XW>(a, xv, p_begin, p_end, xs, ixs, tid);
     for (int v = tid; v < V; v += NT) {
       const int x2 = v % bx2, x1 = v / bx2;
       S[v] = gv[static_cast<int64_t>((it.a1 + x1) % M) * M + (it.a2 + x2) % M];
@@ -475,6 +531,11 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) interp_v4_2d_kernel(PassArg
       const int64_t c0 = p_begin + static_cast<int64_t>(k) * QS;
       const int64_t c1 = lmin(c0 + QS, p_end);
       const int buf = k & 1;
+      const int xo = (k * QS) % XW;  // chunk offset in the staged window
+      if (k > 0 && xo == 0) {        // next window (items longer than XW points)
+        __syncthreads();
+        v4_stage_interp_x<NT, XW>(a, xv, c0, p_end, xs, ixs, tid);
+      }
       cp_async_wait_0();
       __syncthreads();
       if (k + 1 < nch) {
@@ -489,8 +550,9 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) interp_v4_2d_kernel(PassArg
         double xin = 0.0, sin_ = 1.0;
         int64_t ix = 0;
         if (q == 0 && in_chunk) {
-          ix = a.perm ? static_cast<int64_t>(a.perm[ipt]) : ipt;
-          if (xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE) xin = xv[ix];
+          const int o = xo + static_cast<int>(ipt - c0);
+          ix = ixs[o];
+          xin = xs[o];
           if (a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN) sin_ = a.s[ipt];
         }
         double wc[NC][2];  // c = 8 nc + 2 q + i
@@ -566,9 +628,13 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) spread_v4_2d_kernel(PassArg
   pdl_wait();
   using B = Blk4d2<T, PS>;
   constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, P = B::P, SR = B::STRIDE, NC = B::NC, NE = B::NE;
+  constexpr int XW = B::XW;
   extern __shared__ __align__(16) double smem[];
+  // one private box per point stream (a d = 2 box is a few KB): flushes need
+  // no barrier, the boxes are summed in stream order at the end of the item
+  constexpr int NB = P;
   double* S = smem;
-  double* stg = smem + box_stride_smem;
+  double* stg = smem + NB * box_stride_smem;
   double* xs = stg + 2 * QS * SR;
   const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
   const int q = lane & 3, r8 = lane >> 2;
@@ -580,10 +646,11 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) spread_v4_2d_kernel(PassArg
 
   for (int vec = 0; vec < a.nvec; ++vec) {
     const double* xv = a.x + vec * a.ldx;
-    for (int v = tid; v < V; v += NT) S[v] = 0.0;
+    for (int g = 0; g < NB; ++g)
+      for (int v = tid; v < V; v += NT) S[g * box_stride_smem + v] = 0.0;
     v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
     cp_async_commit();
-    if (tid < QS && p_begin + tid < p_end) xs[tid] = v2_x(a, xv, p_begin + tid);
+    v4_stage_spread_x<NT, XW>(a, xv, p_begin, p_end, xs, tid);
     int r = it.run_begin;
     DRun run = a.runs[r];
     double C[NC][NE][2];  // C[m = c][n = e]: lane holds c = 8 mc + lane/4, e = 8 ne + 2 (lane%4) + i
@@ -593,42 +660,39 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) spread_v4_2d_kernel(PassArg
       for (int ne = 0; ne < NE; ++ne) C[mc][ne][0] = C[mc][ne][1] = 0.0;
     auto flush = [&]() {
       const int o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
-      for (int g = 0; g < P; ++g) {
-        if (g == grp) {
+      double* Sg = S + grp * box_stride_smem;
 #pragma unroll
-          for (int mc = 0; mc < NC; ++mc) {
-            const int cc = 8 * mc + r8;
-            double* row = S + (o1 + (cc < T ? cc : 0)) * bx2 + o2;
+      for (int mc = 0; mc < NC; ++mc) {
+        const int cc = 8 * mc + r8;
+        double* row = Sg + (o1 + (cc < T ? cc : 0)) * bx2 + o2;
 #pragma unroll
-            for (int ne = 0; ne < NE; ++ne)
+        for (int ne = 0; ne < NE; ++ne)
 #pragma unroll
-              for (int i = 0; i < 2; ++i) {
-                const int e = 8 * ne + 2 * q + i;
-                if (cc < T && e < T) row[e] += C[mc][ne][i];
-                C[mc][ne][i] = 0.0;
-              }
+          for (int i = 0; i < 2; ++i) {
+            const int e = 8 * ne + 2 * q + i;
+            if (cc < T && e < T) row[e] += C[mc][ne][i];
+            C[mc][ne][i] = 0.0;
           }
-        }
-        __syncthreads();
       }
+      __syncwarp();
     };
     for (int k = 0; k < nch; ++k) {
       const int64_t c0 = p_begin + static_cast<int64_t>(k) * QS;
       const int64_t c1 = lmin(c0 + QS, p_end);
       const int buf = k & 1;
+      const int xo = (k * QS) % XW;  // chunk offset in the staged window
+      if (k > 0 && xo == 0) {        // next window (items longer than XW points)
+        __syncthreads();
+        v4_stage_spread_x<NT, XW>(a, xv, c0, p_end, xs, tid);
+      }
       cp_async_wait_0();
       __syncthreads();
-      const bool more = k + 1 < nch;
-      double xnext = 0.0;
-      int qn = 0;
-      if (more) {
-        qn = static_cast<int>(lmin(QS, p_end - c1));
-        v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, qn, tid, NT);
+      if (k + 1 < nch) {
+        v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, static_cast<int>(lmin(QS, p_end - c1)), tid, NT);
         cp_async_commit();
-        if (tid < qn) xnext = v2_x(a, xv, c1 + tid);
       }
       const double* sb = stg + buf * QS * SR;
-      const double* xb = xs + buf * QS;
+      const double* xb = xs + xo;
       while (true) {
         const int64_t rs = run.pstart, re_ = static_cast<int64_t>(run.pstart) + run.pcount;
         const int64_t s0 = rs > c0 ? rs : c0, s1 = lmin(re_, c1);
@@ -662,11 +726,15 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) spread_v4_2d_kernel(PassArg
         }
         break;
       }
-      if (more && tid < qn) xs[(buf ^ 1) * QS + tid] = xnext;
     }
     __syncthreads();
     double* out = a.priv + (static_cast<int64_t>(vec) * gridDim.x + blockIdx.x) * a.box_stride;
-    for (int v = tid; v < V; v += NT) out[v] = S[v];
+    for (int v = tid; v < V; v += NT) {
+      double sum = S[v];
+#pragma unroll
+      for (int g = 1; g < NB; ++g) sum += S[g * box_stride_smem + v];
+      out[v] = sum;
+    }
     __syncthreads();
   }
 }

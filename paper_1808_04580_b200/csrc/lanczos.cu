@@ -33,29 +33,32 @@ inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) 
 
 // partial[b][j] = sum over block b's rows of Q[r, j] * z[r], j < m
 // (32 columns at a time per warp, transposed through a warp butterfly).
-__global__ void __launch_bounds__(kRedThreads) multidot_kernel(const double* __restrict__ Q, int64_t ldq, int m,
-                                                               const double* __restrict__ z, int64_t n,
-                                                               double* __restrict__ partial) {
+// zr: this thread's rows r = row0 + tid + i * kRedThreads, i < kRowsPerThread.
+__device__ __forceinline__ void multidot_block(const double* __restrict__ Q, int64_t ldq, int m,
+                                               const double (&zr)[kRowsPerThread], int64_t row0, int64_t n,
+                                               double* __restrict__ partial) {
   __shared__ double red[kRedThreads / 32][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
-  double zr[kRowsPerThread];
-#pragma unroll
-  for (int i = 0; i < kRowsPerThread; ++i) {
-    const int64_t r = row0 + threadIdx.x + static_cast<int64_t>(i) * kRedThreads;
-    zr[i] = r < n ? z[r] : 0.0;
-  }
   for (int j0 = 0; j0 < m; j0 += 32) {
     double p[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       double acc = 0.0;
       if (j0 + c < m) {
+        // the column's loads first, read-only path: inlined into the fused
+        // kernels (which also store) nvcc otherwise issued load, fma, load,
+        // ... one latency per row (3.5 vs 0.9 us per column at C2)
         const double* col = Q + static_cast<int64_t>(j0 + c) * ldq;
+        double qv[kRowsPerThread];
 #pragma unroll
         for (int i = 0; i < kRowsPerThread; ++i) {
           const int64_t r = row0 + threadIdx.x + static_cast<int64_t>(i) * kRedThreads;
-          if (r < n) acc = fma(col[r], zr[i], acc);
+          qv[i] = r < n ? __ldg(col + r) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < kRowsPerThread; ++i) {
+          const int64_t r = row0 + threadIdx.x + static_cast<int64_t>(i) * kRedThreads;
+          if (r < n) acc = fma(qv[i], zr[i], acc);
         }
       }
       p[c] = acc;
@@ -79,6 +82,133 @@ __global__ void __launch_bounds__(kRedThreads) multidot_kernel(const double* __r
       if (j0 + lane < m) partial[static_cast<int64_t>(blockIdx.x) * m + j0 + lane] = s;
     }
     __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void load_rows(const double* __restrict__ z, int64_t row0, int64_t n,
+                                          double (&zr)[kRowsPerThread]) {
+#pragma unroll
+  for (int i = 0; i < kRowsPerThread; ++i) {
+    const int64_t r = row0 + threadIdx.x + static_cast<int64_t>(i) * kRedThreads;
+    zr[i] = r < n ? z[r] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) multidot_kernel(const double* __restrict__ Q, int64_t ldq, int m,
+                                                               const double* __restrict__ z, int64_t n,
+                                                               double* __restrict__ partial) {
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
+  double zr[kRowsPerThread];
+  load_rows(z, row0, n, zr);
+  multidot_block(Q, ldq, m, zr, row0, n, partial);
+}
+
+// ---- fused single-device step kernels ------------------------------------
+// The block partials are summed by the last block to finish (an atomic
+// ticket), in exactly reduce_partials_kernel's order, so the fused step is
+// bitwise identical to the unfused one while launching half the kernels
+// (C2: ~13 launches of a few microseconds each per step were most of the
+// reorthogonalisation time).
+__device__ __forceinline__ bool last_block_done(unsigned* ticket) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+__device__ __forceinline__ void reduce_cols_block(const double* partial, int nblocks, int m, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < m; j += kRedThreads / 32) {
+    double s = 0.0;
+    for (int b = lane; b < nblocks; b += 32) s += __ldcg(partial + static_cast<int64_t>(b) * m + j);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) out[j] = s;
+  }
+}
+
+// out[0..m) = Q^T z (one launch)
+__global__ void __launch_bounds__(kRedThreads) multidot_reduce_kernel(const double* __restrict__ Q, int64_t ldq, int m,
+                                                                      const double* __restrict__ z, int64_t n,
+                                                                      double* partial, unsigned* ticket,
+                                                                      double* __restrict__ out) {
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
+  double zr[kRowsPerThread];
+  load_rows(z, row0, n, zr);
+  multidot_block(Q, ldq, m, zr, row0, n, partial);
+  if (ticket && last_block_done(ticket)) {  // else the caller launches reduce_partials_kernel
+    reduce_cols_block(partial, gridDim.x, m, out);
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+}
+
+// z -= alpha q_cur + beta q_prev (three_term_kernel), then out = Q^T z
+__global__ void __launch_bounds__(kRedThreads) three_term_multidot_kernel(
+    double* __restrict__ z, const double* __restrict__ qcur, const double* __restrict__ qprev,
+    const double* __restrict__ alpha, const double* __restrict__ beta, const double* __restrict__ Q, int64_t ldq,
+    int m, int64_t n, double* partial, unsigned* ticket, double* __restrict__ out) {
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
+  const double a = alpha[0], b = qprev ? beta[0] : 0.0;
+  double zr[kRowsPerThread];
+#pragma unroll
+  for (int i = 0; i < kRowsPerThread; ++i) {
+    const int64_t r = row0 + threadIdx.x + static_cast<int64_t>(i) * kRedThreads;
+    double v = 0.0;
+    if (r < n) {
+      v = z[r] - a * qcur[r];
+      if (qprev) v -= b * qprev[r];
+      z[r] = v;
+    }
+    zr[i] = v;
+  }
+  multidot_block(Q, ldq, m, zr, row0, n, partial);
+  if (ticket && last_block_done(ticket)) {  // else the caller launches reduce_partials_kernel
+    reduce_cols_block(partial, gridDim.x, m, out);
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+}
+
+// |z|^2 (multidot_kernel of z with itself), then step m's scalars
+// (lanczos_scalars_kernel) in the last block
+__global__ void __launch_bounds__(kRedThreads) norm_scalars_kernel(
+    const double* __restrict__ z, int64_t n, double* partial, unsigned* ticket, const double* __restrict__ alpha,
+    double* __restrict__ nrm2, double* __restrict__ beta, double* __restrict__ st, int step) {
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
+  double zr[kRowsPerThread];
+  load_rows(z, row0, n, zr);
+  multidot_block(z, n, 1, zr, row0, n, partial);
+  if (last_block_done(ticket)) {
+    reduce_cols_block(partial, gridDim.x, 1, nrm2 + (step - 1));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double a = alpha[step - 1];
+      const double b = sqrt(nrm2[step - 1]);
+      const double bp = step >= 2 ? beta[step - 2] : 0.0;
+      const double scale = fmax(st[0], fabs(a) + b + bp);
+      st[0] = scale;
+      beta[step - 1] = b;
+      if (b > 1e-14 * fmax(scale, 1.0) && st[2] == 0.0) {
+        st[1] = 1.0 / b;
+      } else {
+        st[1] = 0.0;
+        if (st[2] == 0.0) st[2] = static_cast<double>(step);
+      }
+      *ticket = 0u;
+    }
+  }
+}
+
+// q_{m+1} = z / beta into the basis and the apply input
+__global__ void scale2_kernel(const double* __restrict__ z, const double* __restrict__ inv, double* __restrict__ out,
+                              double* __restrict__ out2, int64_t n) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r < n) {
+    const double v = z[r] * inv[0];
+    out[r] = v;
+    out2[r] = v;
   }
 }
 
@@ -452,7 +582,62 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
 
   // enqueue step mm (1-based): z = A q_mm, alpha, three-term, CGS2, |z|^2,
   // scalars, q_{mm+1} = z / beta (when the basis has room)
+  // single device: fused step kernels (last-block reductions, the three-term
+  // folded into the first Gram-Schmidt product, the second update into the
+  // norm and the scalars), bitwise identical to the unfused sequence below,
+  // which sharded runs keep for their allreduces; FGS_LANCZOS_FUSED=0 forces it
+  static const bool fused_env = [] {
+    const char* e = std::getenv("FGS_LANCZOS_FUSED");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool fused = fused_env && !c.sharded;
+  DBuf<unsigned>& ticket = c.lz_ticket;
+  if (!ticket.p) {
+    ticket.alloc(4);
+    FGS_CUDA(cudaMemsetAsync(ticket.p, 0, 4 * sizeof(unsigned), st));
+  }
+  int qin_holds = 0;  // basis column (1-based) currently in qin, 0 = none
+  auto enqueue_fused = [&](int mm, size_t evbase) {
+    const double* qcur = basis.p + static_cast<int64_t>(mm - 1) * nl;
+    FGS_CUDA(cudaEventRecord(ev_at(evbase), st));
+    if (qin_holds != mm) FGS_CUDA(cudaMemcpyAsync(qin.p, qcur, sizeof(double) * nl, cudaMemcpyDeviceToDevice, st));
+    c.apply(epi, qin.p, nl, z.p, nl, 1, false, true);
+    FGS_CUDA(cudaEventRecord(ev_at(evbase + 1), st));
+    // one block sums the partials when they are few (C2: 49 blocks); many
+    // blocks x columns (C4: 977 x 76) would serialise on it, so those
+    // products keep the separate column-parallel reduction
+    const bool tail = static_cast<int64_t>(nblk) * mm <= 8192;
+    multidot_reduce_kernel<<<nblk, kRedThreads, 0, st>>>(qcur, nl, 1, z.p, nl, partial.p, ticket.p,
+                                                        dalpha.p + (mm - 1));
+    three_term_multidot_kernel<<<nblk, kRedThreads, 0, st>>>(
+        z.p, qcur, mm >= 2 ? basis.p + static_cast<int64_t>(mm - 2) * nl : nullptr, dalpha.p + (mm - 1),
+        mm >= 2 ? dbeta.p + (mm - 2) : dbeta.p, basis.p, nl, mm, nl, partial.p, tail ? ticket.p : nullptr, hbuf.p);
+    if (!tail) {
+      reduce_partials_kernel<<<ceil_div(mm, 8), 256, 0, st>>>(partial.p, nblk, mm, hbuf.p, 0);
+      ++c.launches;
+    }
+    update_kernel<<<gsz, 256, sizeof(double) * mm, st>>>(basis.p, nl, mm, hbuf.p, z.p, nl);
+    multidot_reduce_kernel<<<nblk, kRedThreads, 0, st>>>(basis.p, nl, mm, z.p, nl, partial.p,
+                                                        tail ? ticket.p : nullptr, hbuf.p);
+    if (!tail) {
+      reduce_partials_kernel<<<ceil_div(mm, 8), 256, 0, st>>>(partial.p, nblk, mm, hbuf.p, 0);
+      ++c.launches;
+    }
+    update_kernel<<<gsz, 256, sizeof(double) * mm, st>>>(basis.p, nl, mm, hbuf.p, z.p, nl);
+    norm_scalars_kernel<<<nblk, kRedThreads, 0, st>>>(z.p, nl, partial.p, ticket.p, dalpha.p, dnrm.p, dbeta.p, dst.p,
+                                                     mm);
+    c.launches += 6;
+    if (mm < cap) {
+      scale2_kernel<<<gsz, 256, 0, st>>>(z.p, dst.p + 1, basis.p + static_cast<int64_t>(mm) * nl, qin.p, nl);
+      ++c.launches;
+      qin_holds = mm + 1;
+    } else {
+      qin_holds = 0;
+    }
+    FGS_CUDA(cudaEventRecord(ev_at(evbase + 2), st));
+  };
   auto enqueue_step = [&](int mm, size_t evbase) {
+    if (fused) return enqueue_fused(mm, evbase);
     const double* qcur = basis.p + static_cast<int64_t>(mm - 1) * nl;
     FGS_CUDA(cudaEventRecord(ev_at(evbase), st));
     FGS_CUDA(cudaMemcpyAsync(qin.p, qcur, sizeof(double) * nl, cudaMemcpyDeviceToDevice, st));
@@ -563,6 +748,7 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     } else {
       // breakdown: fresh random direction orthogonal to the basis
       // (spectral.cpp:59-75, 225-238), same RNG stream as the start vector
+      qin_holds = 0;  // the host forms q_{m+1}
       bool found = false;
       for (int attempt = 0; attempt < 8 && !found; ++attempt) {
         std::vector<double> v(static_cast<size_t>(n));
