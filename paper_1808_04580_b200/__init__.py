@@ -688,4 +688,5 @@ def workload_nodes(config: int, seed: int = 2024) -> np.ndarray:
 def workload_vectors(n: int, nvec: int, seed: int) -> np.ndarray:
     out = np.zeros(n * nvec)
     _check(lib().fgs_workload_vectors(C.c_int64(n), int(nvec), C.c_uint64(seed), _dp(out)))
-    return out.reshape(nvec, n).T.copy() if nvec > 1 else out
+    # column-major (n, nvec): vector j contiguous, the layout the C ABI takes
+    return out.reshape(nvec, n).T if nvec > 1 else out

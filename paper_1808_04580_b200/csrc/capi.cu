@@ -100,7 +100,7 @@ int epilogue_of(fgs_op op, bool* scale) {
 void upload_block(Core& c, fgsb::DBuf<double>& dst, const double* src, int64_t n, int nvec, int64_t ld) {
   dst.alloc(static_cast<size_t>(n) * nvec);
   if (ld == n) {
-    FGS_CUDA(cudaMemcpyAsync(dst.p, src, sizeof(double) * n * nvec, cudaMemcpyHostToDevice, c.stream));
+    c.host_copy(true, dst.p, src, sizeof(double) * n * nvec);
   } else {
     FGS_CUDA(cudaMemcpy2DAsync(dst.p, sizeof(double) * n, src, sizeof(double) * ld, sizeof(double) * n, nvec,
                                cudaMemcpyHostToDevice, c.stream));
@@ -108,7 +108,7 @@ void upload_block(Core& c, fgsb::DBuf<double>& dst, const double* src, int64_t n
 }
 void download_block(Core& c, double* dst, const fgsb::DBuf<double>& src, int64_t n, int nvec, int64_t ld) {
   if (ld == n) {
-    FGS_CUDA(cudaMemcpyAsync(dst, src.p, sizeof(double) * n * nvec, cudaMemcpyDeviceToHost, c.stream));
+    c.host_copy(false, dst, src.p, sizeof(double) * n * nvec);
   } else {
     FGS_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ld, src.p, sizeof(double) * n, sizeof(double) * n, nvec,
                                cudaMemcpyDeviceToHost, c.stream));

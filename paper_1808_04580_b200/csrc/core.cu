@@ -11,6 +11,7 @@
 #include <mutex>
 #include <cstring>
 #include <numeric>
+#include <thread>
 
 #include "core.cuh"
 #include "kernels.cuh"
@@ -610,7 +611,65 @@ Core::~Core() {
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   for (cudaEvent_t e : lz_events) cudaEventDestroy(e);
   if (comm) nccl().comm_destroy(comm);
+  if (bounce) cudaFreeHost(bounce);
   if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+namespace {
+constexpr size_t kBounceChunk = size_t(4) << 20;
+constexpr size_t kBounceMin = size_t(16) << 20;  // below: one plain async copy
+}  // namespace
+
+void Core::host_copy(bool to_device, void* dst, const void* src, size_t bytes) {
+  const void* host = to_device ? src : dst;
+  cudaPointerAttributes at{};
+  const bool pinned = cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  const int hw = static_cast<int>(std::thread::hardware_concurrency());
+  const int T = std::max(1, std::min(8, hw / 2));
+  if (bytes < kBounceMin || pinned || T < 2) {
+    FGS_CUDA(cudaMemcpyAsync(dst, src, bytes, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, stream));
+    if (!to_device || pinned) FGS_CUDA(cudaStreamSynchronize(stream));
+    return;
+  }
+  if (!bounce || bounce_threads < T) {
+    if (bounce) FGS_CUDA(cudaFreeHost(bounce));
+    bounce = nullptr;
+    FGS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&bounce), kBounceChunk * T, cudaHostAllocPortable));
+    bounce_threads = T;
+  }
+  cudaEvent_t ready;
+  FGS_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  FGS_CUDA(cudaEventRecord(ready, stream));
+  std::vector<std::thread> workers;
+  std::vector<cudaError_t> errs(static_cast<size_t>(T), cudaSuccess);
+  for (int t = 0; t < T; ++t) {
+    workers.emplace_back([&, t] {
+      cudaError_t e = cudaSetDevice(device);
+      cudaStream_t s = nullptr;
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ready, 0);
+      char* buf = bounce + kBounceChunk * static_cast<size_t>(t);
+      const size_t lo = bytes * static_cast<size_t>(t) / T, hi = bytes * static_cast<size_t>(t + 1) / T;
+      for (size_t off = lo; off < hi && e == cudaSuccess; off += kBounceChunk) {
+        const size_t len = std::min(kBounceChunk, hi - off);
+        if (to_device) {
+          std::memcpy(buf, static_cast<const char*>(src) + off, len);
+          e = cudaMemcpyAsync(static_cast<char*>(dst) + off, buf, len, cudaMemcpyHostToDevice, s);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // before the bounce is refilled
+        } else {
+          e = cudaMemcpyAsync(buf, static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, s);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+          if (e == cudaSuccess) std::memcpy(static_cast<char*>(dst) + off, buf, len);
+        }
+      }
+      if (s) cudaStreamDestroy(s);
+      errs[static_cast<size_t>(t)] = e;
+    });
+  }
+  for (auto& w : workers) w.join();
+  cudaEventDestroy(ready);
+  for (cudaError_t e : errs) FGS_CUDA(e);
 }
 
 void Core::set_stream(cudaStream_t s) {

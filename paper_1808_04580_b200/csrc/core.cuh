@@ -143,6 +143,8 @@ class Core {
   DBuf<double> lz_basis, lz_z, lz_partial, lz_hbuf, lz_scal, lz_qin;
   DBuf<double> lz_alpha, lz_nrm, lz_beta, lz_st;  // run-ahead recurrence scalars
   std::vector<cudaEvent_t> lz_events;              // per-step timing events
+  char* bounce = nullptr;  // pinned staging for host_copy (bounce_threads x kBounceChunk)
+  int bounce_threads = 0;
   DBuf<unsigned> lz_ticket;                        // last-block reduction tickets (reset by their kernels)
 
   void set_stream(cudaStream_t s);
@@ -157,6 +159,12 @@ class Core {
   // ybuf) when both host buffers are pinned; false -> caller stages itself.
   // Does not synchronise.
   bool apply_host_graph(int epilogue, const double* hx, double* hy, int64_t ld, int nvec, bool scale_input);
+  // Contiguous host <-> device copy ordered after the work queued on
+  // `stream`; returns when the data has landed.  Large copies to or from
+  // pageable memory go through per-thread pinned bounce buffers so the host
+  // side (memcpy and first-touch page faults, the bound for fresh output
+  // arrays) runs on several cores while the copy engine streams.
+  void host_copy(bool to_device, void* dst, const void* src, size_t bytes);
   void compute_degrees(int64_t* bad_node);
 
   // complex NFFT transforms (NfftPlan), interleaved complex on device

@@ -838,8 +838,7 @@ void lanczos_finish_vectors(Core& c, LanczosResult& r, const std::vector<int>& o
   colmax_partial_kernel<<<dim3(parts, cnt), 256, 0, st>>>(Vc.p, n, n, chunk, pval.p, pidx.p, psigned.p);
   colsign_kernel<<<dim3(gx, cnt), 256, 0, st>>>(Vc.p, n, n, pval.p, psigned.p, parts);
   c.launches += 3;
-  FGS_CUDA(cudaMemcpyAsync(host_out, Vc.p, sizeof(double) * n * cnt, cudaMemcpyDeviceToHost, st));
-  FGS_CUDA(cudaStreamSynchronize(st));
+  c.host_copy(false, host_out, Vc.p, sizeof(double) * n * cnt);
   FGS_CUDA(cudaGetLastError());
 }
 
