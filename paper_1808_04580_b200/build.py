@@ -24,6 +24,8 @@ SOURCES = ["core.cu", "lanczos.cu", "capi.cu", "peak.cu", "kmeans.cu", "cg.cu", 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 NVFLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-O3"]
+# tuning builds: extra nvcc defines, e.g. FGS_NVCC_DEFINES="FGS_INTERP12_MINB=3"
+NVFLAGS += ["-D" + d for d in os.environ.get("FGS_NVCC_DEFINES", "").split() if d]
 
 
 def _deps():

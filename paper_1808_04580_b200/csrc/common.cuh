@@ -50,17 +50,13 @@ struct Error : std::runtime_error {
 // kernel's CTAs are resident and waiting when its predecessor drains
 // instead of paying the launch gap.  A no-op when launched without the
 // attribute.  FGS_PDL selects the mode (see pdl_mode).
-// g_pdl_early: 1 = let the successor launch as soon as every CTA of this
-// grid has passed its wait (FGS_PDL=1), 0 = implicit trigger at grid end.
-__device__ int g_pdl_early;
+// (An explicit early trigger -- launch_dependents right after the wait --
+// parked the successor's CTAs on the SMs the predecessor still needed and
+// measured slower; it also cost every kernel a global flag load.)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
-__device__ __forceinline__ void pdl_wait() {
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  if (g_pdl_early) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-}
-
-// FGS_PDL: 0 off, 1 PDL launches + early trigger, 2 (default) PDL launches
-// with the implicit trigger (validated with FGS_POISON=1 over the GPU suite).
+// FGS_PDL: 0 off, otherwise (default 2) PDL launches with the implicit
+// trigger at grid end (validated with FGS_POISON=1 over the GPU suite).
 inline int pdl_mode() {
   static const int mode = [] {
     const char* e = std::getenv("FGS_PDL");

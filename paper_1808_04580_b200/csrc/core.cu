@@ -507,10 +507,6 @@ Core::Core(const double* nodes_colmajor, int64_t n_, int d_, Kind kind_, const K
   T = 2 * m;
   FGS_CUDA(cudaSetDevice(device));
   FGS_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-  {
-    const int early = pdl_mode() == 1 ? 1 : 0;
-    FGS_CUDA(cudaMemcpyToSymbol(g_pdl_early, &early, sizeof(int)));
-  }
   if (kind == DIRECT) {  // exact operator: raw nodes, no rescaling (graphop.cpp:29-34, fastsum.cpp:126-139)
     if (world != 1 || nccl_id) fail(FGS_EPARAM, "the direct backend is single-device");
     k0 = kernel_value(kernel, 0.0);

@@ -39,7 +39,10 @@ struct Blk4 {
   // QSZ = 0: default chunk (64 for 2m in {8, 16}, 32 for 2m = 12; sweep in tools/sweep_v4.py)
   // warps per footprint group: more warps per footprint = fewer registers
   // per lane (ncu: 236-255 regs capped occupancy at 8 warps/SM with G = 1)
-  static constexpr int G = T == 16 ? (INTERP ? 2 : 4) : (T == 12 ? 2 : 1);
+#ifndef FGS_G12_INTERP
+#define FGS_G12_INTERP 2
+#endif
+  static constexpr int G = T == 16 ? (INTERP ? 2 : 4) : (T == 12 ? (INTERP ? FGS_G12_INTERP : 2) : 1);
   static constexpr int TA = T / 2;           // a-tiles (2 a each)
   static constexpr int TC = T / 4;           // c-tiles (4 c each)
   static constexpr int TAW = TA / G;         // a-tiles per warp
@@ -77,7 +80,11 @@ __device__ __forceinline__ void v4_issue_chunk(double* buf, const double* taps, 
 // warps share a point; for G = 1 chosen by plan size, see Core)
 template <int T, int PS, int QSZ, bool DEFER = (Blk4<T, true, PS, QSZ>::G > 1)>
 // 2m = 12: keep 4 CTAs (16 warps) per SM resident (<= 128 registers)
-__global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT, (T == 12 && Blk4<T, true, PS, QSZ>::NT == 128) ? 4 : 1)
+#ifndef FGS_INTERP12_MINB
+#define FGS_INTERP12_MINB 4
+#endif
+__global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT,
+                                  (T == 12 && Blk4<T, true, PS, QSZ>::NT <= 192) ? FGS_INTERP12_MINB : 1)
     interp_v4_kernel(PassArgs a, int box_stride_smem) {
   pdl_wait();
   using B = Blk4<T, true, PS, QSZ>;

@@ -11,14 +11,17 @@ rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + kern,
                       "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
-agg, total, fname, src = {}, 0, "?", {}
+agg, total, fname, src, hdr, why = {}, 0, "?", {}, None, {}
 for row in csv.reader(io.StringIO(out)):
     if not row:
         continue
     if row[0] == "File Path":
         fname = row[1].rsplit("/", 1)[-1]
         continue
-    if row[0] in ("Function Name", "Line No") or len(row) < 5:
+    if row[0] == "Line No":
+        hdr = row
+        continue
+    if row[0] == "Function Name" or len(row) < 5:
         continue
     if row[0] != "-" and row[0].isdigit():  # a source line row: (line, text, address, sass, samples...)
         key = (fname, int(row[0]))
@@ -29,6 +32,16 @@ for row in csv.reader(io.StringIO(out)):
             continue
         agg[key] = agg.get(key, 0) + s
         total += s
+        if hdr:
+            reasons = why.setdefault(key, {})
+            for i, h in enumerate(hdr):
+                if h.startswith("stall_") and "Not Issued" not in h and i < len(row):
+                    try:
+                        reasons[h[6:]] = reasons.get(h[6:], 0) + int(row[i])
+                    except ValueError:
+                        pass
 print(f"total samples {total}")
 for key, s in sorted(agg.items(), key=lambda kv: -kv[1])[:top]:
-    print(f"{100.0 * s / max(total, 1):5.1f}%  {key[0]}:{key[1]:<5} {src.get(key, '')}")
+    r = sorted(why.get(key, {}).items(), key=lambda kv: -kv[1])[:3]
+    rs = " ".join(f"{k}:{v}" for k, v in r if v)
+    print(f"{100.0 * s / max(total, 1):5.1f}%  {key[0]}:{key[1]:<5} {src.get(key, '')[:70]}  [{rs}]")
