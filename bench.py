@@ -240,14 +240,32 @@ def secondary(cfg, steps, dev):
     out = {"workload": f"config{cfg}", "n": n, "d": info["d"], "N": info["N"], "m": info["m"], "nvec": nvec,
            "value": nvec / (ms / 1000.0), "unit": "matvecs/s", "ms_per_step": ms, "setup_s": setup_s}
     if cfg <= 4:
+        out["lanczos"], _ = lanczos_timing(op, info)
+    return out
+
+
+def lanczos_timing(op, info, warm=2):
+    """Lanczos time-to-k as the reference's eigs command splits it
+    (commands.cpp:174-183): `solve_s` is the first solve on a fresh handle
+    (workspace allocation and graph capture included, what a one-shot run
+    pays); `solve_s_warm` the median of `warm` further solves on the same
+    handle.  Ritz vectors are formed and copied to the host every time."""
+    import torch
+
+    import paper_1808_04580_b200 as fgs
+    times, li, pairs, phases = [], None, None, None
+    for _ in range(1 + warm):
         li = fgs.LanczosInfo()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        fgs.lanczos_largest(op, info["k"], fgs.LanczosOptions(tol=1e-8, seed=1), li)
+        pairs = fgs.lanczos_largest(op, info["k"], fgs.LanczosOptions(tol=1e-8, seed=1), li)
         torch.cuda.synchronize()
-        out["lanczos"] = {"k": info["k"], "tol": 1e-8, "solve_s": time.perf_counter() - t0,
-                          "iterations": li.iterations, "converged": li.converged, "phases": op.lanczos_stats()}
-    return out
+        times.append(time.perf_counter() - t0)
+        phases = op.lanczos_stats()
+    rec = {"k": info["k"], "tol": 1e-8, "solve_s": times[0],
+           "solve_s_warm": float(np.median(times[1:])) if warm else None,
+           "iterations": li.iterations, "converged": li.converged, "phases": phases}
+    return rec, pairs
 
 
 # ---- B200 arm --------------------------------------------------------------
@@ -427,14 +445,8 @@ def run_b200(args, rank, world, local_rank):
     # ---- Lanczos time-to-k (spectral.cpp:141-256 via the device path) -------
     lanczos = None
     if not sharded and not args.no_lanczos and args.config <= 4:
-        li = fgs.LanczosInfo()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        pairs = fgs.lanczos_largest(op, info["k"], fgs.LanczosOptions(tol=1e-8, seed=1), li)
-        torch.cuda.synchronize()
-        solve = time.perf_counter() - t0
-        lanczos = {"k": info["k"], "tol": 1e-8, "setup_s": setup_s, "solve_s": solve, "total_s": setup_s + solve,
-                   "iterations": li.iterations, "converged": li.converged, "phases": op.lanczos_stats(),
+        rec, pairs = lanczos_timing(op, info)
+        lanczos = {"setup_s": setup_s, **rec, "total_s": setup_s + rec["solve_s"],
                    "smallest_laplacian_eigs": [1.0 - v for v in pairs.values[:4].tolist()]}
 
     # ---- CPU baseline (rank 0, N=1) ----------------------------------------
