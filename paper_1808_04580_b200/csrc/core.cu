@@ -613,7 +613,7 @@ Core::~Core() {
 
 namespace {
 constexpr size_t kBounceChunk = size_t(4) << 20;
-constexpr size_t kBounceMin = size_t(16) << 20;  // below: one plain async copy
+constexpr size_t kBounceMin = size_t(16) << 20;  // below: one plain async copy (8 MB: 1.8 vs 2.8 ms)
 }  // namespace
 
 void Core::host_copy(bool to_device, void* dst, const void* src, size_t bytes) {

@@ -145,7 +145,12 @@ class Core {
   std::vector<cudaEvent_t> lz_events;              // per-step timing events
   char* bounce = nullptr;  // pinned staging for host_copy (bounce_threads x kBounceChunk)
   int bounce_threads = 0;
-  DBuf<unsigned> lz_ticket;                        // last-block reduction tickets (reset by their kernels)
+  DBuf<unsigned> lz_ticket;
+  // Ritz-vector buffers kept between solves (cudaMalloc/cudaFree per solve
+  // cost ~6 ms of a 10 ms C2 solve: every free synchronises the device)
+  DBuf<double> lz_vecs, lz_vc, lz_S, lz_pval, lz_psigned;
+  DBuf<int64_t> lz_pidx;
+  DBuf<int> lz_order;                        // last-block reduction tickets (reset by their kernels)
 
   void set_stream(cudaStream_t s);
   Workspace& workspace(int nvec);

@@ -97,6 +97,7 @@ __device__ __forceinline__ void load_rows(const double* __restrict__ z, int64_t 
 __global__ void __launch_bounds__(kRedThreads) multidot_kernel(const double* __restrict__ Q, int64_t ldq, int m,
                                                                const double* __restrict__ z, int64_t n,
                                                                double* __restrict__ partial) {
+  pdl_wait();  // PDL launches in the fused step: predecessor complete
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
   double zr[kRowsPerThread];
   load_rows(z, row0, n, zr);
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(kRedThreads) multidot_reduce_kernel(const doub
                                                                       const double* __restrict__ z, int64_t n,
                                                                       double* partial, unsigned* ticket,
                                                                       double* __restrict__ out) {
+  pdl_wait();  // PDL launches in the fused step: predecessor complete
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
   double zr[kRowsPerThread];
   load_rows(z, row0, n, zr);
@@ -150,6 +152,7 @@ __global__ void __launch_bounds__(kRedThreads) three_term_multidot_kernel(
     double* __restrict__ z, const double* __restrict__ qcur, const double* __restrict__ qprev,
     const double* __restrict__ alpha, const double* __restrict__ beta, const double* __restrict__ Q, int64_t ldq,
     int m, int64_t n, double* partial, unsigned* ticket, double* __restrict__ out) {
+  pdl_wait();  // PDL launches in the fused step: predecessor complete
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
   const double a = alpha[0], b = qprev ? beta[0] : 0.0;
   double zr[kRowsPerThread];
@@ -176,6 +179,7 @@ __global__ void __launch_bounds__(kRedThreads) three_term_multidot_kernel(
 __global__ void __launch_bounds__(kRedThreads) norm_scalars_kernel(
     const double* __restrict__ z, int64_t n, double* partial, unsigned* ticket, const double* __restrict__ alpha,
     double* __restrict__ nrm2, double* __restrict__ beta, double* __restrict__ st, int step) {
+  pdl_wait();  // PDL launches in the fused step: predecessor complete
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
   double zr[kRowsPerThread];
   load_rows(z, row0, n, zr);
@@ -204,6 +208,7 @@ __global__ void __launch_bounds__(kRedThreads) norm_scalars_kernel(
 // q_{m+1} = z / beta into the basis and the apply input
 __global__ void scale2_kernel(const double* __restrict__ z, const double* __restrict__ inv, double* __restrict__ out,
                               double* __restrict__ out2, int64_t n) {
+  pdl_wait();  // PDL launches in the fused step: predecessor complete
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (r < n) {
     const double v = z[r] * inv[0];
@@ -217,6 +222,7 @@ __global__ void scale2_kernel(const double* __restrict__ z, const double* __rest
 // (deterministic; the serial per-column loop cost ~0.5 ms at n = 2M)
 __global__ void reduce_partials_kernel(const double* __restrict__ partial, int nblocks, int m,
                                        double* __restrict__ out, int take_sqrt) {
+  pdl_wait();  // PDL launches in the fused step: predecessor complete
   const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (j >= m) return;
@@ -305,6 +311,7 @@ __global__ void unpermute_cols_kernel(const double* __restrict__ Vi, int64_t ldi
 // z[r] -= sum_j Q[r, j] * h[j]   (the GEMV of one CGS pass, spectral.cpp:195)
 __global__ void update_kernel(const double* __restrict__ Q, int64_t ldq, int m, const double* __restrict__ h,
                               double* __restrict__ z, int64_t n) {
+  pdl_wait();  // PDL launches in the fused step: predecessor complete
   extern __shared__ double hs[];
   for (int j = threadIdx.x; j < m; j += blockDim.x) hs[j] = h[j];
   __syncthreads();
@@ -470,6 +477,7 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   const double kEps = std::numeric_limits<double>::epsilon();
   cudaStream_t st = c.stream;
   const int epi = which == 0 ? EPI_NORMALIZED : EPI_LAPLACIAN;
+  const auto entry = std::chrono::steady_clock::now();
 
   // start vector: mt19937_64(seed) uniform(-1, 1) over the caller order,
   // normalised (spectral.cpp:152-156); moved to the internal order
@@ -607,28 +615,27 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     // blocks x columns (C4: 977 x 76) would serialise on it, so those
     // products keep the separate column-parallel reduction
     const bool tail = static_cast<int64_t>(nblk) * mm <= 8192;
-    multidot_reduce_kernel<<<nblk, kRedThreads, 0, st>>>(qcur, nl, 1, z.p, nl, partial.p, ticket.p,
-                                                        dalpha.p + (mm - 1));
-    three_term_multidot_kernel<<<nblk, kRedThreads, 0, st>>>(
-        z.p, qcur, mm >= 2 ? basis.p + static_cast<int64_t>(mm - 2) * nl : nullptr, dalpha.p + (mm - 1),
-        mm >= 2 ? dbeta.p + (mm - 2) : dbeta.p, basis.p, nl, mm, nl, partial.p, tail ? ticket.p : nullptr, hbuf.p);
+    const dim3 gb(nblk), tb(kRedThreads), gu(gsz), tu(256), gr(ceil_div(mm, 8));
+    const double* qprev = mm >= 2 ? basis.p + static_cast<int64_t>(mm - 2) * nl : nullptr;
+    unsigned* tk = tail ? ticket.p : nullptr;
+    launch_ex(multidot_reduce_kernel, gb, tb, 0, st, qcur, nl, 1, z.p, nl, partial.p, ticket.p, dalpha.p + (mm - 1));
+    launch_ex(three_term_multidot_kernel, gb, tb, 0, st, z.p, qcur, qprev, dalpha.p + (mm - 1),
+              mm >= 2 ? dbeta.p + (mm - 2) : dbeta.p, basis.p, nl, mm, nl, partial.p, tk, hbuf.p);
     if (!tail) {
-      reduce_partials_kernel<<<ceil_div(mm, 8), 256, 0, st>>>(partial.p, nblk, mm, hbuf.p, 0);
+      launch_ex(reduce_partials_kernel, gr, tu, 0, st, partial.p, nblk, mm, hbuf.p, 0);
       ++c.launches;
     }
-    update_kernel<<<gsz, 256, sizeof(double) * mm, st>>>(basis.p, nl, mm, hbuf.p, z.p, nl);
-    multidot_reduce_kernel<<<nblk, kRedThreads, 0, st>>>(basis.p, nl, mm, z.p, nl, partial.p,
-                                                        tail ? ticket.p : nullptr, hbuf.p);
+    launch_ex(update_kernel, gu, tu, sizeof(double) * mm, st, basis.p, nl, mm, hbuf.p, z.p, nl);
+    launch_ex(multidot_reduce_kernel, gb, tb, 0, st, basis.p, nl, mm, z.p, nl, partial.p, tk, hbuf.p);
     if (!tail) {
-      reduce_partials_kernel<<<ceil_div(mm, 8), 256, 0, st>>>(partial.p, nblk, mm, hbuf.p, 0);
+      launch_ex(reduce_partials_kernel, gr, tu, 0, st, partial.p, nblk, mm, hbuf.p, 0);
       ++c.launches;
     }
-    update_kernel<<<gsz, 256, sizeof(double) * mm, st>>>(basis.p, nl, mm, hbuf.p, z.p, nl);
-    norm_scalars_kernel<<<nblk, kRedThreads, 0, st>>>(z.p, nl, partial.p, ticket.p, dalpha.p, dnrm.p, dbeta.p, dst.p,
-                                                     mm);
+    launch_ex(update_kernel, gu, tu, sizeof(double) * mm, st, basis.p, nl, mm, hbuf.p, z.p, nl);
+    launch_ex(norm_scalars_kernel, gb, tb, 0, st, z.p, nl, partial.p, ticket.p, dalpha.p, dnrm.p, dbeta.p, dst.p, mm);
     c.launches += 6;
     if (mm < cap) {
-      scale2_kernel<<<gsz, 256, 0, st>>>(z.p, dst.p + 1, basis.p + static_cast<int64_t>(mm) * nl, qin.p, nl);
+      launch_ex(scale2_kernel, gu, tu, 0, st, z.p, dst.p + 1, basis.p + static_cast<int64_t>(mm) * nl, qin.p, nl);
       ++c.launches;
       qin_holds = mm + 1;
     } else {
@@ -803,8 +810,9 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
       S[static_cast<size_t>(j) * wanted + i] = tvecs[static_cast<size_t>(m - 1 - i) * m + j];
   }
   if (want_vectors) {
-    DBuf<double> dS;
+    DBuf<double>& dS = c.lz_S;
     dS.upload(S.data(), S.size(), st);
+    res.vectors_dev = std::move(c.lz_vecs);  // handed back by lanczos_finish_vectors
     res.vectors_dev.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)) * wanted);
     for (int c0 = 0; c0 < wanted; c0 += 8) {
       ritz_kernel<8><<<ceil_div(std::max<int64_t>(nl, 1), 128), 128, 0, st>>>(basis.p, nl, m, dS.p, wanted, c0,
@@ -814,6 +822,12 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   }
   FGS_CUDA(cudaStreamSynchronize(st));
   FGS_CUDA(cudaGetLastError());
+  if (trace) {
+    const auto end = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[lanczos] prologue %.2f ms  loop %.2f ms  ritz %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(wall0 - entry).count(), res.loop_ms,
+                 std::chrono::duration<double, std::milli>(end - wall0).count() - res.loop_ms);
+  }
   return res;
 }
 
@@ -822,24 +836,30 @@ void lanczos_finish_vectors(Core& c, LanczosResult& r, const std::vector<int>& o
   const int cnt = static_cast<int>(order.size());
   if (cnt == 0) return;
   cudaStream_t st = c.stream;
-  DBuf<int> dorder;
+  DBuf<int>& dorder = c.lz_order;
   dorder.upload(order.data(), order.size(), st);
-  DBuf<double> Vc;
+  DBuf<double>& Vc = c.lz_vc;
   Vc.alloc(static_cast<size_t>(n) * cnt);
   const int gx = std::max(1, std::min(ceil_div(n, 256), 4096));
   unpermute_cols_kernel<<<dim3(gx, cnt), 256, 0, st>>>(r.vectors_dev.p, n, Vc.p, n, c.perm.p, dorder.p, n);
   const int chunk = 1 << 16;
   const int parts = std::max(1, ceil_div(n, chunk));
-  DBuf<double> pval, psigned;
-  DBuf<int64_t> pidx;
+  DBuf<double>& pval = c.lz_pval;
+  DBuf<double>& psigned = c.lz_psigned;
+  DBuf<int64_t>& pidx = c.lz_pidx;
   pval.alloc(static_cast<size_t>(parts) * cnt);
   psigned.alloc(static_cast<size_t>(parts) * cnt);
   pidx.alloc(static_cast<size_t>(parts) * cnt);
   colmax_partial_kernel<<<dim3(parts, cnt), 256, 0, st>>>(Vc.p, n, n, chunk, pval.p, pidx.p, psigned.p);
   colsign_kernel<<<dim3(gx, cnt), 256, 0, st>>>(Vc.p, n, n, pval.p, psigned.p, parts);
   c.launches += 3;
+  const auto t0 = std::chrono::steady_clock::now();
   c.host_copy(false, host_out, Vc.p, sizeof(double) * n * cnt);
   FGS_CUDA(cudaGetLastError());
+  if (std::getenv("FGS_LANCZOS_TRACE"))
+    std::fprintf(stderr, "[lanczos] vectors copy-out %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  c.lz_vecs = std::move(r.vectors_dev);  // keep the device Ritz block for the next solve
 }
 
 }  // namespace fgsb
