@@ -984,12 +984,25 @@ void Core::build_plan(const double* nodes_colmajor) {
                      static_cast<long long>(grid_elems), static_cast<long long>(cnt.back()), mean_list, maxlen,
                      static_cast<long long>(entries[0]), static_cast<long long>(entries[1]),
                      static_cast<long long>(entries[2]));
-      if (split_on && mean_list < 4.0 && n_local >= 100000) {
+      // default: one mixed launch with lanes by class (FGS_ASM_MIXED=0: the
+      // previous policy -- per-class launches for large sparse plans, else
+      // lanes by the mean list length)
+      static const bool mixed_on = [] {
+        const char* e = std::getenv("FGS_ASM_MIXED");
+        return !(e && std::string(e) == "0");
+      }();
+      for (int c = 0; c < 3; ++c) asm_class_n[c] = static_cast<int64_t>(cls[c].size());
+      asm_mixed = false;
+      if (mixed_on) {
+        std::vector<int> all;
+        all.reserve(static_cast<size_t>(grid_elems));
+        for (int c = 0; c < 3; ++c) all.insert(all.end(), cls[c].begin(), cls[c].end());
+        asm_mixed_cells.upload(all.data(), all.size(), stream);
+        asm_mixed = true;
+      } else if (split_on && mean_list < 4.0 && n_local >= 100000) {
         asm_split = true;
-        for (int c = 0; c < 3; ++c) {
-          asm_class_n[c] = static_cast<int64_t>(cls[c].size());
+        for (int c = 0; c < 3; ++c)
           if (!cls[c].empty()) asm_cells[c].upload(cls[c].data(), cls[c].size(), stream);
-        }
       }
     }
   }
@@ -1164,6 +1177,22 @@ void Core::launch_interp(const PassArgs& a) {
 
 void Core::launch_assemble(Workspace& w, int nvec) {
   const int64_t pstride = static_cast<int64_t>(std::max(nitems, 1)) * box_stride;
+  if (asm_mixed) {
+    AssembleMixedArgs m{};
+    m.a = AssembleArgs{asm_ptr.p, asm_idx.p, w.priv.p, pstride, w.grid.p, grid_elems, grid_elems, nvec, nullptr};
+    m.cells = asm_mixed_cells.p;
+    m.n0 = asm_class_n[0];
+    m.n1 = asm_class_n[1];
+    m.n2 = asm_class_n[2];
+    m.w0 = (m.n0 + 31) / 32;
+    m.w1 = (m.n1 + 3) / 4;
+    const int64_t warps = m.w0 + m.w1 + m.n2;
+    launch_ex(assemble_mixed_kernel, dim3(static_cast<unsigned>(std::max<int64_t>(1, ceil_div(warps * 32, 256)))), 256,
+              0, stream, m);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+    return;
+  }
   if (!asm_split) {  // lanes per cell from the mean list length, one launch
     AssembleArgs aa{asm_ptr.p, asm_idx.p, w.priv.p, pstride, w.grid.p, grid_elems, grid_elems, nvec, nullptr};
     const double mean_list = static_cast<double>(asm_idx.n) / static_cast<double>(std::max<int64_t>(grid_elems, 1));

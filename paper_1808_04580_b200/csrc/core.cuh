@@ -122,6 +122,8 @@ class Core {
   DBuf<int> asm_cells[3];      // cells by list-length class (<= 8, 9..64, > 64 entries)
   int64_t asm_class_n[3] = {0, 0, 0};
   bool asm_split = false;
+  DBuf<int> asm_mixed_cells;  // classes 0 | 1 | 2 concatenated (single-launch mixed assembly)
+  bool asm_mixed = false;
   DBuf<cufftDoubleComplex> mult;  // compact Hermitian multiplier (FASTSUM)
   DBuf<double> deconv_d;
   DBuf<double2> tw2;  // d = 2 pruned-convolution twiddles

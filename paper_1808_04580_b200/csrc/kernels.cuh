@@ -285,6 +285,66 @@ __global__ void assemble_kernel(AssembleArgs a) {
   }
 }
 
+// One launch for all list-length classes (cells sorted by class at plan
+// time; classes are warp-aligned): warps [0, w0) take 32 short lists (one
+// lane each), [w0, w0 + w1) four medium lists (8 lanes each), the rest one
+// long list each (32 lanes).  Per cell the arithmetic is assemble_kernel<L>'s
+// for its class.  C2's lists average 17 entries but 88 % of the entries sit
+// in lists of 65-291, which 8 lanes per cell walked as ~20 serial L2 round
+// trips: the straggler set the kernel's length.
+struct AssembleMixedArgs {
+  AssembleArgs a;    // ptr, idx, priv, grid, nvec (cells / cell_ids unused)
+  const int* cells;  // class 0 cells | class 1 cells | class 2 cells
+  int64_t n0, n1, n2, w0, w1;
+};
+
+template <int L>
+__device__ __forceinline__ void assemble_cell(const AssembleArgs& a, int64_t g, bool valid, int sub) {
+  int b = 0, e = 0;
+  if (valid) {
+    const int b0 = a.ptr[g], e0 = a.ptr[g + 1];
+    const int per = (e0 - b0 + L - 1) / L;
+    b = min(e0, b0 + sub * per);
+    e = min(e0, b + per);
+  }
+  for (int v = 0; v < a.nvec; ++v) {
+    const double* pv = a.priv + v * a.priv_stride;
+    double acc = 0.0;
+    int l = b;
+    for (; l + 4 <= e; l += 4) {
+      const int i0 = __ldg(a.idx + l), i1 = __ldg(a.idx + l + 1), i2 = __ldg(a.idx + l + 2), i3 = __ldg(a.idx + l + 3);
+      const double v0 = pv[i0], v1 = pv[i1], v2 = pv[i2], v3 = pv[i3];
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
+    }
+    for (; l < e; ++l) acc += pv[__ldg(a.idx + l)];
+#pragma unroll
+    for (int off = 1; off < L; off <<= 1) acc += __shfl_down_sync(0xffffffffu, acc, off, L);
+    if (valid && sub == 0) a.grid[v * a.grid_stride + g] = acc;
+  }
+}
+
+__global__ void assemble_mixed_kernel(AssembleMixedArgs m) {
+  pdl_wait();
+  const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw < m.w0) {
+    const int64_t ci = gw * 32 + lane;
+    const bool valid = ci < m.n0;
+    assemble_cell<1>(m.a, valid ? m.cells[ci] : 0, valid, 0);
+  } else if (gw < m.w0 + m.w1) {
+    const int64_t ci = (gw - m.w0) * 4 + (lane >> 3);
+    const bool valid = ci < m.n1;
+    assemble_cell<8>(m.a, valid ? m.cells[m.n0 + ci] : 0, valid, lane & 7);
+  } else {
+    const int64_t ci = gw - m.w0 - m.w1;
+    const bool valid = ci < m.n2;
+    assemble_cell<32>(m.a, valid ? m.cells[m.n0 + m.n1 + ci] : 0, valid, lane);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Spectral multiply on the R2C half spectrum by the Hermitian-symmetrised
 // multiplier  m~_k = (m_k + conj(m_-k)) / 2,  m_k = out_factor * bhat_l *
