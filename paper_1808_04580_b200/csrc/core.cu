@@ -996,7 +996,7 @@ void Core::build_plan(const double* nodes_colmajor) {
       if (mixed_on) {
         std::vector<int> all;
         all.reserve(static_cast<size_t>(grid_elems));
-        for (int c = 0; c < 3; ++c) all.insert(all.end(), cls[c].begin(), cls[c].end());
+        for (int c = 2; c >= 0; --c) all.insert(all.end(), cls[c].begin(), cls[c].end());  // heaviest first
         asm_mixed_cells.upload(all.data(), all.size(), stream);
         asm_mixed = true;
       } else if (split_on && mean_list < 4.0 && n_local >= 100000) {
@@ -1184,9 +1184,9 @@ void Core::launch_assemble(Workspace& w, int nvec) {
     m.n0 = asm_class_n[0];
     m.n1 = asm_class_n[1];
     m.n2 = asm_class_n[2];
-    m.w0 = (m.n0 + 31) / 32;
+    m.w2 = m.n2;
     m.w1 = (m.n1 + 3) / 4;
-    const int64_t warps = m.w0 + m.w1 + m.n2;
+    const int64_t warps = m.w2 + m.w1 + (m.n0 + 31) / 32;
     launch_ex(assemble_mixed_kernel, dim3(static_cast<unsigned>(std::max<int64_t>(1, ceil_div(warps * 32, 256)))), 256,
               0, stream, m);
     ++launches;

@@ -286,16 +286,17 @@ __global__ void assemble_kernel(AssembleArgs a) {
 }
 
 // One launch for all list-length classes (cells sorted by class at plan
-// time; classes are warp-aligned): warps [0, w0) take 32 short lists (one
-// lane each), [w0, w0 + w1) four medium lists (8 lanes each), the rest one
-// long list each (32 lanes).  Per cell the arithmetic is assemble_kernel<L>'s
-// for its class.  C2's lists average 17 entries but 88 % of the entries sit
-// in lists of 65-291, which 8 lanes per cell walked as ~20 serial L2 round
-// trips: the straggler set the kernel's length.
+// time; classes are warp-aligned, heaviest first so the long lists start in
+// the first wave): warps [0, w2) take one long list each (> 64 entries, 32
+// lanes), [w2, w2 + w1) four medium lists (9-64, 8 lanes each), the rest 32
+// short lists (one lane each).  Per cell the arithmetic is
+// assemble_kernel<L>'s for its class.  C2's lists average 17 entries but
+// 88 % of the entries sit in lists of 65-291, which 8 lanes per cell walked
+// as ~20 serial L2 round trips: the straggler set the kernel's length.
 struct AssembleMixedArgs {
   AssembleArgs a;    // ptr, idx, priv, grid, nvec (cells / cell_ids unused)
-  const int* cells;  // class 0 cells | class 1 cells | class 2 cells
-  int64_t n0, n1, n2, w0, w1;
+  const int* cells;  // class 2 cells | class 1 cells | class 0 cells
+  int64_t n0, n1, n2, w1, w2;
 };
 
 template <int L>
@@ -330,18 +331,18 @@ __global__ void assemble_mixed_kernel(AssembleMixedArgs m) {
   pdl_wait();
   const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (gw < m.w0) {
-    const int64_t ci = gw * 32 + lane;
-    const bool valid = ci < m.n0;
-    assemble_cell<1>(m.a, valid ? m.cells[ci] : 0, valid, 0);
-  } else if (gw < m.w0 + m.w1) {
-    const int64_t ci = (gw - m.w0) * 4 + (lane >> 3);
-    const bool valid = ci < m.n1;
-    assemble_cell<8>(m.a, valid ? m.cells[m.n0 + ci] : 0, valid, lane & 7);
-  } else {
-    const int64_t ci = gw - m.w0 - m.w1;
+  if (gw < m.w2) {
+    const int64_t ci = gw;
     const bool valid = ci < m.n2;
-    assemble_cell<32>(m.a, valid ? m.cells[m.n0 + m.n1 + ci] : 0, valid, lane);
+    assemble_cell<32>(m.a, valid ? m.cells[ci] : 0, valid, lane);
+  } else if (gw < m.w2 + m.w1) {
+    const int64_t ci = (gw - m.w2) * 4 + (lane >> 3);
+    const bool valid = ci < m.n1;
+    assemble_cell<8>(m.a, valid ? m.cells[m.n2 + ci] : 0, valid, lane & 7);
+  } else {
+    const int64_t ci = (gw - m.w2 - m.w1) * 32 + lane;
+    const bool valid = ci < m.n0;
+    assemble_cell<1>(m.a, valid ? m.cells[m.n2 + m.n1 + ci] : 0, valid, 0);
   }
 }
 
