@@ -24,6 +24,8 @@
 // chunk.  Results are bitwise deterministic (fixed MMA and reduction order).
 #pragma once
 
+#include <type_traits>
+
 #include "kernels_v2.cuh"
 
 namespace fgsb {
@@ -62,6 +64,9 @@ struct Blk4 {
 };
 
 // cp.async a chunk of q points' taps into rows of STRIDE doubles
+template <class I>
+__device__ __forceinline__ I pmin(I x, I y) { return x < y ? x : y; }
+
 template <int TAPS, int STRIDE>
 __device__ __forceinline__ void v4_issue_chunk(double* buf, const double* taps, int64_t p, int q, int tid, int nt) {
   constexpr int H = TAPS / 2;  // 16-byte pieces per point
@@ -110,7 +115,11 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT,
   const int bx1 = it.e1, bx2 = it.e2;
   const int V = it.e0 * it.e1 * it.e2;
   const int M = a.M;
-  const int64_t p_begin = it.p_begin, p_end = it.p_end;
+  // point indices: 32-bit for 2m = 16 (C5 interp 73.6 -> 71.9 ms per block;
+  // for 2m = 8 / 12 the 64-bit form schedules better: C3 73 vs 84 us, C4
+  // 427 vs 438 us)
+  using PI = std::conditional_t<T == 16, int, int64_t>;
+  const PI p_begin = it.p_begin, p_end = it.p_end;
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
 
   for (int vec = 0; vec < a.nvec; ++vec) {
@@ -130,14 +139,14 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT,
 
     // y of chunk kk's points: the G partials in warp order, then the epilogue
     auto finish_chunk = [&](int kk) {
-      const int64_t f0 = p_begin + static_cast<int64_t>(kk) * QS;
-      const int cnt = static_cast<int>(lmin(QS, p_end - f0));
+      const PI f0 = p_begin + static_cast<PI>(kk) * QS;
+      const int cnt = static_cast<int>(pmin<PI>(QS, p_end - f0));
       const int fb = kk & 1;
       for (int pt = tid; pt < cnt; pt += NT) {
         double val = red[(fb * QS + pt) * G];
 #pragma unroll
         for (int w2 = 1; w2 < G; ++w2) val += red[(fb * QS + pt) * G + w2];
-        const int64_t ipt = f0 + pt;
+        const PI ipt = f0 + pt;
         if (a.epilogue == EPI_DEGREE) {
           const double dg = val - a.k0;  // graphop.cpp:55-56
           a.degrees[ipt] = dg;
@@ -158,8 +167,8 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT,
     };
 
     for (int k = 0; k < nch; ++k) {
-      const int64_t c0 = p_begin + static_cast<int64_t>(k) * QS;
-      const int64_t c1 = lmin(c0 + QS, p_end);
+      const PI c0 = p_begin + static_cast<PI>(k) * QS;
+      const PI c1 = pmin<PI>(c0 + QS, p_end);
       const int buf = k & 1;
       cp_async_wait_0();
       __syncthreads();
@@ -169,15 +178,15 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT,
         cp_async_commit();
       }
       const double* sb = stg + buf * QS * SR;
-      for (int64_t b0 = c0 + 8 * grp; b0 < c1; b0 += 8 * P) {
-        const int64_t ipt = b0 + r8;  // this lane's point (C rows / A rows)
+      for (PI b0 = c0 + 8 * grp; b0 < c1; b0 += 8 * P) {
+        const PI ipt = b0 + r8;  // this lane's point (C rows / A rows)
         const bool in_chunk = ipt < c1;
         const double* w = sb + (in_chunk ? (ipt - c0) : 0) * SR;
         // epilogue operands prefetch (lanes q == 0 of warp 0 of the group)
         double xin = 0.0, sin_ = 1.0;
-        int64_t ix = 0;
+        PI ix = 0;
         if (wg == 0 && q == 0 && in_chunk) {
-          ix = a.perm ? static_cast<int64_t>(a.perm[ipt]) : ipt;
+          ix = a.perm ? static_cast<PI>(a.perm[ipt]) : ipt;
           if (xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE) xin = xv[ix];
           if (a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN) sin_ = a.s[ipt];
         }
@@ -192,7 +201,7 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT,
         }
         double yacc = 0.0;
         while (true) {
-          while (static_cast<int64_t>(run.pstart) + run.pcount <= b0 && r + 1 < it.run_end) run = a.runs[++r];
+          while (static_cast<PI>(run.pstart) + run.pcount <= b0 && r + 1 < it.run_end) run = a.runs[++r];
           if (loaded != r) {
             const int o0 = run.off & 1023, o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
 #pragma unroll
@@ -205,7 +214,7 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT,
             }
             loaded = r;
           }
-          const int64_t rs = run.pstart, re_ = static_cast<int64_t>(run.pstart) + run.pcount;
+          const PI rs = run.pstart, re_ = static_cast<PI>(run.pstart) + run.pcount;
           const bool mine = in_chunk && ipt >= rs && ipt < re_;
           double aF[KS];  // A fragments: we_{point}[4 ks + q], zero outside this run
 #pragma unroll
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT,
           }
 #pragma unroll
           for (int t = 0; t < TAW; ++t) yacc = fma(wa[t], K[t], yacc);
-          if (re_ < lmin(b0 + 8, c1) && r + 1 < it.run_end) {  // batch continues in the next run
+          if (re_ < pmin<PI>(b0 + 8, c1) && r + 1 < it.run_end) {  // batch continues in the next run
             run = a.runs[++r];
             continue;
           }
