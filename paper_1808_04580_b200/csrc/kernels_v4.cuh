@@ -54,7 +54,9 @@ struct Blk4 {
   // groups (point streams) per CTA; PS > 0 overrides the default
   static constexpr int P = PS > 0 ? PS : (T == 8 ? 4 : (T == 12 ? 2 : (INTERP ? 2 : 1)));
   static constexpr int NT = 32 * G * P;
-  static constexpr int QS = QSZ > 0 ? QSZ : (T == 12 ? 32 : 64);  // points per staged chunk
+  // points per staged chunk (2m = 12: spread 64 -- C4 spread 412 -> 391 us
+  // with the private group boxes -- interp 32)
+  static constexpr int QS = QSZ > 0 ? QSZ : ((T == 12 && INTERP) ? 32 : 64);
   static constexpr int TAPS = 3 * T;
   // staged row stride: = 4 or 12 (mod 16 doubles) so the 4 (spread) or 8
   // (interp) points a warp reads per LDS fall on distinct bank pairs; 2m = 16
