@@ -52,7 +52,8 @@ struct Blk4 {
   static constexpr int KS = T / 4;           // interp K-steps over e
   static constexpr int NE = (T + 7) / 8;     // spread N-tiles over e (2m = 12 pads 12 -> 16)
   // groups (point streams) per CTA; PS > 0 overrides the default
-  static constexpr int P = PS > 0 ? PS : (T == 8 ? 4 : (T == 12 ? 2 : (INTERP ? 2 : 1)));
+  // (2m = 16 spread: 2 streams, C5 64.9 -> 62.2 ms per 16-vector block)
+  static constexpr int P = PS > 0 ? PS : (T == 8 ? 4 : 2);
   static constexpr int NT = 32 * G * P;
   // points per staged chunk (2m = 12: spread 64 -- C4 spread 412 -> 391 us
   // with the private group boxes -- interp 32)
