@@ -3,22 +3,34 @@
 
 Metric (BASELINE.json): fp64 Laplacian matvecs/s (+ Lanczos time-to-k and the
 roofline fraction of the dominant kernel).  One step = one application of
-L_s = I - D^-1/2 W D^-1/2 to a block of `nvec` seeded N(0,1) vectors (1 for
-configs 1-4, 16 for config 5) on the BASELINE configuration's synthetic point
-set.  Default workload: configs[1] (config 2, 100k points in 2-D).
+L_s = I - D^-1/2 W D^-1/2 to a block of `nvec` seeded N(0,1) vectors on the
+BASELINE configuration's synthetic point set.  Default workload: config 5
+(`configs[4]`, the largest single-GPU configuration: a block of 16 vectors at
+n = 10M points in 3-D, N = 64, m = 8); configs 2 and 4 are reported under
+"also" with their Lanczos time-to-k.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--weak]
+                  [--impl b200|reference]
 
-Multi-GPU: launched by torchrun, one process per GPU; points are sharded by
-the internal spatial order and the truncated spectrum is summed with NCCL
-(strong scaling, whole-job matvecs/s, max over ranks of device time).
+Multi-GPU: one process per GPU.  `--gpus N` without a torchrun environment
+re-launches itself under `torch.distributed.run` with N ranks.  Points are
+sharded by the internal spatial order, each rank spreads its slice, and one
+NCCL allreduce per apply sums the truncated spectra (strong scaling at fixed n;
+`--weak`: config 5 at 1.25M points per GPU).  Whole-job matvecs/s = the
+vectors all ranks applied / the max over ranks of the device time.
+
+`--impl reference`: the reference's own CPU implementation of the path
+(/root/reference/proj compiled unchanged against shim headers, oracle/_ref;
+else the oracle restatement), serial as the reference is, on rank 0 only.
+The reference arm never loads the product library: its inputs come from the
+same seeded generator linked into oracle/liboracle.so.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,25 +43,64 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SEED = 2024
+VEC_SEED = 99
 STAGES = ("spread", "assemble", "fft_r2c", "multiply", "fft_c2r", "interp")
+WEAK_PER_GPU = 1_250_000
+METRIC = "fp64 Laplacian matvecs/sec"
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--config", type=int, default=5)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--weak", action="store_true", help="config 5 at 1.25M points per GPU (weak scaling)")
     p.add_argument("--nvec", type=int, default=0, help="vectors per step (0: 16 for config 5, else 1)")
     p.add_argument("--no-lanczos", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=8.0)
+    p.add_argument("--also", default="2,4", help="comma list of extra configs measured after the main line "
+                   "(device matvecs/s + Lanczos time-to-k), '' to skip")
     p.add_argument("--force-sharded", action="store_true",
                    help=argparse.SUPPRESS)  # run the sharded (NCCL) path even at world size 1 (under torchrun)
-    p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=12.0)
-    p.add_argument("--also", default="4", help="comma list of extra configs measured after the main line "
-                   "(device matvecs/s + Lanczos time-to-k), '' to skip; N=1 only")
     return p.parse_args()
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`--gpus N` outside torchrun: re-run this script with N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def workload(args, world):
+    """(config dict shared by both arms, n, nvec, info) -- from the oracle
+    library's copy of the generator (no product import)."""
+    from oracle import oracle as orc
+    info = orc.workload_info(args.config)
+    n = info["n"]
+    if args.weak:
+        if args.config != 5:
+            raise SystemExit("--weak is defined for config 5 (1.25M points per GPU)")
+        n = WEAK_PER_GPU * world
+    nvec = args.nvec or (16 if args.config == 5 else 1)
+    cfg = {"workload": f"config{args.config}", "n": n, "d": info["d"], "sigma": info["sigma"], "N": info["N"],
+           "m": info["m"], "p": info["p"], "nvec": nvec, "op": "L_s x"}
+    return cfg, n, nvec, info
+
+
+def nodes_for(args, n):
+    from oracle import oracle as orc
+    return orc.workload_nodes(args.config, SEED, n=n if args.weak else 0)
 
 
 def measured_peaks():
@@ -58,6 +109,17 @@ def measured_peaks():
             return json.load(f), "measured"
     except OSError:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ---- clocks sampling (B200_PROFILING.md clocks line) ---------------------
@@ -70,15 +132,13 @@ class ClockSampler:
         self.device = device
         self.samples = []
         self._proc = None
-        self._t = None
 
     def start(self):
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self._proc = None
 
@@ -109,147 +169,146 @@ class ClockSampler:
 
 
 # ---- algorithmic work of one spread / interpolation launch ----------------
-def stage_work(geom, n, nvec, scaled_input=True):
-    """bytes and flops the kernels must move / execute per launch.
+def stage_work(geom, n, nvec):
+    """Algorithmic bytes and flops per launch.
 
-    spread: taps n*d*T*8 (read once per block of vectors), x (+ s) per vector,
-            item boxes written per vector; flops 2*n*T^d per vector.
-    interp: taps, item boxes read, x, s, y per vector; flops 2*n*T^d per vector.
+    flops: 2 n (2m)^d per vector and pass (window evaluation precomputed).
+    bytes: the per-point inputs the pass must read -- coordinates-equivalent
+    taps are not counted (§8d counts coordinates, 8 d bytes per point), x and
+    s per vector (spread), x, s and y (interp) -- plus one grid write (spread)
+    or read (interp) of M^d doubles per vector.
     """
-    d, T = geom["d"], geom["taps"]
-    taps = n * d * T * 8
-    vec = n * 8
-    box = geom["items"] * geom["box_stride"] * 8
+    d, T, M = geom["d"], geom["taps"], geom["M"]
     flops = 2.0 * n * T ** d * nvec
-    spread_b = taps + nvec * (vec * (2 if scaled_input else 1) + box)
-    interp_b = taps + nvec * (box + 3 * vec)
+    coords = 8.0 * n * d
+    grid = 8.0 * M ** d
+    spread_b = coords + nvec * (16.0 * n + grid)
+    interp_b = coords + nvec * (24.0 * n + grid)
     return {"spread": (spread_b, flops), "interp": (interp_b, flops)}
 
 
-# ---- CPU side: the oracle restatement (the reference is not buildable) ----
-def cpu_matvecs_per_s(config, X, info, nvec, budget_s):
-    """Serial oracle (kind "port") on the same nodes; bounded sample.  Returns
-    (matvecs/s, sample description, setup seconds)."""
+# ---- the reference's CPU path (oracle/_ref if built, else the restatement) --
+def cpu_backend():
+    """(module, kind): oracle/_ref = the reference's own nfft/kernels/fastsum/
+    graphop/spectral .cpp compiled unchanged against shim Eigen/FFTW headers
+    (kind "reference"); without it the oracle restatement (kind "port")."""
+    try:
+        from oracle import ref as R
+        if R.available():
+            return R, "reference"
+    except Exception:  # noqa: BLE001 - fall back to the restatement
+        pass
     from oracle import oracle as orc
-    n = X.shape[0]
-    sub = X
-    scale = 1.0
-    if n > 500_000:  # bounded sample: a point subsample, extrapolated linearly in n
-        idx = np.random.default_rng(config).choice(n, 500_000 if info["d"] < 3 or info["m"] < 8 else 200_000,
-                                                   replace=False)
-        sub = X[np.sort(idx)]
-        scale = sub.shape[0] / n
+    return orc, "port"
+
+
+class Pinned:
+    """Run the serial CPU path pinned to one core."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = min(self.old)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.old)
+
+
+def cpu_apply_seconds(X, info, budget_s):
+    """Mean seconds of one L_s apply (one warm-up, then >= 2 timed applies,
+    acceptance.cpp:400-404) and the setup seconds, on the serial CPU path."""
+    R, _ = cpu_backend()
     t0 = time.perf_counter()
-    ref = orc.AdjacencyOperator(sub, 0, info["sigma"], N=info["N"], m=info["m"], p=info["p"])
+    op = R.AdjacencyOperator(X, 0, info["sigma"], N=info["N"], m=info["m"], p=info["p"])
     setup = time.perf_counter() - t0
-    x = np.random.default_rng(1).standard_normal(sub.shape[0])
-    ref.apply_sym_laplacian(x)  # warm-up (acceptance.cpp:400-404)
+    x = np.random.default_rng(1).standard_normal(X.shape[0])
+    op.apply_sym_laplacian(x)
     reps, t0 = 0, time.perf_counter()
     while True:
-        ref.apply_sym_laplacian(x)
+        op.apply_sym_laplacian(x)
         reps += 1
         el = time.perf_counter() - t0
-        if (el >= budget_s and reps >= 2) or reps >= 500:
+        if (el >= budget_s and reps >= 2) or reps >= 200:
             break
-    per = el / reps
-    rate = scale / per
-    desc = (f"serial oracle port, {reps} matvecs of L_s on {sub.shape[0]} points"
-            + (f" (random subsample of {n}, throughput scaled by n_sample/n)" if scale < 1 else "")
-            + f", 1 thread, config {config}")
-    return rate, desc, setup
+    return el / reps, setup, reps
 
 
-def cpu_model():
-    try:
-        with open("/proc/cpuinfo") as f:
-            for line in f:
-                if line.startswith("model name"):
-                    return line.split(":", 1)[1].strip()
-    except OSError:
-        pass
-    return "unknown"
+def cpu_matvec_rate(config, X, info, budget_s):
+    """matvecs/s of the serial CPU path on this workload.  Up to 400k points
+    the full set is timed; beyond, two prefixes of the seeded point stream
+    (n1, 2 n1 points: the same distribution) give t(n) = a + b n and the full
+    size is extrapolated (a = the n-independent FFT/multiply part)."""
+    _, kind = cpu_backend()
+    n = X.shape[0]
+    with Pinned() as pin:
+        if n <= 400_000:
+            t, setup, reps = cpu_apply_seconds(X, info, budget_s)
+            desc = f"{reps} timed applies of L_s on all {n} points"
+        else:
+            n1 = 50_000 if (info["d"] == 3 and info["m"] >= 8) else 100_000
+            t1, _, r1 = cpu_apply_seconds(X[:n1], info, budget_s / 2)
+            t2, setup, r2 = cpu_apply_seconds(X[:2 * n1], info, budget_s / 2)
+            b = (t2 - t1) / n1
+            a = max(0.0, t1 - b * n1)
+            t = a + b * n
+            desc = (f"L_s applies timed on the first {n1} and {2 * n1} points of the same seeded stream "
+                    f"({r1} / {r2} timed applies: {t1:.3f} s / {t2:.3f} s), t(n) = a + b n fitted and evaluated "
+                    f"at n = {n} (a = {a:.4f} s, b = {b * 1e6:.3f} us/point)")
+        core = pin.core
+    return 1.0 / t, t, setup, f"{desc}; serial, pinned to core {core}", kind
+
+
+def cpu_lanczos(config, budget_ok=True):
+    """Lanczos time-to-k of the serial CPU path (commands.cpp:174-183 split:
+    setup = plan + degrees, solve = lanczos_largest with Ritz vectors)."""
+    from oracle import oracle as orc
+    R, kind = cpu_backend()
+    info = orc.workload_info(config)
+    X = orc.workload_nodes(config, SEED)
+    with Pinned() as pin:
+        t0 = time.perf_counter()
+        op = R.AdjacencyOperator(X, 0, info["sigma"], N=info["N"], m=info["m"], p=info["p"])
+        setup = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        vals, _, iters, conv = op.lanczos_largest(info["k"], max_iter=1000, tol=1e-8, seed=1)
+        solve = time.perf_counter() - t0
+    return {"workload": f"config{config}", "n": X.shape[0], "k": info["k"], "tol": 1e-8, "setup_s": setup,
+            "solve_s": solve, "total_s": setup + solve, "iterations": iters, "converged": bool(conv),
+            "kind": kind, "cores": 1, "core": pin.core, "top_eig_A": [float(v) for v in vals[:3]]}
 
 
 # ---- reference arm ---------------------------------------------------------
 def run_reference(args, rank, world):
-    import paper_1808_04580_b200 as fgs
     if rank != 0:
         return
-    info = fgs.workload_info(args.config)
-    nvec = args.nvec or (16 if args.config == 5 else 1)
-    X = fgs.workload_nodes(args.config, SEED)
-    from oracle import oracle as orc
-    n = X.shape[0]
-    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
-    rate, desc, setup = cpu_matvecs_per_s(args.config, X, info, nvec, budget)
-    value = rate * 1.0
+    cfg, n, nvec, info = workload(args, world)
+    X = nodes_for(args, n)
+    # each timed "step" is the bounded CPU sample; its budget keeps the whole
+    # --steps/--warmup run within a few minutes
+    budget = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    rate, t, setup, desc, kind = cpu_matvec_rate(args.config, X, info, budget)
+    value = rate
     line = {
-        "impl": "reference", "metric": "fp64 Laplacian matvecs/sec", "value": value, "unit": "matvecs/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * nvec / value, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded stand-in for the paper's datasets)",
-        "config": {"workload": f"config{args.config}", "n": n, "d": info["d"], "sigma": info["sigma"],
-                   "N": info["N"], "m": info["m"], "p": info["p"], "nvec": nvec},
-        "cpu_baseline": {"value": value, "unit": "matvecs/s", "cores": 1, "kind": "port",
-                         "sample": desc + "; reference C++ is not buildable here (Eigen3/FFTW3 absent)",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * nvec * t, "higher_is_better": True,
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded stand-in for the paper's datasets)", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "matvecs/s", "cores": 1, "kind": kind, "sample": desc,
                          "cpu": cpu_model(), "host_cores": os.cpu_count(), "setup_s": setup},
         "e2e": {"value": value, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-# ---- secondary configurations (reported under "also") ----------------------
-def secondary(cfg, steps, dev):
-    """Device matvecs/s and Lanczos time-to-k of another BASELINE config on
-    the same GPU (graph replays, L2 flushed between steps)."""
-    import torch
-    import paper_1808_04580_b200 as fgs
-    info = fgs.workload_info(cfg)
-    nvec = 16 if cfg == 5 else 1
-    X = fgs.workload_nodes(cfg, SEED)
-    n = X.shape[0]
-    t0 = time.perf_counter()
-    op = fgs.AdjacencyOperator(X, fgs.KernelSpec.gaussian(info["sigma"]),
-                               fgs.FastsumParams(info["N"], info["m"], info["p"], 0.0), device=dev)
-    setup_s = time.perf_counter() - t0
-    stream = torch.cuda.current_stream()
-    op.set_stream(stream.cuda_stream)
-    xh = fgs.workload_vectors(n, nvec, 99)
-    xh = xh if xh.ndim == 2 else xh[:, None]
-    xc = torch.from_numpy(np.asfortranarray(xh).T.copy()).to(f"cuda:{dev}")
-    xi = torch.empty((nvec, n), dtype=torch.float64, device=f"cuda:{dev}")
-    for v in range(nvec):
-        op.permute_device(xc[v].data_ptr(), xi[v].data_ptr(), nvec=1, ld=n, direction=0)
-    yi = torch.empty_like(xi)
-    flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=f"cuda:{dev}")
-
-    def step():
-        op.apply_device(fgs.OP_SYM_LAPLACIAN, xi.data_ptr(), yi.data_ptr(), nvec=nvec, ld=n, internal_order=True)
-
-    for _ in range(3):
-        step()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    torch.cuda.synchronize()
-    for s0, s1 in ev:
-        flush.zero_()
-        s0.record(stream)
-        step()
-        s1.record(stream)
-    torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
-    out = {"workload": f"config{cfg}", "n": n, "d": info["d"], "N": info["N"], "m": info["m"], "nvec": nvec,
-           "value": nvec / (ms / 1000.0), "unit": "matvecs/s", "ms_per_step": ms, "setup_s": setup_s}
-    if cfg <= 4:
-        out["lanczos"], _ = lanczos_timing(op, info)
-    return out
-
-
+# ---- B200 arm --------------------------------------------------------------
 def lanczos_timing(op, info, warm=2):
     """Lanczos time-to-k as the reference's eigs command splits it
     (commands.cpp:174-183): `solve_s` is the first solve on a fresh handle
     (workspace allocation and graph capture included, what a one-shot run
     pays); `solve_s_warm` the median of `warm` further solves on the same
-    handle.  Ritz vectors are formed and copied to the host every time."""
+    handle.  Ritz vectors are formed and copied to the host every time
+    (single device; sharded runs return the eigenvalues)."""
     import torch
 
     import paper_1808_04580_b200 as fgs
@@ -258,31 +317,101 @@ def lanczos_timing(op, info, warm=2):
         li = fgs.LanczosInfo()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        pairs = fgs.lanczos_largest(op, info["k"], fgs.LanczosOptions(tol=1e-8, seed=1), li)
+        pairs = fgs.lanczos_largest(op, info["k"], fgs.LanczosOptions(tol=1e-8, seed=1), li,
+                                    want_vectors=op.world == 1)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
         phases = op.lanczos_stats()
     rec = {"k": info["k"], "tol": 1e-8, "solve_s": times[0],
            "solve_s_warm": float(np.median(times[1:])) if warm else None,
-           "iterations": li.iterations, "converged": li.converged, "phases": phases}
-    return rec, pairs
+           "iterations": li.iterations, "converged": li.converged, "phases": phases,
+           "top_eig_A": [float(v) for v in pairs.values[:3]]}
+    return rec
 
 
-# ---- B200 arm --------------------------------------------------------------
+def make_op(X, info, dev, rank, world, nccl_id, sharded):
+    import paper_1808_04580_b200 as fgs
+    params = fgs.FastsumParams(info["N"], info["m"], info["p"], 0.0)
+    kernel = fgs.KernelSpec.gaussian(info["sigma"])
+    if sharded:
+        return fgs.AdjacencyOperator(X, kernel, params, device=dev, rank=rank, world=world, nccl_id=nccl_id)
+    return fgs.AdjacencyOperator(X, kernel, params, device=dev)
+
+
+def device_inputs(op, n, nvec, dev):
+    """This rank's slice of the seeded vectors in the internal order."""
+    import torch
+
+    import paper_1808_04580_b200 as fgs
+    xs_host = fgs.workload_vectors(n, nvec, VEC_SEED)
+    xs_host = xs_host if xs_host.ndim == 2 else xs_host[:, None]
+    nl = op.n_local
+    x_int = torch.empty((nvec, nl), dtype=torch.float64, device=f"cuda:{dev}")
+    for v in range(nvec):  # caller order -> this rank's slice of the internal order
+        xc = torch.from_numpy(np.ascontiguousarray(xs_host[:, v])).to(f"cuda:{dev}")
+        op.permute_device(xc.data_ptr(), x_int[v].data_ptr(), nvec=1, ld=n, direction=0)
+    return xs_host, x_int
+
+
+def secondary(cfg_id, steps, dev, rank, world, nccl_id, sharded, dist):
+    """Device matvecs/s and Lanczos time-to-k of another BASELINE config on
+    the same GPU(s) (graph replays, L2 flushed between steps)."""
+    import torch
+
+    import paper_1808_04580_b200 as fgs
+    from oracle import oracle as orc
+    info = orc.workload_info(cfg_id)
+    nvec = 16 if cfg_id == 5 else 1
+    X = orc.workload_nodes(cfg_id, SEED)
+    n = X.shape[0]
+    t0 = time.perf_counter()
+    op = make_op(X, info, dev, rank, world, nccl_id, sharded)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    op.set_stream(stream.cuda_stream)
+    _, xi = device_inputs(op, n, nvec, dev)
+    yi = torch.empty_like(xi)
+    flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def step():
+        op.apply_device(fgs.OP_SYM_LAPLACIAN, xi.data_ptr(), yi.data_ptr(), nvec=nvec, ld=op.n_local,
+                        internal_order=True)
+
+    for _ in range(3):
+        step()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    for s0, s1 in ev:
+        flush.zero_()
+        s0.record(stream)
+        step()
+        s1.record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    out = {"workload": f"config{cfg_id}", "n": n, "d": info["d"], "N": info["N"], "m": info["m"], "nvec": nvec,
+           "value": nvec / (ms / 1000.0), "unit": "matvecs/s", "ms_per_step": ms, "setup_s": setup_s}
+    if cfg_id <= 4:
+        out["lanczos"] = {"setup_s": setup_s, **lanczos_timing(op, info)}
+    return out
+
+
 def run_b200(args, rank, world, local_rank):
     import torch
+
     import paper_1808_04580_b200 as fgs
     dev = local_rank
     torch.cuda.set_device(dev)
-    info = fgs.workload_info(args.config)
-    nvec = args.nvec or (16 if args.config == 5 else 1)
-    X = fgs.workload_nodes(args.config, SEED)
-    n = X.shape[0]
-    params = fgs.FastsumParams(info["N"], info["m"], info["p"], 0.0)
-    kernel = fgs.KernelSpec.gaussian(info["sigma"])
+    cfg, n, nvec, info = workload(args, world)
+    X = nodes_for(args, n)
 
     sharded = world > 1 or args.force_sharded
-    dist = None
+    dist, nccl_id = None, None
     if sharded:
         import torch.distributed as dist
         nid = [fgs.nccl_unique_id() if rank == 0 else None]
@@ -290,24 +419,14 @@ def run_b200(args, rank, world, local_rank):
         nccl_id = nid[0]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    if sharded:
-        op = fgs.AdjacencyOperator(X, kernel, params, device=dev, rank=rank, world=world, nccl_id=nccl_id)
-    else:
-        op = fgs.AdjacencyOperator(X, kernel, params, device=dev)
+    op = make_op(X, info, dev, rank, world, nccl_id, sharded)
     setup_s = time.perf_counter() - t0
     stream = torch.cuda.Stream(device=dev)  # non-default: applies replay captured CUDA graphs
     torch.cuda.set_stream(stream)
     op.set_stream(stream.cuda_stream)
     nl = op.n_local
     geom = op.geometry()
-
-    # device-resident inputs in the internal order (this rank's slice)
-    xs_host = fgs.workload_vectors(n, nvec, 99)
-    xs_host = xs_host if xs_host.ndim == 2 else xs_host[:, None]
-    x_caller = torch.from_numpy(np.asfortranarray(xs_host).T.copy()).to(f"cuda:{dev}")  # [nvec][n]
-    x_int = torch.empty((nvec, nl), dtype=torch.float64, device=f"cuda:{dev}")
-    for v in range(nvec):  # caller order -> this rank's slice of the internal order
-        op.permute_device(x_caller[v].data_ptr(), x_int[v].data_ptr(), nvec=1, ld=n, direction=0)
+    xs_host, x_int = device_inputs(op, n, nvec, dev)
     y_int = torch.empty_like(x_int)
     flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=f"cuda:{dev}")  # > 126 MB L2
 
@@ -315,7 +434,7 @@ def run_b200(args, rank, world, local_rank):
         op.apply_device(fgs.OP_SYM_LAPLACIAN, x_int.data_ptr(), y_int.data_ptr(), nvec=nvec, ld=nl,
                         internal_order=True)
 
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     if dist:
@@ -339,9 +458,9 @@ def run_b200(args, rank, world, local_rank):
     if dist:
         dist.barrier()
     launches = op.launch_count() - launches0
-    # per-kernel durations: the same K steps again with stage events between
-    # the launches (direct launches; kernel durations do not depend on graph
-    # vs direct launch)
+    # per-kernel durations: K more steps with stage events between the
+    # launches (direct launches on the same stream; CUDA events on the
+    # launching stream)
     op.profile(True)
     for _ in range(args.steps):
         flush.zero_()
@@ -372,7 +491,7 @@ def run_b200(args, rank, world, local_rank):
     if t_fp >= t_hbm:
         roof = {"bound": "fp64", "achieved": f / t / 1e12, "peak": fp64_tf, "unit": "TFLOP/s",
                 "frac": (f / t / 1e12) / fp64_tf, "traffic": None,
-                "peak_source": "fp64 DFMA microbenchmark on this B200 (not in MEASURED_PEAKS.json)"}
+                "peak_source": "fp64 DFMA microbenchmark on this B200 (MEASURED_PEAKS.json has no fp64 entry)"}
     else:
         roof = {"bound": "hbm", "achieved": b / t / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": (b / t / 1e9) / peaks["hbm_gbs"], "traffic": None,
@@ -380,101 +499,112 @@ def run_b200(args, rank, world, local_rank):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh).get(f"config{args.config}", {}).get(dom)
-        if tr:
-            roof["traffic"] = tr["dram_bytes"] * (nvec if args.config != 5 else 1)
+        if tr and not args.weak and world == 1:
+            roof["traffic"] = tr["dram_bytes"]
             roof["traffic_source"] = f"ncu --set full, {tr['source']} ({tr['kernel']}), dram read+write per launch"
     except (OSError, ValueError):
         pass
+    step_flops = 2 * work["spread"][1]
     roof.update({"kernel": dom, "launch_ms": per_launch[dom], "algorithmic_bytes": b, "algorithmic_flops": f,
-                 "t_roof_ms": 1e3 * max(t_hbm, t_fp), "frac_of_max_roof": max(t_hbm, t_fp) / t,
-                 "stage_ms_per_step": {k: per_launch[k] for k in STAGES}})
+                 "t_roof_ms": 1e3 * max(t_hbm, t_fp), "stage_ms_per_step": {k: per_launch[k] for k in STAGES},
+                 "step_fp64_frac": step_flops / (ms_per_step * 1e-3) / (fp64_tf * 1e12)})
 
     # ---- end to end through the public API with pinned host buffers ---------
     e2e = None
-    if not sharded:
-        hx = torch.from_numpy(np.asfortranarray(xs_host)).pin_memory()
-        hy = torch.empty_like(hx).pin_memory()
-        import ctypes as C
-        L = fgs.lib()
-        xp = C.cast(hx.data_ptr(), C.POINTER(C.c_double))
-        yp = C.cast(hy.data_ptr(), C.POINTER(C.c_double))
-        for _ in range(args.warmup):
-            L.fgs_adjacency_apply(op.handle, fgs.OP_SYM_LAPLACIAN, xp, yp, nvec, C.c_int64(n))
-        torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        for _ in range(args.steps):
-            st = L.fgs_adjacency_apply(op.handle, fgs.OP_SYM_LAPLACIAN, xp, yp, nvec, C.c_int64(n))
-            assert st == 0, L.fgs_last_error()
-        s1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = s0.elapsed_time(s1) / args.steps
+    if not args.no_e2e:
+        if not sharded:
+            import ctypes as C
+            hx = torch.from_numpy(np.asfortranarray(xs_host).T.copy()).pin_memory()  # [nvec][n] = column-major
+            hy = torch.empty_like(hx).pin_memory()
+            L = fgs.lib()
+            xp = C.cast(hx.data_ptr(), C.POINTER(C.c_double))
+            yp = C.cast(hy.data_ptr(), C.POINTER(C.c_double))
+            for _ in range(2):
+                L.fgs_adjacency_apply(op.handle, fgs.OP_SYM_LAPLACIAN, xp, yp, nvec, C.c_int64(n))
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(args.steps):
+                st = L.fgs_adjacency_apply(op.handle, fgs.OP_SYM_LAPLACIAN, xp, yp, nvec, C.c_int64(n))
+                assert st == 0, L.fgs_last_error()
+            s1.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms = s0.elapsed_time(s1) / args.steps
+            path = "fgs_adjacency_apply (C ABI) with pinned host x/y in caller order"
+        else:
+            # sharded handles take device vectors in the internal order (the
+            # public multi-GPU API, fgs_adjacency_apply_device): each rank
+            # uploads its slice from pinned memory, applies, downloads
+            hx = x_int.cpu().pin_memory()
+            hy = torch.empty_like(hx).pin_memory()
+            for _ in range(2):
+                x_int.copy_(hx, non_blocking=True)
+                step()
+                hy.copy_(y_int, non_blocking=True)
+            torch.cuda.synchronize()
+            dist.barrier()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(args.steps):
+                x_int.copy_(hx, non_blocking=True)
+                step()
+                hy.copy_(y_int, non_blocking=True)
+                stream.synchronize()
+            s1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+            path = ("per rank: pinned slice H2D + fgs_adjacency_apply_device (sharded, internal order) + D2H; "
+                    "max over ranks")
         e2e = {"value": nvec / (e2e_ms / 1000.0), "unit": "matvecs/s", "h2d_bytes_per_step": 8 * n * nvec,
-               "d2h_bytes_per_step": 8 * n * nvec, "ms_per_step": e2e_ms,
-               "path": "fgs_adjacency_apply (C ABI) with pinned host x/y, caller order"}
+               "d2h_bytes_per_step": 8 * n * nvec, "ms_per_step": e2e_ms, "path": path}
+    del op
+    torch.cuda.synchronize()
 
-    else:
-        # sharded handles take device vectors in the internal order (the
-        # public multi-GPU API, fgs_adjacency_apply_device): each rank uploads
-        # its slice from pinned memory, applies, downloads; max over ranks
-        hx = x_int.cpu().pin_memory()
-        hy = torch.empty_like(hx).pin_memory()
-        for _ in range(args.warmup):
-            x_int.copy_(hx, non_blocking=True)
-            step()
-            hy.copy_(y_int, non_blocking=True)
-        torch.cuda.synchronize()
-        dist.barrier()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        for _ in range(args.steps):
-            x_int.copy_(hx, non_blocking=True)
-            step()
-            hy.copy_(y_int, non_blocking=True)
-            stream.synchronize()
-        s1.record(stream)
-        torch.cuda.synchronize()
-        t = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-        e2e = {"value": nvec / (e2e_ms / 1000.0), "unit": "matvecs/s", "h2d_bytes_per_step": 8 * n * nvec,
-               "d2h_bytes_per_step": 8 * n * nvec, "ms_per_step": e2e_ms,
-               "path": "per rank: pinned slice H2D + fgs_adjacency_apply_device (sharded, internal order) + D2H; "
-                       "max over ranks"}
-
-    # ---- Lanczos time-to-k (spectral.cpp:141-256 via the device path) -------
-    lanczos = None
-    if not sharded and not args.no_lanczos and args.config <= 4:
-        rec, pairs = lanczos_timing(op, info)
-        lanczos = {"setup_s": setup_s, **rec, "total_s": setup_s + rec["solve_s"],
-                   "smallest_laplacian_eigs": [1.0 - v for v in pairs.values[:4].tolist()]}
-
-    # ---- CPU baseline (rank 0, N=1) ----------------------------------------
-    cpu = None
-    if not sharded and not args.no_cpu:
-        rate, desc, csetup = cpu_matvecs_per_s(args.config, X, info, nvec, args.cpu_seconds)
-        cpu = {"value": rate, "unit": "matvecs/s", "cores": 1, "kind": "port", "sample": desc,
-               "cpu": cpu_model(), "host_cores": os.cpu_count(), "setup_s": csetup}
-
+    # ---- secondary configurations with Lanczos time-to-k -------------------
     also = []
-    if not sharded and args.also:
-        for cfg in [int(c) for c in args.also.split(",") if c.strip()]:
-            if cfg != args.config:
+    if args.also:
+        for c in [int(c) for c in args.also.split(",") if c.strip()]:
+            if c == args.config and not args.weak:
+                continue
+            try:
+                also.append(secondary(c, 10 if c != 5 else 2, dev, rank, world, nccl_id, sharded, dist))
+            except Exception as ex:  # noqa: BLE001 - report, do not lose the main line
+                also.append({"workload": f"config{c}", "error": str(ex)[:300]})
+    lanczos = None
+    if not args.no_lanczos and args.config <= 4 and not args.weak:
+        try:
+            op = make_op(X, info, dev, rank, world, nccl_id, sharded)
+            op.set_stream(stream.cuda_stream)
+            lanczos = {"setup_s": setup_s, **lanczos_timing(op, info)}
+            lanczos["total_s"] = setup_s + lanczos["solve_s"]
+            del op
+        except Exception as ex:  # noqa: BLE001
+            lanczos = {"error": str(ex)[:300]}
+
+    # ---- CPU baseline (rank 0, N = 1): matvecs/s + Lanczos time-to-k ---------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, _, csetup, desc, kind = cpu_matvec_rate(args.config, X, info, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "matvecs/s", "cores": 1, "kind": kind, "sample": desc,
+               "cpu": cpu_model(), "host_cores": os.cpu_count(), "setup_s": csetup}
+        if not args.no_lanczos:
+            cpu["lanczos"] = []
+            for c in (1, 2):
                 try:
-                    also.append(secondary(cfg, 10 if cfg != 5 else 2, dev))
-                except Exception as e:  # noqa: BLE001 - report, do not lose the main line
-                    also.append({"workload": f"config{cfg}", "error": str(e)[:200]})
+                    cpu["lanczos"].append(cpu_lanczos(c))
+                except Exception as ex:  # noqa: BLE001
+                    cpu["lanczos"].append({"workload": f"config{c}", "error": str(ex)[:300]})
 
     if rank == 0:
         line = {
-            "metric": "fp64 Laplacian matvecs/sec", "value": value, "unit": "matvecs/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded stand-in for the paper's datasets)",
-            "config": {"workload": f"config{args.config}", "n": n, "d": info["d"], "sigma": info["sigma"],
-                       "N": info["N"], "m": info["m"], "p": info["p"], "nvec": nvec, "op": "L_s x",
-                       "parallelism": f"points sharded x{world}" if sharded else "single GPU",
-                       "l2": "flushed (256 MB write) between timed steps, outside the events"},
+            "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded stand-in for the paper's datasets)", "config": cfg,
+            "parallelism": f"points sharded x{world} (NCCL)" if sharded else "single GPU",
+            "l2": "flushed (256 MB write) between timed steps, outside the events",
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(w0, w1), "lanczos": lanczos, "setup_s": setup_s, "also": also,
         }
@@ -483,21 +613,27 @@ def run_b200(args, rank, world, local_rank):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if (world > 1 or args.force_sharded) and args.impl == "b200":
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+    if args.gpus != world and "WORLD_SIZE" in os.environ:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
-    else:
+        return
+    import torch
+    import torch.distributed as dist
+    distributed = world > 1 or args.force_sharded
+    if distributed:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
         run_b200(args, rank, world, local_rank)
-    if (world > 1 or args.force_sharded) and args.impl == "b200":
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    finally:
+        if distributed:
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -186,6 +186,10 @@ fgs_status fgs_lanczos_stats(fgs_adjacency_t h, double* out4);
 fgs_status fgs_workload_info(int config, int64_t* n, int* d, double* sigma, int* N, int* m, int* p,
                              int* k);
 fgs_status fgs_workload_generate(int config, uint64_t seed, double* nodes_colmajor);
+/* the same generator with n_points points instead of the config's n (0: the
+ * config's n; config 3's image is fixed-size) -- BASELINE config 5's weak
+ * scaling at 1.25M points per GPU */
+fgs_status fgs_workload_generate_n(int config, uint64_t seed, int64_t n_points, double* nodes_colmajor);
 fgs_status fgs_workload_vectors(int64_t n, int nvec, uint64_t seed, double* out);
 
 /* ---- conjugate gradients (spectral.hpp:120-140, spectral.cpp:446-495) ---- */

@@ -42,8 +42,9 @@ class OracleError(Exception):
 
 def build() -> str:
     """Compile the oracle if its shared object is missing or stale."""
-    src = os.path.join(_HERE, "fgs_oracle.cpp")
-    if (not os.path.exists(_SO)) or os.path.getmtime(_SO) < os.path.getmtime(src):
+    srcs = [os.path.join(_HERE, "fgs_oracle.cpp"),
+            os.path.join(_HERE, "..", "paper_1808_04580_b200", "csrc", "workload.cpp")]
+    if (not os.path.exists(_SO)) or os.path.getmtime(_SO) < max(os.path.getmtime(s) for s in srcs if os.path.exists(s)):
         subprocess.check_call(["bash", os.path.join(_HERE, "build_oracle.sh")])
     return _SO
 
@@ -462,3 +463,26 @@ def nystrom_dense(A, k, L, M, seed=1):
 
 def nystrom_adjacency(adj, n, k, L, M, seed=1):
     return _nystrom(lib().orc_nystrom_adjacency, (adj._h,), n, k, L, M, seed)
+
+
+# ---- seeded BASELINE workloads (the same generator the product exports) ----
+def workload_info(config: int) -> dict:
+    n, d, N, m, p, k = C.c_int64(), C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    sigma = C.c_double()
+    _check(lib().fgs_workload_info(int(config), C.byref(n), C.byref(d), C.byref(sigma), C.byref(N), C.byref(m),
+                                   C.byref(p), C.byref(k)))
+    return dict(n=n.value, d=d.value, sigma=sigma.value, N=N.value, m=m.value, p=p.value, k=k.value)
+
+
+def workload_nodes(config: int, seed: int = 2024, n: int = 0) -> np.ndarray:
+    info = workload_info(config)
+    npts = n or info["n"]
+    out = np.zeros(npts * info["d"])
+    _check(lib().fgs_workload_generate_n(int(config), C.c_uint64(seed), C.c_int64(n), _dp(out)))
+    return out.reshape(info["d"], npts).T.copy()
+
+
+def workload_vectors(n: int, nvec: int, seed: int) -> np.ndarray:
+    out = np.zeros(n * nvec)
+    _check(lib().fgs_workload_vectors(C.c_int64(n), int(nvec), C.c_uint64(seed), _dp(out)))
+    return out.reshape(nvec, n).T if nvec > 1 else out

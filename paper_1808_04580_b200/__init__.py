@@ -678,11 +678,14 @@ def workload_info(config: int) -> dict:
     return dict(n=n.value, d=d.value, sigma=sigma.value, N=N.value, m=m.value, p=p.value, k=k.value)
 
 
-def workload_nodes(config: int, seed: int = 2024) -> np.ndarray:
+def workload_nodes(config: int, seed: int = 2024, n: int = 0) -> np.ndarray:
+    """Seeded synthetic nodes of BASELINE config 1..5 (n > 0: that many
+    points from the same generator, e.g. config 5's weak scaling)."""
     info = workload_info(config)
-    out = np.zeros(info["n"] * info["d"])
-    _check(lib().fgs_workload_generate(int(config), C.c_uint64(seed), _dp(out)))
-    return out.reshape(info["d"], info["n"]).T.copy()
+    npts = n or info["n"]
+    out = np.zeros(npts * info["d"])
+    _check(lib().fgs_workload_generate_n(int(config), C.c_uint64(seed), C.c_int64(n), _dp(out)))
+    return out.reshape(info["d"], npts).T.copy()
 
 
 def workload_vectors(n: int, nvec: int, seed: int) -> np.ndarray:

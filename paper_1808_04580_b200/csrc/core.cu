@@ -16,7 +16,6 @@
 #include "core.cuh"
 #include "kernels.cuh"
 #include "kernels_v2.cuh"
-#include "kernels_v3.cuh"
 #include "kernels_v4.cuh"
 #include "conv2d.cuh"
 #include "direct.cuh"
@@ -162,9 +161,11 @@ __global__ void permute_kernel(const double* x, int64_t ldx, double* y, int64_t 
 }
 
 // ---- launch policy ----------------------------------------------------------
-// 2m <= 16: register-blocked cp.async kernels (kernels_v2.cuh); FGS_KERNEL=v1
-// selects the first-generation single-row kernels (kept for A/B timing);
-// 2m > 16: runtime-2m single-value kernels (kernels.cuh).
+// d = 3, 2m in {8, 12, 16}: fp64 tensor-core (DMMA) kernels (kernels_v4.cuh);
+// the spread needs dense runs (>= kDenseRun points per cell), sparser plans
+// use the register-blocked cp.async kernel (kernels_v2.cuh).  d = 2, 2m in
+// {8, 12, 16}: the d = 2 DMMA kernels, same rule.  Other 2m <= 16: v2
+// kernels; 2m > 16: runtime-2m single-value kernels (kernels.cuh).
 // cudaFuncSetAttribute is a driver call; raise each kernel's dynamic shared
 // memory limit once, not on every launch (ncu/launch-overhead hygiene)
 void set_smem(const void* func, size_t smem) {
@@ -177,141 +178,41 @@ void set_smem(const void* func, size_t smem) {
   done[func] = smem;
 }
 
-bool kernel_env(const char* v) {
-  const char* e = std::getenv("FGS_KERNEL");
-  return e && std::string(e) == v;
-}
 // the tensor-core spread needs runs of >= this many points (K-steps of 4,
 // one block flush per run); sparser plans use the scalar register-blocked one
 constexpr double kDenseRun = 12.0;
 
-bool use_v1() {
-  static const bool v1 = kernel_env("v1");
-  return v1;
-}
-// warp-resident-footprint interpolation (kernels_v3.cuh) for d = 3, 2m in {8,12,16}
 template <int D, int T>
-constexpr bool has_v3() {
+constexpr bool has_v4_3d() {
   return D == 3 && (T == 8 || T == 12 || T == 16);
 }
 template <int D, int T>
 constexpr bool has_v4_2d() {
   return D == 2 && (T == 8 || T == 12 || T == 16);
 }
-bool use_v3() {
-  static const bool v3 = kernel_env("v3");
-  return v3;
-}
-// d = 3 tensor-core kernel variants: (point streams P, chunk QS) from
-// FGS_V4_SPREAD / FGS_V4_INTERP = "P,QS" (0 = default P); default "0,32"
-struct V4Var {
-  int p, qs;
-};
-V4Var v4_variant(bool interp) {
-  const char* e = std::getenv(interp ? "FGS_V4_INTERP" : "FGS_V4_SPREAD");
-  V4Var v{0, 0};
-  if (e) std::sscanf(e, "%d,%d", &v.p, &v.qs);
-  if (v.qs != 64 && v.qs != 32) v.qs = 0;
-  if (v.p != 1 && v.p != 2 && v.p != 4) v.p = 0;
-  return v;
-}
+
+// d = 2 tensor-core kernels: point-stream warps per CTA (interpolation 2:
+// C2 22.8 k vs 22.2 k with 4, 21.7 k with 1; spread 1)
+constexpr int kInterp2dP = 2;
+constexpr int kSpread2dP = 1;
+// staged input window (Blk4d2::XW) of the d = 2 variant with P streams
+constexpr size_t xw2d(int p) { return static_cast<size_t>(p * 32 > 64 ? p * 32 : 64); }
 
 template <int T, bool INTERP>
-size_t v4_stage_doubles(V4Var v) {
-  auto one = [](auto tag) -> size_t {
-    using B = decltype(tag);
-    return INTERP ? 2 * static_cast<size_t>(B::QS) * B::STRIDE + 2 * static_cast<size_t>(B::QS) * (B::G + 3)
-                  : 2 * static_cast<size_t>(B::QS) * B::STRIDE + 2 * B::QS;
-  };
-#define FGS_V4V(PP, QQ) \
-  if (v.p == PP && v.qs == QQ) return one(Blk4<T, INTERP, PP, QQ>{});
-  FGS_V4V(0, 0) FGS_V4V(0, 32) FGS_V4V(0, 64) FGS_V4V(1, 32) FGS_V4V(1, 64) FGS_V4V(2, 32) FGS_V4V(2, 64) FGS_V4V(4, 32)
-  FGS_V4V(4, 64)
-#undef FGS_V4V
-  return one(Blk4<T, INTERP, 0, 0>{});
+constexpr size_t v4_stage_doubles() {
+  using B = Blk4<T, INTERP>;
+  return INTERP ? 2 * static_cast<size_t>(B::QS) * B::STRIDE + 2 * static_cast<size_t>(B::QS) * (B::G + 3)
+                : 2 * static_cast<size_t>(B::QS) * B::STRIDE + 2 * B::QS;
 }
 
-// private spread boxes of the variant in use (P when P >= 4, else one shared box)
+// private spread boxes of the d = 3 DMMA spread (P when P >= 4, else one shared box)
 int v4_spread_groups(int T) {
-  const V4Var v = v4_variant(false);
-  auto pick = [&](auto tag) -> int {
-    constexpr int TT = decltype(tag)::value;
-#define FGS_V4P(PP, QQ) \
-  if (v.p == PP && v.qs == QQ) return Blk4<TT, false, PP, QQ>::P >= 4 ? Blk4<TT, false, PP, QQ>::P : 1;
-    FGS_V4P(0, 0) FGS_V4P(0, 32) FGS_V4P(0, 64) FGS_V4P(1, 32) FGS_V4P(1, 64) FGS_V4P(2, 32) FGS_V4P(2, 64)
-    FGS_V4P(4, 32) FGS_V4P(4, 64)
-#undef FGS_V4P
-    return Blk4<TT, false, 0, 0>::P >= 4 ? Blk4<TT, false, 0, 0>::P : 1;
-  };
   switch (T) {
-    case 8: return pick(std::integral_constant<int, 8>{});
-    case 12: return pick(std::integral_constant<int, 12>{});
-    case 16: return pick(std::integral_constant<int, 16>{});
+    case 8: return Blk4<8, false>::P >= 4 ? Blk4<8, false>::P : 1;
+    case 12: return Blk4<12, false>::P >= 4 ? Blk4<12, false>::P : 1;
+    case 16: return Blk4<16, false>::P >= 4 ? Blk4<16, false>::P : 1;
     default: return 1;
   }
-}
-
-template <int T, bool INTERP>
-void v4_launch(V4Var v, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
-#define FGS_V4L(PP, QQ)                                                               \
-  if (v.p == PP && v.qs == QQ) {                                                      \
-    if (INTERP) {                                                                     \
-      auto k = interp_v4_kernel<T, PP, QQ>;                                           \
-      set_smem(reinterpret_cast<const void*>(k), smem);                               \
-      launch_ex(k, nitems, Blk4<T, true, PP, QQ>::NT, smem, s, a, box_stride);               \
-    } else {                                                                          \
-      auto k = spread_v4_kernel<T, PP, QQ>;                                           \
-      set_smem(reinterpret_cast<const void*>(k), smem);                               \
-      launch_ex(k, nitems, Blk4<T, false, PP, QQ>::NT, smem, s, a, box_stride);              \
-    }                                                                                 \
-    return;                                                                           \
-  }
-  if (INTERP && v.p == 0 && v.qs == 0 && a.defer_epilogue) {  // default interp variant, large plan
-    auto k = interp_v4_kernel<T, 0, 0, true>;
-    set_smem(reinterpret_cast<const void*>(k), smem);
-    launch_ex(k, nitems, Blk4<T, true, 0, 0>::NT, smem, s, a, box_stride);
-    return;
-  }
-  FGS_V4L(0, 0) FGS_V4L(0, 32) FGS_V4L(0, 64) FGS_V4L(1, 32) FGS_V4L(1, 64) FGS_V4L(2, 32) FGS_V4L(2, 64) FGS_V4L(4, 32)
-  FGS_V4L(4, 64)
-#undef FGS_V4L
-}
-
-// fp64 tensor-core kernels (kernels_v4.cuh): the default for d = 3, 2m in {8,12,16}
-bool use_v4() {
-  static const bool v4 = !kernel_env("v1") && !kernel_env("v2") && !kernel_env("v3");
-  return v4;
-}
-
-// d = 2 tensor-core kernels: point-stream warps per CTA.  Interp 2 measured
-// best on C2 (22.8 k vs 22.2 k with 4, 21.7 k with 1), FGS_INTERP2D_P
-// overrides; spread 1, FGS_SPREAD2D_P overrides.
-int interp2d_p() {
-  static const int p = [] {
-    const char* e = std::getenv("FGS_INTERP2D_P");
-    const int v = e ? std::atoi(e) : 2;
-    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 2;
-  }();
-  return p;
-}
-int spread2d_p() {
-  static const int p = [] {
-    const char* e = std::getenv("FGS_SPREAD2D_P");
-    const int v = e ? std::atoi(e) : 1;
-    return v == 1 || v == 2 || v == 4 ? v : 1;
-  }();
-  return p;
-}
-// staged input window (Blk4d2::XW) of the d = 2 variant with P streams
-size_t xw2d(int p) { return static_cast<size_t>(std::max(64, 32 * p)); }
-
-template <int D, int T>
-constexpr int e_of() {
-  return D == 3 ? T : (D == 2 ? (T >= 2 ? T / 2 : 1) : (T >= 2 ? 2 : 1));
-}
-template <int D, int T>
-constexpr int nt_of() {
-  return D == 3 ? ((T * T + 31) / 32 * 32 > 256 ? 256 : (T * T + 31) / 32 * 32) : 32;
 }
 
 // shared-memory doubles beyond the box, and threads, of the kernel that
@@ -323,29 +224,19 @@ struct LaunchShape {
 
 template <int D, int T>
 LaunchShape shape_t(bool dense) {
-  if (use_v1()) {
-    const size_t base = static_cast<size_t>(kQ) * D * T + kQ;
-    return {nt_of<D, T>(), base, base + nt_of<D, T>()};
-  }
   using B = Blk<D, T>;
   const size_t base = 2 * static_cast<size_t>(B::QS) * B::TAPS + 2 * B::QS;
   size_t interp = base + 2 * static_cast<size_t>(B::NT / 32) * B::QB;
   size_t spread = base;
-  if constexpr (has_v3<D, T>()) {
-    using B3 = Blk3<T>;
-    if (use_v3()) interp = 2 * static_cast<size_t>(B3::QS) * B3::TAPS + static_cast<size_t>(B3::P) * B3::G * B3::QB;
-    if (use_v4()) {
-      interp = v4_stage_doubles<T, true>(v4_variant(true));
-      if (dense) spread = v4_stage_doubles<T, false>(v4_variant(false));
-    }
+  if constexpr (has_v4_3d<D, T>()) {
+    interp = v4_stage_doubles<T, true>();
+    if (dense) spread = v4_stage_doubles<T, false>();
   }
   if constexpr (has_v4_2d<D, T>()) {
     using B4 = Blk4d2<T>;
-    if (use_v4()) {
-      // taps double buffer + staged inputs (interp: x and caller index)
-      interp = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE + 2 * xw2d(interp2d_p());
-      if (dense) spread = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE + xw2d(spread2d_p());
-    }
+    // taps double buffer + staged inputs (interp: x and caller index)
+    interp = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE + 2 * xw2d(kInterp2dP);
+    if (dense) spread = 2 * static_cast<size_t>(B4::QS) * B4::STRIDE + xw2d(kSpread2dP);
   }
   return {B::NT, spread, interp};
 }
@@ -367,87 +258,35 @@ LaunchShape shape_of(int T, bool dense) {
   return {256, base, base + 256};
 }
 
+template <class K, class... Args>
+void launch_smem(K k, int nitems, int nt, size_t smem, cudaStream_t s, Args... args) {
+  set_smem(reinterpret_cast<const void*>(k), smem);
+  launch_ex(k, nitems, nt, smem, s, args...);
+}
+
 template <int D, int T>
 void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
-  if (use_v1()) {
-    constexpr int E = e_of<D, T>();
-    constexpr int NT = nt_of<D, T>();
+  if constexpr (has_v4_2d<D, T>()) {
+    if (interp)
+      return launch_smem(interp_v4_2d_kernel<T, kInterp2dP>, nitems, Blk4d2<T, kInterp2dP>::NT, smem, s, a, box_stride);
+    if (dense)
+      return launch_smem(spread_v4_2d_kernel<T, kSpread2dP>, nitems, Blk4d2<T, kSpread2dP>::NT, smem, s, a, box_stride);
+  }
+  if constexpr (has_v4_3d<D, T>()) {
     if (interp) {
-      auto k = interp_kernel<D, T, E, NT>;
-      set_smem(reinterpret_cast<const void*>(k), smem);
-      k<<<nitems, NT, smem, s>>>(a, T, box_stride);
-    } else {
-      auto k = spread_kernel<D, T, E, NT>;
-      set_smem(reinterpret_cast<const void*>(k), smem);
-      k<<<nitems, NT, smem, s>>>(a, T, box_stride);
+      // one warp per footprint: partials combined per chunk only on large
+      // plans (C3 +7 %, C1 -5 %); G > 1 always combines per chunk
+      if (a.defer_epilogue)
+        return launch_smem(interp_v4_kernel<T, 0, 0, true>, nitems, Blk4<T, true>::NT, smem, s, a, box_stride);
+      return launch_smem(interp_v4_kernel<T, 0, 0>, nitems, Blk4<T, true>::NT, smem, s, a, box_stride);
     }
-    return;
+    if (dense) return launch_smem(spread_v4_kernel<T, 0, 0>, nitems, Blk4<T, false>::NT, smem, s, a, box_stride);
   }
   constexpr int NT = Blk<D, T>::NT;
-  if constexpr (has_v4_2d<D, T>()) {
-    if (use_v4() && (interp || dense)) {
-      if (interp) {
-        const int pi = interp2d_p();
-        if (pi == 1) {
-          auto k = interp_v4_2d_kernel<T, 1>;
-          set_smem(reinterpret_cast<const void*>(k), smem);
-          launch_ex(k, nitems, Blk4d2<T, 1>::NT, smem, s, a, box_stride);
-        } else if (pi == 2) {
-          auto k = interp_v4_2d_kernel<T, 2>;
-          set_smem(reinterpret_cast<const void*>(k), smem);
-          launch_ex(k, nitems, Blk4d2<T, 2>::NT, smem, s, a, box_stride);
-        } else if (pi == 8) {
-          auto k = interp_v4_2d_kernel<T, 8>;
-          set_smem(reinterpret_cast<const void*>(k), smem);
-          launch_ex(k, nitems, Blk4d2<T, 8>::NT, smem, s, a, box_stride);
-        } else {
-          auto k = interp_v4_2d_kernel<T, 4>;
-          set_smem(reinterpret_cast<const void*>(k), smem);
-          launch_ex(k, nitems, Blk4d2<T, 4>::NT, smem, s, a, box_stride);
-        }
-      } else {
-        const int ps = spread2d_p();
-        if (ps == 4) {
-          auto k = spread_v4_2d_kernel<T, 4>;
-          set_smem(reinterpret_cast<const void*>(k), smem);
-          launch_ex(k, nitems, Blk4d2<T, 4>::NT, smem, s, a, box_stride);
-        } else if (ps == 2) {
-          auto k = spread_v4_2d_kernel<T, 2>;
-          set_smem(reinterpret_cast<const void*>(k), smem);
-          launch_ex(k, nitems, Blk4d2<T, 2>::NT, smem, s, a, box_stride);
-        } else {
-          auto k = spread_v4_2d_kernel<T, 1>;
-          set_smem(reinterpret_cast<const void*>(k), smem);
-          launch_ex(k, nitems, Blk4d2<T, 1>::NT, smem, s, a, box_stride);
-        }
-      }
-      return;
-    }
-  }
-  if constexpr (has_v3<D, T>()) {
-    if (use_v4() && (interp || dense)) {
-      if (interp)
-        v4_launch<T, true>(v4_variant(true), a, nitems, smem, box_stride, s);
-      else
-        v4_launch<T, false>(v4_variant(false), a, nitems, smem, box_stride, s);
-      return;
-    }
-    if (interp && use_v3()) {
-      auto k = interp_v3_kernel<T>;
-      set_smem(reinterpret_cast<const void*>(k), smem);
-      k<<<nitems, Blk3<T>::NT, smem, s>>>(a, box_stride);
-      return;
-    }
-  }
-  if (interp) {
-    auto k = interp_v2_kernel<D, T>;
-    set_smem(reinterpret_cast<const void*>(k), smem);
-    k<<<nitems, NT, smem, s>>>(a, box_stride);
-  } else {
-    auto k = spread_v2_kernel<D, T>;
-    set_smem(reinterpret_cast<const void*>(k), smem);
-    k<<<nitems, NT, smem, s>>>(a, box_stride);
-  }
+  if (interp)
+    launch_smem(interp_v2_kernel<D, T>, nitems, NT, smem, s, a, box_stride);
+  else
+    launch_smem(spread_v2_kernel<D, T>, nitems, NT, smem, s, a, box_stride);
 }
 
 template <int D>
@@ -464,7 +303,7 @@ void dispatch(bool interp, bool dense, int T, const PassArgs& a, int nitems, siz
     case 16: return launch_t<D, 16>(interp, dense, a, nitems, smem, box_stride, s);
     default: break;
   }
-  // runtime-2m fallback (m > 8): one value per unit, 256 threads
+  // runtime-2m kernels (m > 8): one value per unit, 256 threads
   if (interp) {
     auto k = interp_kernel<D, 0, 1, 256>;
     set_smem(reinterpret_cast<const void*>(k), smem);
@@ -957,56 +796,27 @@ void Core::build_plan(const double* nodes_colmajor) {
     asm_idx.upload(idx.data(), idx.size(), stream);
     // lanes per cell by list length: clustered data concentrates most entries
     // in a few long lists (C3-C5: ~85 % of the entries sit in lists > 64),
-    // which one lane per cell walks serially.  Split only when the mean list
-    // is short (one lane per cell would be chosen) and the plan is large
-    // enough to amortise two more launches; otherwise one launch with lanes
-    // by the mean.  FGS_ASM_STATS=1 prints the distribution.
-    asm_split = false;
-    asm_class_n[0] = asm_class_n[1] = asm_class_n[2] = 0;
+    // which one lane per cell walks serially.  Cells are sorted into three
+    // warp-aligned classes (<= 8 entries: one lane, 9..64: 8 lanes, > 64: a
+    // warp), heaviest first, and one launch serves all three.  Cells no item
+    // box touches are not listed: the spread grid is zeroed once when the
+    // workspace is created and those cells are never written (the convolution
+    // writes a separate output grid), so the assembly covers only the point
+    // cloud's footprint (and, sharded, only this rank's slab of it).
     {
-      const double mean_list = static_cast<double>(cnt.back()) / static_cast<double>(std::max<int64_t>(grid_elems, 1));
-      static const bool split_on = [] {
-        const char* e = std::getenv("FGS_ASM_CLASSES");
-        return !(e && std::string(e) == "0");
-      }();
       std::vector<int> cls[3];
-      int64_t entries[3] = {0, 0, 0};
-      int maxlen = 0;
       for (int64_t g = 0; g < grid_elems; ++g) {
         const int len = cnt[static_cast<size_t>(g) + 1] - cnt[static_cast<size_t>(g)];
-        const int c = len <= 8 ? 0 : (len <= 64 ? 1 : 2);
-        cls[c].push_back(static_cast<int>(g));
-        entries[c] += len;
-        maxlen = std::max(maxlen, len);
+        if (len == 0) continue;
+        cls[len <= 8 ? 0 : (len <= 64 ? 1 : 2)].push_back(static_cast<int>(g));
       }
-      if (std::getenv("FGS_ASM_STATS"))
-        std::fprintf(stderr, "[asm] cells %lld entries %lld mean %.2f max %d | entries in lists <=8 %lld, 9..64 %lld, >64 %lld\n",
-                     static_cast<long long>(grid_elems), static_cast<long long>(cnt.back()), mean_list, maxlen,
-                     static_cast<long long>(entries[0]), static_cast<long long>(entries[1]),
-                     static_cast<long long>(entries[2]));
-      // default: one mixed launch with lanes by class (FGS_ASM_MIXED=0: the
-      // previous policy -- per-class launches for large sparse plans, else
-      // lanes by the mean list length)
-      static const bool mixed_on = [] {
-        const char* e = std::getenv("FGS_ASM_MIXED");
-        return !(e && std::string(e) == "0");
-      }();
-      for (int c = 0; c < 3; ++c) asm_class_n[c] = static_cast<int64_t>(cls[c].size());
-      asm_mixed = false;
-      if (mixed_on) {
-        std::vector<int> all;
-        all.reserve(static_cast<size_t>(grid_elems));
-        for (int c = 2; c >= 0; --c) all.insert(all.end(), cls[c].begin(), cls[c].end());  // heaviest first
-        asm_mixed_cells.upload(all.data(), all.size(), stream);
-        asm_mixed = true;
+      std::vector<int> all;
+      for (int c = 2; c >= 0; --c) {
+        asm_class_n[c] = static_cast<int64_t>(cls[c].size());
+        all.insert(all.end(), cls[c].begin(), cls[c].end());  // heaviest first
       }
-      // FGS_ASM_MIXED=0: per-class launches for large sparse plans, else
-      // lanes by the mean list length
-      if (!asm_mixed && split_on && mean_list < 4.0 && n_local >= 100000) {
-        asm_split = true;
-        for (int c = 0; c < 3; ++c)
-          if (!cls[c].empty()) asm_cells[c].upload(cls[c].data(), cls[c].size(), stream);
-      }
+      if (all.empty()) all.push_back(0);
+      asm_cells.upload(all.data(), all.size(), stream);
     }
   }
   if (ditems.empty()) {
@@ -1128,6 +938,9 @@ Workspace& Core::workspace(int nvec) {
   }
   w->priv.alloc(static_cast<size_t>(std::max(nitems, 1)) * box_stride * nvec);
   w->grid.alloc(static_cast<size_t>(grid_elems) * nvec);
+  FGS_CUDA(cudaMemsetAsync(w->grid.p, 0, sizeof(double) * grid_elems * nvec, stream));
+  w->grid_out.alloc(static_cast<size_t>(grid_elems) * nvec);
+  if (sharded && d == 2) w->grid_sum.alloc(static_cast<size_t>(grid_elems) * nvec);
   w->spec.alloc(static_cast<size_t>(spec_elems) * nvec);
   if (sharded) w->window.alloc(static_cast<size_t>(window_elems) * nvec);
   int dims[3] = {M, M, M};
@@ -1147,9 +960,9 @@ size_t Core::smem_bytes(bool interp) const {
   const bool dense = mean_run >= kDenseRun;
   const LaunchShape sh = d == 3 ? shape_of<3>(T, dense) : (d == 2 ? shape_of<2>(T, dense) : shape_of<1>(T, dense));
   size_t boxes = static_cast<size_t>(box_stride);
-  if (d == 3 && !interp && dense && use_v4()) boxes *= static_cast<size_t>(v4_spread_groups(T));  // per-group boxes
-  if (d == 2 && !interp && dense && use_v4() && (T == 8 || T == 12 || T == 16))
-    boxes *= static_cast<size_t>(spread2d_p());  // per-stream boxes
+  if (d == 3 && !interp && dense) boxes *= static_cast<size_t>(v4_spread_groups(T));  // per-group boxes
+  if (d == 2 && !interp && dense && (T == 8 || T == 12 || T == 16))
+    boxes *= static_cast<size_t>(kSpread2dP);  // per-stream boxes
   return (boxes + (interp ? sh.extra_interp : sh.extra_spread)) * sizeof(double);
 }
 
@@ -1180,50 +993,23 @@ void Core::launch_interp(const PassArgs& a) {
 
 void Core::launch_assemble(Workspace& w, int nvec) {
   const int64_t pstride = static_cast<int64_t>(std::max(nitems, 1)) * box_stride;
-  if (asm_mixed) {
-    AssembleMixedArgs m{};
-    m.a = AssembleArgs{asm_ptr.p, asm_idx.p, w.priv.p, pstride, w.grid.p, grid_elems, grid_elems, nvec, nullptr};
-    m.cells = asm_mixed_cells.p;
-    m.n0 = asm_class_n[0];
-    m.n1 = asm_class_n[1];
-    m.n2 = asm_class_n[2];
-    m.w2 = m.n2;
-    m.w1 = (m.n1 + 3) / 4;
-    const int64_t warps = m.w2 + m.w1 + (m.n0 + 31) / 32;
-    const dim3 blocks(static_cast<unsigned>(std::max<int64_t>(1, ceil_div(warps * 32, 256))));
-    if (nvec > 1)  // indices hoisted out of the vector loop (C5 16-vector blocks: 1.82 -> 1.71 ms)
-      launch_ex(assemble_mixed_kernel<true>, blocks, 256, 0, stream, m);
-    else
-      launch_ex(assemble_mixed_kernel<false>, blocks, 256, 0, stream, m);
-    ++launches;
-    FGS_CUDA(cudaGetLastError());
-    return;
-  }
-  if (!asm_split) {  // lanes per cell from the mean list length, one launch
-    AssembleArgs aa{asm_ptr.p, asm_idx.p, w.priv.p, pstride, w.grid.p, grid_elems, grid_elems, nvec, nullptr};
-    const double mean_list = static_cast<double>(asm_idx.n) / static_cast<double>(std::max<int64_t>(grid_elems, 1));
-    if (mean_list >= 16.0)
-      launch_ex(assemble_kernel<8>, dim3(ceil_div(grid_elems * 8, 256)), 256, 0, stream, aa);
-    else if (mean_list >= 4.0)
-      launch_ex(assemble_kernel<4>, dim3(ceil_div(grid_elems * 4, 256)), 256, 0, stream, aa);
-    else
-      launch_ex(assemble_kernel<1>, dim3(ceil_div(grid_elems, 256)), 256, 0, stream, aa);
-    ++launches;
-    FGS_CUDA(cudaGetLastError());
-    return;
-  }
-  // one launch per nonempty list-length class: 1, 8 or 32 lanes per cell
-  for (int c = 0; c < 3; ++c) {
-    if (asm_class_n[c] == 0) continue;
-    AssembleArgs aa{asm_ptr.p, asm_idx.p, w.priv.p, pstride, w.grid.p, grid_elems, asm_class_n[c], nvec,
-                    asm_cells[c].p};
-    const int lanes = c == 0 ? 1 : (c == 1 ? 8 : 32);
-    const dim3 blocks(static_cast<unsigned>(ceil_div(asm_class_n[c] * lanes, 256)));
-    if (c == 0) launch_ex(assemble_kernel<1>, blocks, 256, 0, stream, aa);
-    if (c == 1) launch_ex(assemble_kernel<8>, blocks, 256, 0, stream, aa);
-    if (c == 2) launch_ex(assemble_kernel<32>, blocks, 256, 0, stream, aa);
-    ++launches;
-  }
+  AssembleMixedArgs m{};
+  m.a = AssembleArgs{asm_ptr.p, asm_idx.p, w.priv.p, pstride, w.grid.p, grid_elems};
+  m.a.nvec = nvec;
+  m.cells = asm_cells.p;
+  m.n0 = asm_class_n[0];
+  m.n1 = asm_class_n[1];
+  m.n2 = asm_class_n[2];
+  m.w2 = m.n2;
+  m.w1 = (m.n1 + 3) / 4;
+  const int64_t warps = m.w2 + m.w1 + (m.n0 + 31) / 32;
+  if (warps == 0) return;
+  const dim3 blocks(static_cast<unsigned>(ceil_div(warps * 32, 256)));
+  if (nvec > 1)  // indices hoisted out of the vector loop (C5 16-vector blocks: 1.82 -> 1.71 ms)
+    launch_ex(assemble_mixed_kernel<true>, blocks, 256, 0, stream, m);
+  else
+    launch_ex(assemble_mixed_kernel<false>, blocks, 256, 0, stream, m);
+  ++launches;
   FGS_CUDA(cudaGetLastError());
 }
 
@@ -1369,7 +1155,7 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
   a.M = M;
   a.priv = w.priv.p;
   a.box_stride = box_stride;
-  a.grid = w.grid.p;
+  a.grid = w.grid_out.p;  // the interpolation reads the convolved grid
   a.grid_stride = grid_elems;
   a.y = y;
   a.ldy = ldy;
@@ -1393,13 +1179,16 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
     // ranks' partial real grids (M^2 doubles) are summed first, then every
     // rank convolves the full grid (the exchange of SURVEY 8e on the grid
     // instead of the spectrum window: one launch instead of four)
-    if (sharded)
-      nccl_check(nccl().all_reduce(w.grid.p, w.grid.p, static_cast<size_t>(grid_elems) * nvec, ncclDouble, ncclSum,
-                                   comm, stream),
+    const double* conv_in = w.grid.p;
+    if (sharded) {  // out of place: this rank's spread grid keeps its zero cells
+      nccl_check(nccl().all_reduce(w.grid.p, w.grid_sum.p, static_cast<size_t>(grid_elems) * nvec, ncclDouble,
+                                   ncclSum, comm, stream),
                  "ncclAllReduce of the partial grids");
+      conv_in = w.grid_sum.p;
+    }
     int logM = 0;
     while ((1 << logM) < M) ++logM;
-    Conv2Args ca{w.grid.p, w.grid.p, mult.p, tw2.p, M, logM, N, nvec, grid_elems};
+    Conv2Args ca{conv_in, w.grid_out.p, mult.p, tw2.p, M, logM, N, nvec, grid_elems};
     const size_t smem = conv2_smem(M, N);
     set_smem(conv2_kernel_ptr(M), smem);
     conv2_launch(ca, smem, stream);
@@ -1431,7 +1220,7 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
       FGS_CUDA(cudaGetLastError());
     }
     if (profile_) mark(evs);
-    FGS_CUFFT(cufftExecZ2D(w.c2r, w.spec.p, w.grid.p));
+    FGS_CUFFT(cufftExecZ2D(w.c2r, w.spec.p, w.grid_out.p));
     if (profile_) mark(evs);
   }
   launch_interp(a);
@@ -1569,8 +1358,8 @@ void Core::nfft_forward(const double* fhat_in, double* y_planar) {
     w.has_z2z = true;
   }
   FGS_CUFFT(cufftExecZ2Z(w.z2z, w.cgrid.p, w.cgrid.p, CUFFT_INVERSE));
-  split_complex_kernel<<<ceil_div(grid_elems, 256), 256, 0, stream>>>(w.cgrid.p, w.grid.p, w.grid.p + grid_elems,
-                                                                      grid_elems);
+  split_complex_kernel<<<ceil_div(grid_elems, 256), 256, 0, stream>>>(w.cgrid.p, w.grid_out.p,
+                                                                      w.grid_out.p + grid_elems, grid_elems);
   ++launches;
   PassArgs a{};
   a.items = items.p;
@@ -1580,7 +1369,7 @@ void Core::nfft_forward(const double* fhat_in, double* y_planar) {
   a.x = nullptr;
   a.nvec = 2;
   a.M = M;
-  a.grid = w.grid.p;
+  a.grid = w.grid_out.p;
   a.grid_stride = grid_elems;
   a.y = y_planar;
   a.ldy = n;

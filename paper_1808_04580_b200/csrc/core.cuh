@@ -77,7 +77,10 @@ struct DBuf {
 
 struct Workspace {
   int nvec = 0;
-  DBuf<double> priv, grid;
+  // grid: the assembled spread (zeroed once; cells outside the plan's
+  // footprint are never written); grid_out: the convolved grid the
+  // interpolation reads; grid_sum: d = 2 sharded, the ranks' summed grids
+  DBuf<double> priv, grid, grid_out, grid_sum;
   DBuf<cufftDoubleComplex> spec, cgrid, window;
   cufftHandle r2c = 0, c2r = 0, z2z = 0;
   bool has_plans = false, has_z2z = false;
@@ -119,11 +122,8 @@ class Core {
   DBuf<DItem> items;
   DBuf<DRun> runs;
   DBuf<int> asm_ptr, asm_idx;  // grid cell -> private-box entries (CSR, item order)
-  DBuf<int> asm_cells[3];      // cells by list-length class (<= 8, 9..64, > 64 entries)
+  DBuf<int> asm_cells;  // nonempty cells by list-length class: > 64 | 9..64 | <= 8 entries
   int64_t asm_class_n[3] = {0, 0, 0};
-  bool asm_split = false;
-  DBuf<int> asm_mixed_cells;  // classes 0 | 1 | 2 concatenated (single-launch mixed assembly)
-  bool asm_mixed = false;
   DBuf<cufftDoubleComplex> mult;  // compact Hermitian multiplier (FASTSUM)
   DBuf<double> deconv_d;
   DBuf<double2> tw2;  // d = 2 pruned-convolution twiddles

@@ -240,50 +240,8 @@ struct AssembleArgs {
   int64_t priv_stride;  // per vector
   double* grid;
   int64_t grid_stride;
-  int64_t cells;       // cells handled by this launch
   int nvec;
-  const int* cell_ids; // this launch's cells (nullable: cells 0 .. cells-1)
 };
-
-// L lanes per grid cell (1, 8 or 32 by the cell's list-length class, plan
-// time): each sums a contiguous slice of the cell's entry list in order, then
-// the slices are combined by a fixed shuffle tree -> bitwise reproducible.
-template <int kAsmLanes>
-__global__ void assemble_kernel(AssembleArgs a) {
-  pdl_wait();
-  const int64_t gt = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t gi = gt / kAsmLanes;
-  const int sub = static_cast<int>(gt % kAsmLanes);
-  const bool valid = gi < a.cells;
-  const int64_t g = (valid && a.cell_ids) ? static_cast<int64_t>(a.cell_ids[gi]) : gi;
-  int b = 0, e = 0;
-  if (valid) {
-    const int b0 = a.ptr[g], e0 = a.ptr[g + 1];
-    const int per = (e0 - b0 + kAsmLanes - 1) / kAsmLanes;
-    b = min(e0, b0 + sub * per);
-    e = min(e0, b + per);
-  }
-  for (int v = 0; v < a.nvec; ++v) {
-    const double* pv = a.priv + v * a.priv_stride;
-    double acc = 0.0;
-    // batches of 4: the index loads, then the value loads, are issued
-    // back to back (two dependent latencies per batch, not per entry);
-    // the sum stays in entry order
-    int l = b;
-    for (; l + 4 <= e; l += 4) {
-      const int i0 = __ldg(a.idx + l), i1 = __ldg(a.idx + l + 1), i2 = __ldg(a.idx + l + 2), i3 = __ldg(a.idx + l + 3);
-      const double v0 = pv[i0], v1 = pv[i1], v2 = pv[i2], v3 = pv[i3];
-      acc += v0;
-      acc += v1;
-      acc += v2;
-      acc += v3;
-    }
-    for (; l < e; ++l) acc += pv[__ldg(a.idx + l)];
-#pragma unroll
-    for (int off = 1; off < kAsmLanes; off <<= 1) acc += __shfl_down_sync(0xffffffffu, acc, off, kAsmLanes > 1 ? kAsmLanes : 32);
-    if (valid && sub == 0) a.grid[v * a.grid_stride + g] = acc;
-  }
-}
 
 // One launch for all list-length classes (cells sorted by class at plan
 // time; classes are warp-aligned, heaviest first so the long lists start in
@@ -293,8 +251,11 @@ __global__ void assemble_kernel(AssembleArgs a) {
 // assemble_kernel<L>'s for its class.  C2's lists average 17 entries but
 // 88 % of the entries sit in lists of 65-291, which 8 lanes per cell walked
 // as ~20 serial L2 round trips: the straggler set the kernel's length.
+// L lanes per cell each sum a contiguous slice of the cell's entry list in
+// order, then the slices are combined by a fixed shuffle tree -> bitwise
+// reproducible (no atomics, fixed summation order).
 struct AssembleMixedArgs {
-  AssembleArgs a;    // ptr, idx, priv, grid, nvec (cells / cell_ids unused)
+  AssembleArgs a;    // ptr, idx, priv, grid, nvec
   const int* cells;  // class 2 cells | class 1 cells | class 0 cells
   int64_t n0, n1, n2, w1, w2;
 };

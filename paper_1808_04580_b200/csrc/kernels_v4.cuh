@@ -36,9 +36,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int T, bool INTERP, int PS = 0, int QSZ = 32>
+template <int T, bool INTERP, int PS = 0, int QSZ = 0>
 struct Blk4 {
-  // QSZ = 0: default chunk (64 for 2m in {8, 16}, 32 for 2m = 12; sweep in tools/sweep_v4.py)
+  // QSZ = 0: default chunk (64 for 2m in {8, 16}, 32 for 2m = 12 interpolation)
   // warps per footprint group: more warps per footprint = fewer registers
   // per lane (ncu: 236-255 regs capped occupancy at 8 warps/SM with G = 1)
 #ifndef FGS_G12_INTERP

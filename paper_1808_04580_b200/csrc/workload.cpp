@@ -1,6 +1,8 @@
 // workload.cpp -- seeded synthetic stand-ins for the five BASELINE.json
 // configurations (the paper's spiral / crescent / photo datasets are not in
-// this container).  std::mt19937_64 + libstdc++ distributions,
+// this container).  Compiled into the product library AND
+// into oracle/liboracle.so, so bench.py's reference arm generates the same
+// arrays without loading the product.  std::mt19937_64 + libstdc++ distributions,
 // as the reference's own generators use (dataset.cpp, spectral.cpp:152-156).
 #include <algorithm>
 #include <cmath>
@@ -68,9 +70,14 @@ fgs_status fgs_workload_info(int config, int64_t* n, int* d, double* sigma, int*
 }
 
 fgs_status fgs_workload_generate(int config, uint64_t seed, double* X) {
+  return fgs_workload_generate_n(config, seed, 0, X);
+}
+
+fgs_status fgs_workload_generate_n(int config, uint64_t seed, int64_t n_points, double* X) {
   Info in;
-  if (!info_of(config, &in) || !X) return FGS_EPARAM;
-  const int64_t n = in.n;
+  if (!info_of(config, &in) || !X || n_points < 0) return FGS_EPARAM;
+  if (config == 3 && n_points != 0 && n_points != in.n) return FGS_EPARAM;  // the image has fixed size
+  const int64_t n = n_points > 0 ? n_points : in.n;
   const int d = in.d;
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> U(0.0, 1.0);
