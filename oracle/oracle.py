@@ -7,10 +7,12 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU baseline /
 reference arm may import this module, and only as the checker.  The product
 package ``paper_1808_04580_b200`` never imports it.
 
-Parity pin: see ``tests/test_oracle_*.py`` -- the oracle is checked against
-the reference's own known-answer tests (test_nfft.cpp, test_kernels.cpp,
+Parity pin: ``tests/test_ref_pin.py`` requires it to reproduce, bit for bit,
+the reference's own sources compiled against shim Eigen/FFTW headers
+(``oracle/_ref``, wrapped by ``oracle/ref.py``); ``tests/test_oracle_*.py``
+run the reference's known-answer tests (test_nfft.cpp, test_kernels.cpp,
 test_fastsum.cpp, test_graphop.cpp, test_spectral.cpp, acceptance.cpp) and
-its FFT against numpy.fft.
+check its FFT against numpy.fft.
 """
 from __future__ import annotations
 

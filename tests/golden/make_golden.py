@@ -1,11 +1,13 @@
-"""Generates tests/golden/golden.npz: small seeded inputs + outputs of the CPU
-oracle (oracle/, the C++ restatement of the reference path pinned by the
-reference's own known-answer tests -- see tests/test_oracle_*.py).
-
-The reference itself cannot be built or imported here (Eigen3/FFTW3 absent,
-DESIGN.md §2), so these fixtures freeze the pinned oracle's answers: the CPU
-suite checks the oracle still reproduces them bit-for-bit, the GPU suite
-checks the B200 path against them at the north-star tolerances.
+"""Generates tests/golden/golden.npz: small seeded inputs + the REFERENCE'S
+outputs on them.  The NFFT / graph-operator / Lanczos fixtures come from
+oracle/_ref/libfgsref.so -- the reference's own nfft.cpp, kernels.cpp,
+fastsum.cpp, graphop.cpp and spectral.cpp compiled unchanged against the
+shim Eigen/FFTW headers (oracle/build_ref.sh); inputs come from the oracle's
+seeded generators; the kernel-coefficient fixtures from the oracle (pinned
+bitwise to the reference by tests/test_ref_pin.py).  The CPU suite checks
+that both the oracle and the reference binary reproduce them bit for bit,
+the GPU suite checks the B200 path against them at the north-star
+tolerances.
 
     python tests/golden/make_golden.py
 """
@@ -17,12 +19,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 from oracle import oracle as orc  # noqa: E402
+from oracle import ref  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
 
 
 def main():
     orc.build()
+    if not ref.available():
+        raise SystemExit("oracle/_ref is not built: bash oracle/build_ref.sh")
     g = {}
     # NFFT (nfft.cpp), d = 1..3, m = 4 and 8
     for d in (1, 2, 3):
@@ -30,7 +35,7 @@ def main():
             n = 60 if d == 3 else 150
             nodes = orc.random_nodes(n, d, 10 * d + m)
             N = 8
-            plan = orc.NfftPlan(d, N, m, nodes)
+            plan = ref.NfftPlan(d, N, m, nodes)
             f = orc.random_coeffs(N ** d, 3 + d)
             x = orc.random_coeffs(n, 5 + d)
             key = f"nfft_d{d}_m{m}"
@@ -48,7 +53,7 @@ def main():
         dirs = rng.standard_normal((n, d))
         X = 0.2 * dirs / np.linalg.norm(dirs, axis=1)[:, None] * rng.uniform(0, 1, (n, 1)) ** (1.0 / d)
         x = rng.standard_normal(n)
-        op = orc.AdjacencyOperator(X, 0, sigma, N=N, m=m, p=m)
+        op = ref.AdjacencyOperator(X, 0, sigma, N=N, m=m, p=m)
         key = f"graph_d{d}"
         g[key + "_nodes"] = X
         g[key + "_x"] = x
