@@ -10,7 +10,9 @@
 //                        coefficients, kernel_error_estimate)
 //   graphop.hpp:45-97    AdjacencyOperator (degrees, apply_kernel/weight/normalized/
 //                        sym_laplacian)
-//   spectral.hpp:33-70   EigenPairs, LanczosOptions, LanczosInfo, lanczos_largest,
+//   spectral.hpp:18-30   SymmetricOperatorHandle, dense_handle, adjacency_handle,
+//                        laplacian_handle
+//   spectral.hpp:33-79   EigenPairs, LanczosOptions, LanczosInfo, lanczos_largest,
 //                        adjacency_to_laplacian, residual_norms, max_residual
 //   learn.hpp            KMeansOptions, KMeansResult, kmeans, spectral_cluster,
 //                        misclassification_rate(_permuted), kernel_ssl_solve,
@@ -18,17 +20,24 @@
 //   spectral.hpp:120-140 CgStatus, CgResult
 //   spectral.hpp:81-86   NystromOptions, nystrom_gaussian
 //   graphop.hpp:19-22    AdjacencyBackend {Fastsum, Direct}
-// Differences a caller sees: lanczos_largest takes the AdjacencyOperator itself
-// (the Krylov basis stays in HBM; the reference's std::function handle would
-// copy every vector through the host), and the vector types are Eigen's when
-// FGS_B200_WITH_EIGEN is defined, else the minimal column-major stand-ins
-// below (Eigen is not installed in this build image).
+// The reference's call sites compile unchanged, e.g. commands.cpp:179
+//   pairs = lanczos_largest(adjacency_handle(op), opts.k, lopts, &info);
+// A handle made by adjacency_handle / laplacian_handle remembers its device
+// operator, so lanczos_largest / residual_norms / nystrom_gaussian on it run
+// device-resident (Krylov basis in HBM, fgs_lanczos_largest); any other
+// handle (dense_handle, a user std::function) runs the device recurrence
+// with the caller's apply per step (fgs_lanczos_largest_operator).  The
+// vector types are Eigen's when FGS_B200_WITH_EIGEN is defined, else the
+// minimal column-major stand-ins below (Eigen is not installed in this build
+// image).
 #pragma once
 
 #include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <functional>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -358,6 +367,106 @@ struct LanczosInfo {
   bool converged = false;
 };
 
+/// spectral.hpp:18-22: a symmetric operator as a dimension and an apply
+/// function.  `device` / `which` are set by adjacency_handle /
+/// laplacian_handle (non-owning, as the reference's handles,
+/// spectral.hpp:28-30) and route the solvers to the device operator.
+struct SymmetricOperatorHandle {
+  Index dimension = 0;
+  std::function<VectorXd(const VectorXd&)> apply;
+  const AdjacencyOperator* device = nullptr;
+  int which = 0;  // 0: A = D^-1/2 W D^-1/2, 1: L_s = I - A
+};
+
+/// spectral.cpp:79-89: a dense symmetric matrix as an operator
+inline SymmetricOperatorHandle dense_handle(MatrixXd matrix) {
+  if (matrix.rows() != matrix.cols()) throw ShapeError("dense operator must be square");
+  auto shared = std::make_shared<MatrixXd>(std::move(matrix));
+  SymmetricOperatorHandle h;
+  h.dimension = shared->rows();
+  h.apply = [shared](const VectorXd& x) -> VectorXd {
+    const MatrixXd& a = *shared;
+    VectorXd y(a.rows());
+    for (Index i = 0; i < a.rows(); ++i) y(i) = 0.0;
+    for (Index j = 0; j < a.cols(); ++j)
+      for (Index i = 0; i < a.rows(); ++i) y(i) += a(i, j) * x(j);
+    return y;
+  };
+  return h;
+}
+
+/// spectral.cpp:91-96
+inline SymmetricOperatorHandle adjacency_handle(const AdjacencyOperator& op) {
+  SymmetricOperatorHandle h;
+  h.dimension = op.size();
+  h.apply = [&op](const VectorXd& x) { return op.apply_normalized(x); };
+  h.device = &op;
+  h.which = 0;
+  return h;
+}
+
+/// spectral.cpp:98-103
+inline SymmetricOperatorHandle laplacian_handle(const AdjacencyOperator& op) {
+  SymmetricOperatorHandle h;
+  h.dimension = op.size();
+  h.apply = [&op](const VectorXd& x) { return op.apply_sym_laplacian(x); };
+  h.device = &op;
+  h.which = 1;
+  return h;
+}
+
+namespace detail {
+inline EigenPairs pairs_from(Index n, int count, const std::vector<double>& vals, const MatrixXd& vecs,
+                             bool with_vectors) {
+  EigenPairs out;
+  out.values = VectorXd(count);
+  out.vectors = MatrixXd(with_vectors ? n : 0, count);
+  for (int i = 0; i < count; ++i) {
+    out.values(i) = vals[static_cast<size_t>(i)];
+    if (with_vectors)
+      for (Index r = 0; r < n; ++r) out.vectors(r, i) = vecs(r, i);
+  }
+  return out;
+}
+inline int apply_trampoline(void* ctx, const double* x, double* y, std::int64_t n) {
+  try {
+    const auto& h = *static_cast<const SymmetricOperatorHandle*>(ctx);
+    VectorXd xv(n);
+    for (std::int64_t i = 0; i < n; ++i) xv(i) = x[i];
+    const VectorXd yv = h.apply(xv);
+    if (yv.size() != n) return 1;
+    for (std::int64_t i = 0; i < n; ++i) y[i] = yv(i);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+}  // namespace detail
+
+/// spectral.cpp:141-256 on any handle: device-resident over the fast graph
+/// operator when the handle came from adjacency_handle / laplacian_handle,
+/// else the device recurrence with the handle's apply per step.
+inline EigenPairs lanczos_largest(const SymmetricOperatorHandle& op, int k, const LanczosOptions& opts = {},
+                                  LanczosInfo* info = nullptr, int device = 0) {
+  if (op.dimension < 1 || (!op.apply && !op.device)) throw ParameterError("operator handle is empty");
+  const Index n = op.dimension;
+  std::vector<double> vals(static_cast<size_t>(k > 0 ? k : 1));
+  MatrixXd vecs(n, k > 0 ? k : 1);
+  int count = 0, it = 0, conv = 0;
+  if (op.device)
+    detail::check(fgs_lanczos_largest(op.device->handle(), op.which, k, opts.max_iter, opts.tol, opts.seed,
+                                      vals.data(), vecs.data(), &count, &it, &conv));
+  else
+    detail::check(fgs_lanczos_largest_operator(n, &detail::apply_trampoline, const_cast<SymmetricOperatorHandle*>(&op),
+                                               device, k, opts.max_iter, opts.tol, opts.seed, vals.data(),
+                                               vecs.data(), &count, &it, &conv));
+  if (info) {
+    info->iterations = it;
+    info->converged = conv != 0;
+  }
+  return detail::pairs_from(n, count, vals, vecs, true);
+}
+
 /// k largest eigenpairs of A = D^-1/2 W D^-1/2 (what lanczos_largest(
 /// adjacency_handle(op), ...) computes in the reference, spectral.cpp:91-96).
 inline EigenPairs lanczos_largest(const AdjacencyOperator& op, int k, const LanczosOptions& opts = {},
@@ -424,6 +533,48 @@ inline double max_residual(const AdjacencyOperator& op, const EigenPairs& pairs)
   return m;
 }
 
+/// spectral.cpp:258-269 on any handle (device block apply for the graph
+/// operator's handles; the handle's apply per pair otherwise)
+inline VectorXd residual_norms(const SymmetricOperatorHandle& reference, const EigenPairs& pairs) {
+  if (reference.dimension < 1 || (!reference.apply && !reference.device))
+    throw ParameterError("operator handle is empty");
+  const Index n = reference.dimension, k = pairs.count();
+  if (k > 0 && pairs.vectors.rows() != n) throw ShapeError("eigenvector length does not match operator dimension");
+  VectorXd norms(k);
+  if (k == 0) return norms;
+  MatrixXd av(n, k);
+  if (reference.device) {
+    detail::check(fgs_adjacency_apply(reference.device->handle(),
+                                      reference.which == 0 ? FGS_OP_NORMALIZED : FGS_OP_SYM_LAPLACIAN,
+                                      pairs.vectors.data(), av.data(), static_cast<int>(k), n));
+  } else {
+    for (Index j = 0; j < k; ++j) {
+      VectorXd v(n);
+      for (Index i = 0; i < n; ++i) v(i) = pairs.vectors(i, j);
+      const VectorXd y = reference.apply(v);
+      if (y.size() != n) throw ShapeError("vector length does not match operator dimension");
+      for (Index i = 0; i < n; ++i) av(i, j) = y(i);
+    }
+  }
+  for (Index j = 0; j < k; ++j) {
+    double s = 0.0;
+    for (Index i = 0; i < n; ++i) {
+      const double r = av(i, j) - pairs.values(j) * pairs.vectors(i, j);
+      s += r * r;
+    }
+    norms(j) = std::sqrt(s);
+  }
+  return norms;
+}
+
+inline double max_residual(const SymmetricOperatorHandle& reference, const EigenPairs& pairs) {
+  if (pairs.count() == 0) return 0.0;
+  VectorXd r = residual_norms(reference, pairs);
+  double m = r(0);
+  for (Index j = 1; j < r.size(); ++j) m = std::max(m, r(j));
+  return m;
+}
+
 // ---- spectral.hpp:81-86 Nystrom (spectral.cpp:384-444) ---------------------
 struct NystromOptions {
   int k = 10;
@@ -447,6 +598,14 @@ inline EigenPairs nystrom_gaussian(const AdjacencyOperator& op, const NystromOpt
     for (Index r = 0; r < n; ++r) out.vectors(r, i) = vecs(r, i);
   }
   return out;
+}
+
+/// nystrom_gaussian(adjacency_handle(op), opts) as the reference's CLI calls it
+/// (commands.cpp:207): device block applies of the graph operator
+inline EigenPairs nystrom_gaussian(const SymmetricOperatorHandle& op, const NystromOptions& opts) {
+  if (!op.device || op.which != 0)
+    throw ParameterError("nystrom_gaussian runs on adjacency_handle(op) of a device AdjacencyOperator");
+  return nystrom_gaussian(*op.device, opts);
 }
 
 // ---- spectral.hpp:120-140 CG, learn.hpp SSL / ridge (learn.cpp:364-445) ----

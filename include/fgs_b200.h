@@ -156,6 +156,11 @@ fgs_status fgs_adjacency_profile_read(fgs_adjacency_t h, double* ms6, int64_t* a
  * counts. */
 fgs_status fgs_adjacency_geometry(fgs_adjacency_t h, int* d, int* N, int* M, int* taps, int* items,
                                   int64_t* box_stride);
+/* Which spread / interpolation kernels the plan runs (instrumentation for
+ * the parity tests): points per run (nonempty cell piece), and 1 when the
+ * fp64 tensor-core (DMMA) spread / interpolation is used, 0 for the scalar
+ * kernels. */
+fgs_status fgs_adjacency_plan_stats(fgs_adjacency_t h, double* mean_run, int* tensor_spread, int* tensor_interp);
 /* fp64 FMA-pipe peak of `device` in TFLOP/s (independent DFMA chains, CUDA
  * events), the denominator of the spread/interp roofline. */
 fgs_status fgs_measure_fp64_peak(int device, double* tflops);
@@ -175,6 +180,19 @@ void fgs_adjacency_destroy(fgs_adjacency_t h);
 fgs_status fgs_lanczos_largest(fgs_adjacency_t h, int which, int k, int max_iter, double tol,
                                uint64_t seed, double* values, double* vectors, int* count,
                                int* iterations, int* converged);
+
+/* lanczos_largest over a generic symmetric operator: the reference's
+ * SymmetricOperatorHandle {dimension, std::function apply} (spectral.hpp:
+ * 18-30; dense_handle, user operators).  `apply(ctx, x, y, n)` writes y = A x
+ * for host vectors of length n and returns 0 (nonzero aborts with
+ * FGS_ENUMERIC).  The recurrence and both Gram-Schmidt passes run on
+ * `device` (basis in HBM); q_m and A q_m cross to/from the host once per
+ * step.  Same outputs as fgs_lanczos_largest (values descending, vectors
+ * n x count column-major, sign-normalised; vectors may be NULL). */
+typedef int (*fgs_operator_apply)(void* ctx, const double* x, double* y, int64_t n);
+fgs_status fgs_lanczos_largest_operator(int64_t n, fgs_operator_apply apply, void* ctx, int device, int k,
+                                        int max_iter, double tol, uint64_t seed, double* values, double* vectors,
+                                        int* count, int* iterations, int* converged);
 
 /* Device milliseconds of the last fgs_lanczos_largest on this handle spent in
  * operator applies and in reorthogonalisation, the host wall time of its

@@ -42,6 +42,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "linalg.hpp"
@@ -66,6 +67,36 @@ struct Error : std::runtime_error {
   Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+// Host threads of the NFFT loops (orc_set_threads; default 1 = the serial
+// reference order, which tests/test_ref_pin.py pins bit for bit).  With more
+// threads the taps and the gather are split over points (results unchanged)
+// and the spread goes into per-thread grids summed in thread order (a fixed
+// order, but a different rounding of the grid sums than the serial loop):
+// used only to make full-size GPU parity checks (C4/C5) affordable.
+int g_threads = 1;
+
+template <class F>
+void parallel_ranges(int64_t n, F&& fn) {  // fn(thread, lo, hi)
+  const int T = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g_threads, n / 1024)));
+  if (T <= 1) {
+    fn(0, int64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs(static_cast<size_t>(T));
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        fn(t, n * t / T, n * (t + 1) / T);
+      } catch (...) {
+        errs[static_cast<size_t>(t)] = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
 
 size_t ipow(size_t base, int e) {  // nfft.cpp:53-57
   size_t r = 1;
@@ -185,17 +216,19 @@ struct Nfft {
     taps = 2 * m;  // nfft.cpp:356-369
     w.resize(static_cast<size_t>(n) * d * taps);
     idx.resize(static_cast<size_t>(n) * d * taps);
-    for (int64_t j = 0; j < n; ++j)
-      for (int t = 0; t < d; ++t) {
-        double v = nodes(j, t);
-        int u0 = static_cast<int>(std::ceil(v * M - m));
-        size_t base = (static_cast<size_t>(j) * d + t) * taps;
-        for (int a = 0; a < taps; ++a) {
-          int u = u0 + a;
-          w[base + a] = window(v - static_cast<double>(u) / M);
-          idx[base + a] = ((u % M) + M) % M;
+    parallel_ranges(n, [&](int, int64_t lo, int64_t hi) {
+      for (int64_t j = lo; j < hi; ++j)
+        for (int t = 0; t < d; ++t) {
+          double v = nodes(j, t);
+          int u0 = static_cast<int>(std::ceil(v * M - m));
+          size_t base = (static_cast<size_t>(j) * d + t) * taps;
+          for (int a = 0; a < taps; ++a) {
+            int u = u0 + a;
+            w[base + a] = window(v - static_cast<double>(u) / M);
+            idx[base + a] = ((u % M) + M) % M;
+          }
         }
-      }
+    });
     grid_in.assign(grid_total, 0.0);
     grid_out.assign(grid_total, 0.0);
   }
@@ -306,18 +339,31 @@ struct Nfft {
     if (fhat.size() != coeff_total) fail(S_SHAPE, "coefficient vector has wrong length");
     place_coefficients(fhat, grid_in.data());
     grid_out = grid_in;
-    fft_nd(grid_out.data(), d, M, +1);  // FFTW_BACKWARD
+    fft_nd(grid_out.data(), d, M, +1, g_threads);  // FFTW_BACKWARD
     std::vector<cd> result(static_cast<size_t>(n));
-    for (int64_t j = 0; j < n; ++j) result[static_cast<size_t>(j)] = gather(grid_out.data(), j);
+    parallel_ranges(n, [&](int, int64_t lo, int64_t hi) {
+      for (int64_t j = lo; j < hi; ++j) result[static_cast<size_t>(j)] = gather(grid_out.data(), j);
+    });
     return result;
   }
 
   std::vector<cd> adjoint(const std::vector<cd>& x) const {  // nfft.cpp:415-427
     if (static_cast<int64_t>(x.size()) != n) fail(S_SHAPE, "input vector length does not match node count");
     std::fill(grid_in.begin(), grid_in.end(), cd(0.0));
-    for (int64_t j = 0; j < n; ++j) spread(x[static_cast<size_t>(j)], j, grid_in.data());
+    if (g_threads <= 1 || n < 2048) {
+      for (int64_t j = 0; j < n; ++j) spread(x[static_cast<size_t>(j)], j, grid_in.data());
+    } else {
+      std::vector<std::vector<cd>> part(static_cast<size_t>(g_threads));
+      parallel_ranges(n, [&](int t, int64_t lo, int64_t hi) {
+        part[static_cast<size_t>(t)].assign(grid_total, cd(0.0));
+        for (int64_t j = lo; j < hi; ++j) spread(x[static_cast<size_t>(j)], j, part[static_cast<size_t>(t)].data());
+      });
+      for (auto& g : part)
+        if (!g.empty())
+          for (size_t i = 0; i < grid_total; ++i) grid_in[i] += g[i];
+    }
     grid_out = grid_in;
-    fft_nd(grid_out.data(), d, M, -1);  // FFTW_FORWARD
+    fft_nd(grid_out.data(), d, M, -1, g_threads);  // FFTW_FORWARD
     std::vector<cd> result;
     extract_coefficients(grid_out.data(), result);
     return result;
@@ -1332,6 +1378,13 @@ using namespace orc;
 extern "C" {
 
 const char* orc_last_error(void) { return g_last_error.c_str(); }
+
+// host threads of the NFFT loops (see g_threads); returns the previous value
+int orc_set_threads(int threads) {
+  const int old = g_threads;
+  g_threads = std::max(1, threads);
+  return old;
+}
 
 double orc_bessel_i0(double x) { return bessel_i0(x); }
 double orc_std_bessel_i0(double x) { return std::cyl_bessel_i(0.0, x); }

@@ -25,6 +25,7 @@
 #include <limits>
 #include <numbers>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 namespace orc_linalg {
@@ -101,19 +102,32 @@ inline void fft_line(cd* x, int n, int sign) {
 
 // d-dimensional transform of a row-major M^d array (dimension 0 slowest),
 // the layout FFTW's fftw_plan_dft(d, {M,M,M}, ...) uses.
-inline void fft_nd(cd* data, int d, int M, int sign) {
+inline void fft_nd(cd* data, int d, int M, int sign, int threads = 1) {
+  // every line is transformed by the same serial code, so splitting the
+  // lines over threads leaves the result bit for bit unchanged
   size_t total = ipow(static_cast<size_t>(M), d);
-  std::vector<cd> line(static_cast<size_t>(M));
   for (int t = 0; t < d; ++t) {
-    size_t stride = ipow(static_cast<size_t>(M), d - 1 - t);
-    size_t outer = total / (stride * M);
-    for (size_t o = 0; o < outer; ++o)
-      for (size_t s = 0; s < stride; ++s) {
+    const size_t stride = ipow(static_cast<size_t>(M), d - 1 - t);
+    const size_t outer = total / (stride * M);
+    const size_t lines = outer * stride;
+    auto run = [&](size_t lo, size_t hi) {
+      std::vector<cd> line(static_cast<size_t>(M));
+      for (size_t l = lo; l < hi; ++l) {
+        const size_t o = l / stride, s = l % stride;
         cd* base = data + o * stride * M + s;
         for (int k = 0; k < M; ++k) line[static_cast<size_t>(k)] = base[k * stride];
         fft_line(line.data(), M, sign);
         for (int k = 0; k < M; ++k) base[k * stride] = line[static_cast<size_t>(k)];
       }
+    };
+    const int T = static_cast<int>(std::min<size_t>(std::max(threads, 1), lines / 64 + 1));
+    if (T <= 1) {
+      run(0, lines);
+    } else {
+      std::vector<std::thread> pool;
+      for (int q = 0; q < T; ++q) pool.emplace_back(run, lines * q / T, lines * (q + 1) / T);
+      for (auto& th : pool) th.join();
+    }
   }
 }
 

@@ -98,6 +98,26 @@ def _cplx_in(v) -> np.ndarray:
     return v.view(np.float64)
 
 
+def set_threads(threads: int) -> int:
+    """Host threads of the oracle's NFFT loops (1 = the serial reference
+    order, pinned bitwise to oracle/_ref); returns the previous setting."""
+    return lib().orc_set_threads(int(threads))
+
+
+class threads:
+    """with orc.threads(n): ... -- temporarily parallel oracle NFFT loops."""
+
+    def __init__(self, n):
+        self.n = n
+
+    def __enter__(self):
+        self.old = set_threads(self.n)
+        return self
+
+    def __exit__(self, *exc):
+        set_threads(self.old)
+
+
 def bessel_i0(x: float) -> float:
     return lib().orc_bessel_i0(C.c_double(x))
 

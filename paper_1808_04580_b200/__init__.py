@@ -416,6 +416,12 @@ class AdjacencyOperator:
                                             C.byref(items), C.byref(bs)))
         return dict(d=d.value, N=N.value, M=M.value, taps=T.value, items=items.value, box_stride=bs.value)
 
+    def plan_stats(self) -> dict:
+        """mean points per run and whether the DMMA spread / interpolation run."""
+        mr, ts, ti = C.c_double(), C.c_int(), C.c_int()
+        _check(lib().fgs_adjacency_plan_stats(self._h, C.byref(mr), C.byref(ts), C.byref(ti)))
+        return dict(mean_run=mr.value, tensor_spread=bool(ts.value), tensor_interp=bool(ti.value))
+
     def lanczos_stats(self) -> dict:
         out = np.zeros(4)
         _check(lib().fgs_lanczos_stats(self._h, _dp(out)))

@@ -464,6 +464,16 @@ fgs_status fgs_adjacency_geometry(fgs_adjacency_t h, int* d, int* N, int* M, int
   });
 }
 
+fgs_status fgs_adjacency_plan_stats(fgs_adjacency_t h, double* mean_run, int* tensor_spread, int* tensor_interp) {
+  return guard([&] {
+    need(h, "handle");
+    const Core& c = *h->core;
+    if (mean_run) *mean_run = c.mean_run;
+    if (tensor_spread) *tensor_spread = c.tensor_spread() ? 1 : 0;
+    if (tensor_interp) *tensor_interp = c.tensor_interp() ? 1 : 0;
+  });
+}
+
 fgs_status fgs_measure_fp64_peak(int device, double* tflops) {
   return guard([&] {
     need(tflops, "tflops");
@@ -518,6 +528,16 @@ fgs_status fgs_lanczos_largest(fgs_adjacency_t h, int which, int k, int max_iter
     if (count) *count = cnt;
     if (iterations) *iterations = r.iterations;
     if (converged) *converged = r.converged ? 1 : 0;
+  });
+}
+
+fgs_status fgs_lanczos_largest_operator(int64_t n, fgs_operator_apply apply, void* ctx, int device, int k,
+                                        int max_iter, double tol, uint64_t seed, double* values, double* vectors,
+                                        int* count, int* iterations, int* converged) {
+  return guard([&] {
+    need(values, "values");
+    fgsb::lanczos_operator(n, apply, ctx, device, k, max_iter, tol, seed, values, vectors, count, iterations,
+                           converged);
   });
 }
 

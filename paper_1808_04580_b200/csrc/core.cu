@@ -966,6 +966,11 @@ size_t Core::smem_bytes(bool interp) const {
   return (boxes + (interp ? sh.extra_interp : sh.extra_spread)) * sizeof(double);
 }
 
+bool Core::tensor_spread() const {
+  return kind != DIRECT && (d == 2 || d == 3) && (T == 8 || T == 12 || T == 16) && mean_run >= kDenseRun;
+}
+bool Core::tensor_interp() const { return kind != DIRECT && (d == 2 || d == 3) && (T == 8 || T == 12 || T == 16); }
+
 void Core::launch_spread(const PassArgs& a) {
   if (nitems == 0) return;
   const size_t smem = smem_bytes(false);

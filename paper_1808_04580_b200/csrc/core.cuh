@@ -131,6 +131,8 @@ class Core {
   bool use_conv2d() const;
   int nitems = 0;
   double mean_run = 0.0;  // points per run (cell piece) of this shard: picks the spread kernel
+  bool tensor_spread() const;  // the DMMA spread runs (dense runs, 2m in {8, 12, 16}, d in {2, 3})
+  bool tensor_interp() const;
   int64_t box_stride = 0;
   int64_t grid_elems = 0, spec_elems = 0, window_elems = 0;
   std::vector<int> host_perm;

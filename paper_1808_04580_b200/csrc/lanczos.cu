@@ -836,6 +836,206 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   return res;
 }
 
+namespace {
+__global__ void div_scalar_kernel(const double* __restrict__ z, double beta, double* __restrict__ out, int64_t n) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r < n) out[r] = z[r] / beta;  // basis.col(m) = z / beta (spectral.cpp:227)
+}
+}  // namespace
+
+// lanczos_largest over a generic symmetric operator given as a host callback
+// (the reference's SymmetricOperatorHandle, spectral.hpp:18-30: dense_handle,
+// user operators).  The recurrence runs on the device -- basis in HBM,
+// alpha, the three-term update, both classical Gram-Schmidt passes and beta
+// by the same fixed-order kernels as lanczos_device -- and each step moves
+// q_m to the host for the caller's apply and z back.  Control flow, start
+// vector, convergence schedule, breakdown restart and Ritz conventions are
+// spectral.cpp:141-256's; q_{m+1} = z / beta by division as the reference.
+void lanczos_operator(int64_t n, OperatorApply apply, void* ctx, int device, int k, int max_iter, double tol,
+                      uint64_t seed, double* values, double* vectors, int* count, int* iterations, int* converged) {
+  if (n < 1 || apply == nullptr) fail(FGS_EPARAM, "operator handle is empty");
+  if (k < 1) fail(FGS_EPARAM, "at least one eigenpair must be requested");
+  if (k > n) fail(FGS_EPARAM, "requested pairs must not exceed the operator dimension");
+  if (max_iter < 1) fail(FGS_EPARAM, "max_iter must be positive");
+  if (!(tol > 0.0)) fail(FGS_EPARAM, "tolerance must be positive");
+  const double kEps = std::numeric_limits<double>::epsilon();
+  FGS_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  FGS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } guard{st};
+
+  std::mt19937_64 rng(seed);  // spectral.cpp:152-156
+  std::uniform_real_distribution<double> unif(-1.0, 1.0);
+  std::vector<double> hx(static_cast<size_t>(n)), hy(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) hx[static_cast<size_t>(i)] = unif(rng);
+  double sn = 0.0;
+  for (double v : hx) sn += v * v;
+  sn = std::sqrt(sn);
+  for (double& v : hx) v /= sn;  // start.normalize()
+
+  int64_t cap = std::min<int64_t>(n, 64);
+  const int64_t amax = std::min<int64_t>(n, max_iter) + 2;
+  const int nblk = std::max(1, ceil_div(n, kRowsPerBlock));
+  const int gsz = ceil_div(n, 256);
+  DBuf<double> basis, z, hbuf, partial, dalpha, dbeta, dnrm;
+  basis.alloc(static_cast<size_t>(n) * cap);
+  z.alloc(static_cast<size_t>(n));
+  hbuf.alloc(static_cast<size_t>(amax));
+  partial.alloc(static_cast<size_t>(nblk) * amax);
+  dalpha.alloc(static_cast<size_t>(amax));
+  dbeta.alloc(static_cast<size_t>(amax));
+  dnrm.alloc(static_cast<size_t>(amax));
+  FGS_CUDA(cudaMemcpyAsync(basis.p, hx.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+
+  auto multidot = [&](const double* Q, int m, const double* v, double* out) {
+    multidot_kernel<<<nblk, kRedThreads, 0, st>>>(Q, n, m, v, n, partial.p);
+    reduce_partials_kernel<<<ceil_div(m, 8), 256, 0, st>>>(partial.p, nblk, m, out, 0);
+  };
+  auto cgs_pass = [&](int m, double* v) {  // v -= Q (Q^T v)
+    multidot(basis.p, m, v, hbuf.p);
+    update_kernel<<<gsz, 256, sizeof(double) * m, st>>>(basis.p, n, m, hbuf.p, v, n);
+  };
+  auto host_scalar = [&](const double* d) {
+    double h = 0.0;
+    FGS_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, st));
+    FGS_CUDA(cudaStreamSynchronize(st));
+    return h;
+  };
+
+  std::vector<double> alphas, betas, tvals, tvecs;
+  int tri_size = 0, iters = 0, next_check = k;
+  double scale = 0.0;
+  bool conv = false;
+  auto solve_tri = [&](int m) {
+    tvals.assign(alphas.begin(), alphas.begin() + m);
+    std::vector<double> sub(betas.begin(), betas.begin() + (m - 1));
+    tridiagonal_eigen(m, tvals, sub, tvecs);
+    tri_size = m;
+  };
+  while (true) {
+    const int m = static_cast<int>(alphas.size()) + 1;
+    const double* qcur = basis.p + static_cast<int64_t>(m - 1) * n;
+    FGS_CUDA(cudaMemcpyAsync(hx.data(), qcur, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    FGS_CUDA(cudaStreamSynchronize(st));
+    if (apply(ctx, hx.data(), hy.data(), n) != 0) fail(FGS_ENUMERIC, "operator apply callback failed");
+    FGS_CUDA(cudaMemcpyAsync(z.p, hy.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    ++iters;
+    multidot(qcur, 1, z.p, dalpha.p + (m - 1));  // alpha = q_m . z
+    three_term_kernel<<<gsz, 256, 0, st>>>(z.p, qcur, m >= 2 ? qcur - n : nullptr, dalpha.p + (m - 1),
+                                           m >= 2 ? dbeta.p + (m - 2) : dbeta.p, n);
+    cgs_pass(m, z.p);  // full reorthogonalisation, twice (spectral.cpp:193-195)
+    cgs_pass(m, z.p);
+    multidot(z.p, 1, z.p, dnrm.p + (m - 1));
+    const double alpha = host_scalar(dalpha.p + (m - 1));
+    const double beta = std::sqrt(host_scalar(dnrm.p + (m - 1)));
+    const double beta_prev = m >= 2 ? betas[static_cast<size_t>(m - 2)] : 0.0;
+    alphas.push_back(alpha);
+    scale = std::max(scale, std::abs(alpha) + beta + beta_prev);
+    const bool last = iters >= max_iter || m == static_cast<int>(n);
+    if (m >= k && (m >= next_check || last)) {  // spectral.cpp:200-215
+      solve_tri(m);
+      bool all_small = true;
+      for (int i = 0; i < k && all_small; ++i) {
+        const double theta = tvals[static_cast<size_t>(m - 1 - i)];
+        const double est = beta * std::abs(tvecs[static_cast<size_t>(m - 1 - i) * m + (m - 1)]);
+        if (est > tol * std::max(std::abs(theta), kEps * std::max(scale, 1.0))) all_small = false;
+      }
+      if (all_small) {
+        conv = true;
+        break;
+      }
+      next_check = m + std::max(8, m / 8);
+    }
+    if (iters >= max_iter) break;
+    if (m == static_cast<int>(n)) {
+      conv = true;
+      break;
+    }
+    if (m == cap) {  // basis.conservativeResize(NoChange, min(n, 2 cap))
+      const int64_t ncap = std::min<int64_t>(n, cap * 2);
+      DBuf<double> nb;
+      nb.alloc(static_cast<size_t>(n) * ncap);
+      FGS_CUDA(cudaMemcpyAsync(nb.p, basis.p, sizeof(double) * n * cap, cudaMemcpyDeviceToDevice, st));
+      FGS_CUDA(cudaStreamSynchronize(st));
+      std::swap(basis.p, nb.p);
+      std::swap(basis.n, nb.n);
+      cap = ncap;
+    }
+    double* qnext = basis.p + static_cast<int64_t>(m) * n;
+    if (beta > 1e-14 * std::max(scale, 1.0)) {
+      betas.push_back(beta);
+      FGS_CUDA(cudaMemcpyAsync(dbeta.p + (m - 1), &betas.back(), sizeof(double), cudaMemcpyHostToDevice, st));
+      div_scalar_kernel<<<gsz, 256, 0, st>>>(z.p, beta, qnext, n);
+    } else {  // breakdown (spectral.cpp:59-75, 225-238)
+      bool found = false;
+      for (int attempt = 0; attempt < 8 && !found; ++attempt) {
+        for (int64_t i = 0; i < n; ++i) hx[static_cast<size_t>(i)] = unif(rng);
+        FGS_CUDA(cudaMemcpyAsync(z.p, hx.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        cgs_pass(m, z.p);
+        cgs_pass(m, z.p);
+        multidot(z.p, 1, z.p, hbuf.p);
+        const double nv = std::sqrt(host_scalar(hbuf.p));
+        if (nv > 1e-8) {
+          div_scalar_kernel<<<gsz, 256, 0, st>>>(z.p, nv, qnext, n);
+          found = true;
+        }
+      }
+      if (!found) {
+        conv = true;
+        break;
+      }
+      betas.push_back(0.0);
+      FGS_CUDA(cudaMemcpyAsync(dbeta.p + (m - 1), &betas.back(), sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    FGS_CUDA(cudaGetLastError());
+  }
+  const int m = static_cast<int>(alphas.size());
+  if (tri_size != m) solve_tri(m);
+  const int wanted = std::min(k, m);
+  std::vector<double> vals(static_cast<size_t>(wanted)), S(static_cast<size_t>(m) * wanted);
+  for (int i = 0; i < wanted; ++i) {
+    vals[static_cast<size_t>(i)] = tvals[static_cast<size_t>(m - 1 - i)];
+    for (int j = 0; j < m; ++j) S[static_cast<size_t>(j) * wanted + i] = tvecs[static_cast<size_t>(m - 1 - i) * m + j];
+  }
+  std::vector<double> V;
+  if (vectors) {  // V = Q_m S on the device (spectral.cpp:250)
+    DBuf<double> dS, dV;
+    dS.upload(S.data(), S.size(), st);
+    dV.alloc(static_cast<size_t>(n) * wanted);
+    for (int c0 = 0; c0 < wanted; c0 += 8)
+      ritz_kernel<8><<<ceil_div(n, 128), 128, 0, st>>>(basis.p, n, m, dS.p, wanted, c0, dV.p, n, n);
+    V.resize(static_cast<size_t>(n) * wanted);
+    FGS_CUDA(cudaMemcpyAsync(V.data(), dV.p, sizeof(double) * V.size(), cudaMemcpyDeviceToHost, st));
+    FGS_CUDA(cudaStreamSynchronize(st));
+  }
+  FGS_CUDA(cudaGetLastError());
+  // make_eigenpairs (spectral.cpp:105-127)
+  std::vector<int> order(static_cast<size_t>(wanted));
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return vals[static_cast<size_t>(a)] > vals[static_cast<size_t>(b)]; });
+  for (int i = 0; i < wanted; ++i) {
+    const int src = order[static_cast<size_t>(i)];
+    values[i] = vals[static_cast<size_t>(src)];
+    if (vectors) {
+      const double* col = V.data() + static_cast<size_t>(src) * n;
+      int64_t at = 0;
+      for (int64_t r = 1; r < n; ++r)
+        if (std::abs(col[r]) > std::abs(col[at])) at = r;
+      const double sg = col[at] < 0.0 ? -1.0 : 1.0;
+      for (int64_t r = 0; r < n; ++r) vectors[static_cast<size_t>(i) * n + r] = sg * col[r];
+    }
+  }
+  if (count) *count = wanted;
+  if (iterations) *iterations = iters;
+  if (converged) *converged = conv ? 1 : 0;
+}
+
 void lanczos_finish_vectors(Core& c, LanczosResult& r, const std::vector<int>& order, double* host_out) {
   const int64_t n = c.n;
   const int cnt = static_cast<int>(order.size());

@@ -21,5 +21,9 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
 // `order`, copied to host_out (n x order.size(), column-major)
 void lanczos_finish_vectors(Core& c, LanczosResult& r, const std::vector<int>& order, double* host_out);
 void tridiagonal_eigen(int m, std::vector<double>& diag, const std::vector<double>& offd, std::vector<double>& z);
+// lanczos_largest over a host-callback operator (SymmetricOperatorHandle)
+using OperatorApply = int (*)(void* ctx, const double* x, double* y, int64_t n);
+void lanczos_operator(int64_t n, OperatorApply apply, void* ctx, int device, int k, int max_iter, double tol,
+                      uint64_t seed, double* values, double* vectors, int* count, int* iterations, int* converged);
 
 }  // namespace fgsb

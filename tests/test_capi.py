@@ -87,3 +87,13 @@ def test_cpp_dropin_layer_compiles_against_the_header():
     import __graft_entry__ as g
     exe = g.build_cpp_dropin_test()
     assert os.path.exists(exe)
+
+
+@pytest.mark.parametrize("eigen", [False, True])
+def test_cpp_dropin_header_builds(eigen):
+    # include/fgs/b200.hpp with the reference's solve_pairs call site
+    # (commands.cpp:171-188) compiles and links, in its plain and its
+    # Eigen-typed mode (the latter against oracle/shim's Eigen stand-in)
+    import __graft_entry__ as g
+    exe = g.build_cpp_dropin_test(eigen=eigen)
+    assert os.path.exists(exe)

@@ -252,11 +252,14 @@ def test_lanczos_laplacian_handle_and_reproducibility(orc):
     assert np.max(np.abs(lp.values - lv)) <= 1e-8 * np.max(np.abs(lv))
 
 
-def test_cpp_dropin_program_passes():
-    # the reference's test cases written against include/fgs/b200.hpp
+@pytest.mark.parametrize("eigen", [False, True])
+def test_cpp_dropin_program_passes(eigen):
+    # the reference's test cases and its CLI's solve_pairs call site
+    # (commands.cpp:171-188, verbatim) written against include/fgs/b200.hpp;
+    # eigen=True: the header's Eigen-typed mode
     import subprocess
     import __graft_entry__ as g
-    exe = g.build_cpp_dropin_test()
+    exe = g.build_cpp_dropin_test(eigen=eigen)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
 
