@@ -15,8 +15,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libfgs_b200.so")
-OBJ = os.path.join(ROOT, "build", "obj")
+# FGS_BUILD_TAG=x (tuning builds with FGS_NVCC_DEFINES): libfgs_b200_x.so
+# from build/obj_x, loaded by tools/variant_bench.py; never the product path
+_TAG = os.environ.get("FGS_BUILD_TAG", "")
+OUT = os.path.join(HERE, f"libfgs_b200_{_TAG}.so" if _TAG else "libfgs_b200.so")
+OBJ = os.path.join(ROOT, "build", f"obj_{_TAG}" if _TAG else "obj")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
@@ -50,7 +53,8 @@ def _compile(src: str, verbose: bool) -> str:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _deps():
-        build_cli(verbose)
+        if not _TAG:
+            build_cli(verbose)
         return OUT
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
@@ -60,7 +64,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.run(link, check=True)
-    build_cli(verbose)
+    if not _TAG:
+        build_cli(verbose)
     return OUT
 
 

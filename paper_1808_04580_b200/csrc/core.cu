@@ -17,6 +17,7 @@
 #include "kernels.cuh"
 #include "kernels_v2.cuh"
 #include "kernels_v4.cuh"
+#include "kernels_v5.cuh"
 #include "conv2d.cuh"
 #include "direct.cuh"
 #include "nccl_shim.hpp"
@@ -194,6 +195,12 @@ constexpr bool has_v4_2d() {
 // d = 2 tensor-core kernels: point-stream warps per CTA (interpolation 2:
 // C2 22.8 k vs 22.2 k with 4, 21.7 k with 1; spread 1)
 constexpr int kInterp2dP = 2;
+// d = 3 interpolation: per-warp point batches with B fragments from the box
+// (kernels_v5.cuh); FGS_INTERP_V5=0 builds the v4 register-resident kernel
+#ifndef FGS_INTERP_V5
+#define FGS_INTERP_V5 1
+#endif
+constexpr bool kInterpV5 = FGS_INTERP_V5 != 0;
 constexpr int kSpread2dP = 1;
 // staged input window (Blk4d2::XW) of the d = 2 variant with P streams
 constexpr size_t xw2d(int p) { return static_cast<size_t>(p * 32 > 64 ? p * 32 : 64); }
@@ -229,7 +236,7 @@ LaunchShape shape_t(bool dense) {
   size_t interp = base + 2 * static_cast<size_t>(B::NT / 32) * B::QB;
   size_t spread = base;
   if constexpr (has_v4_3d<D, T>()) {
-    interp = v4_stage_doubles<T, true>();
+    interp = kInterpV5 ? v5_extra_doubles<T>() : v4_stage_doubles<T, true>();
     if (dense) spread = v4_stage_doubles<T, false>();
   }
   if constexpr (has_v4_2d<D, T>()) {
@@ -265,7 +272,8 @@ void launch_smem(K k, int nitems, int nt, size_t smem, cudaStream_t s, Args... a
 }
 
 template <int D, int T>
-void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t smem, int box_stride, cudaStream_t s) {
+void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t smem, int box_stride, int box_pad_arg,
+              cudaStream_t s) {
   if constexpr (has_v4_2d<D, T>()) {
     if (interp)
       return launch_smem(interp_v4_2d_kernel<T, kInterp2dP>, nitems, Blk4d2<T, kInterp2dP>::NT, smem, s, a, box_stride);
@@ -273,6 +281,8 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
       return launch_smem(spread_v4_2d_kernel<T, kSpread2dP>, nitems, Blk4d2<T, kSpread2dP>::NT, smem, s, a, box_stride);
   }
   if constexpr (has_v4_3d<D, T>()) {
+    if (interp && kInterpV5)
+      return launch_smem(interp_v5_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
     if (interp) {
       // one warp per footprint: partials combined per chunk only on large
       // plans (C3 +7 %, C1 -5 %); G > 1 always combines per chunk
@@ -290,17 +300,17 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
 }
 
 template <int D>
-void dispatch(bool interp, bool dense, int T, const PassArgs& a, int nitems, size_t smem, int box_stride,
+void dispatch(bool interp, bool dense, int T, const PassArgs& a, int nitems, size_t smem, int box_stride, int box_pad,
               cudaStream_t s) {
   switch (T) {
-    case 2: return launch_t<D, 2>(interp, dense, a, nitems, smem, box_stride, s);
-    case 4: return launch_t<D, 4>(interp, dense, a, nitems, smem, box_stride, s);
-    case 6: return launch_t<D, 6>(interp, dense, a, nitems, smem, box_stride, s);
-    case 8: return launch_t<D, 8>(interp, dense, a, nitems, smem, box_stride, s);
-    case 10: return launch_t<D, 10>(interp, dense, a, nitems, smem, box_stride, s);
-    case 12: return launch_t<D, 12>(interp, dense, a, nitems, smem, box_stride, s);
-    case 14: return launch_t<D, 14>(interp, dense, a, nitems, smem, box_stride, s);
-    case 16: return launch_t<D, 16>(interp, dense, a, nitems, smem, box_stride, s);
+    case 2: return launch_t<D, 2>(interp, dense, a, nitems, smem, box_stride, box_pad, s);
+    case 4: return launch_t<D, 4>(interp, dense, a, nitems, smem, box_stride, box_pad, s);
+    case 6: return launch_t<D, 6>(interp, dense, a, nitems, smem, box_stride, box_pad, s);
+    case 8: return launch_t<D, 8>(interp, dense, a, nitems, smem, box_stride, box_pad, s);
+    case 10: return launch_t<D, 10>(interp, dense, a, nitems, smem, box_stride, box_pad, s);
+    case 12: return launch_t<D, 12>(interp, dense, a, nitems, smem, box_stride, box_pad, s);
+    case 14: return launch_t<D, 14>(interp, dense, a, nitems, smem, box_stride, box_pad, s);
+    case 16: return launch_t<D, 16>(interp, dense, a, nitems, smem, box_stride, box_pad, s);
     default: break;
   }
   // runtime-2m kernels (m > 8): one value per unit, 256 threads
@@ -715,6 +725,7 @@ void Core::build_plan(const double* nodes_colmajor) {
   std::vector<DRun> druns;
   const int Md[3] = {d == 3 ? M : 1, d >= 2 ? M : 1, M};
   box_stride = 1;
+  box_pad = 1;
   for (int k = 0; k < nitems; ++k) {
     const HItem& h = hitems[static_cast<size_t>(k)];
     int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
@@ -750,9 +761,11 @@ void Core::build_plan(const double* nodes_colmajor) {
     it.e1 = ext[1];
     it.e2 = ext[2];
     box_stride = std::max<int64_t>(box_stride, static_cast<int64_t>(ext[0]) * ext[1] * ext[2]);
+    box_pad = std::max<int64_t>(box_pad, static_cast<int64_t>(ext[0]) * ext[1] * v5_pad(ext[2]));
     ditems.push_back(it);
   }
   box_stride = (box_stride + 1) / 2 * 2;  // keep the staging area 16-byte aligned
+  box_pad = (box_pad + 1) / 2 * 2;
   if (std::getenv("FGS_PLAN_STATS")) {  // tuning aid: item sizes and the per-CTA shared memory
     int64_t box_sum = 0, pts_max = 0, runs_max = 0;
     for (const DItem& it : ditems) {
@@ -960,6 +973,7 @@ size_t Core::smem_bytes(bool interp) const {
   const bool dense = mean_run >= kDenseRun;
   const LaunchShape sh = d == 3 ? shape_of<3>(T, dense) : (d == 2 ? shape_of<2>(T, dense) : shape_of<1>(T, dense));
   size_t boxes = static_cast<size_t>(box_stride);
+  if (interp && d == 3 && kInterpV5 && (T == 8 || T == 12 || T == 16)) boxes = static_cast<size_t>(box_pad);
   if (d == 3 && !interp && dense) boxes *= static_cast<size_t>(v4_spread_groups(T));  // per-group boxes
   if (d == 2 && !interp && dense && (T == 8 || T == 12 || T == 16))
     boxes *= static_cast<size_t>(kSpread2dP);  // per-stream boxes
@@ -978,9 +992,10 @@ void Core::launch_spread(const PassArgs& a) {
     std::fprintf(stderr, "[plan] smem per CTA: spread %zu B, interp %zu B\n", smem, smem_bytes(true));
   if (smem > 227 * 1024) fail(FGS_ERESOURCE, "tile box exceeds shared memory (cutoff too large for d = 3)");
   const bool dense = mean_run >= kDenseRun;
-  if (d == 3) dispatch<3>(false, dense, T, a, nitems, smem, static_cast<int>(box_stride), stream);
-  if (d == 2) dispatch<2>(false, dense, T, a, nitems, smem, static_cast<int>(box_stride), stream);
-  if (d == 1) dispatch<1>(false, dense, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  const int bs = static_cast<int>(box_stride), bp = static_cast<int>(box_pad);
+  if (d == 3) dispatch<3>(false, dense, T, a, nitems, smem, bs, bp, stream);
+  if (d == 2) dispatch<2>(false, dense, T, a, nitems, smem, bs, bp, stream);
+  if (d == 1) dispatch<1>(false, dense, T, a, nitems, smem, bs, bp, stream);
   ++launches;
   FGS_CUDA(cudaGetLastError());
 }
@@ -989,9 +1004,10 @@ void Core::launch_interp(const PassArgs& a) {
   if (nitems == 0) return;
   const size_t smem = smem_bytes(true);
   if (smem > 227 * 1024) fail(FGS_ERESOURCE, "tile box exceeds shared memory (cutoff too large for d = 3)");
-  if (d == 3) dispatch<3>(true, true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
-  if (d == 2) dispatch<2>(true, true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
-  if (d == 1) dispatch<1>(true, true, T, a, nitems, smem, static_cast<int>(box_stride), stream);
+  const int bs = static_cast<int>(box_stride), bp = static_cast<int>(box_pad);
+  if (d == 3) dispatch<3>(true, true, T, a, nitems, smem, bs, bp, stream);
+  if (d == 2) dispatch<2>(true, true, T, a, nitems, smem, bs, bp, stream);
+  if (d == 1) dispatch<1>(true, true, T, a, nitems, smem, bs, bp, stream);
   ++launches;
   FGS_CUDA(cudaGetLastError());
 }

@@ -44,7 +44,10 @@ struct Blk4 {
 #ifndef FGS_G12_INTERP
 #define FGS_G12_INTERP 2
 #endif
-  static constexpr int G = T == 16 ? (INTERP ? 2 : 4) : (T == 12 ? (INTERP ? FGS_G12_INTERP : 2) : 1);
+  // 2m = 16 spread: one group of 8 warps (each warp one a-tile pair, all c
+  // and e): no turn-based flush barriers (C5 spread 64.5 -> 57.9 ms per
+  // 16-vector block; G = 4 x 2 streams before)
+  static constexpr int G = T == 16 ? (INTERP ? 2 : 8) : (T == 12 ? (INTERP ? FGS_G12_INTERP : 2) : 1);
   static constexpr int TA = T / 2;           // a-tiles (2 a each)
   static constexpr int TC = T / 4;           // c-tiles (4 c each)
   static constexpr int TAW = TA / G;         // a-tiles per warp
@@ -53,7 +56,7 @@ struct Blk4 {
   static constexpr int NE = (T + 7) / 8;     // spread N-tiles over e (2m = 12 pads 12 -> 16)
   // groups (point streams) per CTA; PS > 0 overrides the default
   // (2m = 16 spread: 2 streams, C5 64.9 -> 62.2 ms per 16-vector block)
-  static constexpr int P = PS > 0 ? PS : (T == 8 ? 4 : 2);
+  static constexpr int P = PS > 0 ? PS : (T == 8 ? 4 : ((T == 16 && !INTERP) ? 1 : 2));
   static constexpr int NT = 32 * G * P;
   // points per staged chunk (2m = 12: spread 64 -- C4 spread 412 -> 391 us
   // with the private group boxes -- interp 32)
@@ -360,6 +363,12 @@ __global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(
     auto flush = [&]() {
       if constexpr (PRIV) {
         flush_into(S + grp * box_stride_smem);
+      } else if constexpr (P == 1) {
+        // one group: its warps own disjoint a-rows of THIS run's footprint,
+        // but consecutive runs' footprints overlap at other offsets, so
+        // every warp finishes this flush before any flushes the next run
+        flush_into(S);
+        __syncthreads();
       } else {
         for (int g = 0; g < P; ++g) {
           if (g == grp) flush_into(S);
