@@ -201,6 +201,22 @@ constexpr int kInterp2dP = 2;
 #define FGS_INTERP_V5 1
 #endif
 constexpr bool kInterpV5 = FGS_INTERP_V5 != 0;
+// d = 3 spread, 2m in {12, 16}: warps own box rows x0 = w (mod W), no
+// barrier per run (kernels_v5.cuh); FGS_SPREAD_V5=0 builds the v4 kernel
+#ifndef FGS_SPREAD_V5
+#define FGS_SPREAD_V5 1
+#endif
+#ifndef FGS_V5S_W16
+#define FGS_V5S_W16 8
+#endif
+template <int T>
+constexpr bool use_spread_v5() {  // 2m = 12 (C4) measured slower: 449 vs 391 us
+  return FGS_SPREAD_V5 != 0 && T == 16;
+}
+template <int T>
+constexpr int v5s_w() {
+  return T == 16 ? FGS_V5S_W16 : T / 2;
+}
 constexpr int kSpread2dP = 1;
 // staged input window (Blk4d2::XW) of the d = 2 variant with P streams
 constexpr size_t xw2d(int p) { return static_cast<size_t>(p * 32 > 64 ? p * 32 : 64); }
@@ -214,6 +230,7 @@ constexpr size_t v4_stage_doubles() {
 
 // private spread boxes of the d = 3 DMMA spread (P when P >= 4, else one shared box)
 int v4_spread_groups(int T) {
+  if (T == 16 && FGS_SPREAD_V5) return 1;  // spread_v5: one box
   switch (T) {
     case 8: return Blk4<8, false>::P >= 4 ? Blk4<8, false>::P : 1;
     case 12: return Blk4<12, false>::P >= 4 ? Blk4<12, false>::P : 1;
@@ -237,7 +254,12 @@ LaunchShape shape_t(bool dense) {
   size_t spread = base;
   if constexpr (has_v4_3d<D, T>()) {
     interp = kInterpV5 ? v5_extra_doubles<T>() : v4_stage_doubles<T, true>();
-    if (dense) spread = v4_stage_doubles<T, false>();
+    if (dense) {
+      if constexpr (use_spread_v5<T>())
+        spread = v5s_extra_doubles<T, v5s_w<T>()>();
+      else
+        spread = v4_stage_doubles<T, false>();
+    }
   }
   if constexpr (has_v4_2d<D, T>()) {
     using B4 = Blk4d2<T>;
@@ -290,7 +312,14 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
         return launch_smem(interp_v4_kernel<T, 0, 0, true>, nitems, Blk4<T, true>::NT, smem, s, a, box_stride);
       return launch_smem(interp_v4_kernel<T, 0, 0>, nitems, Blk4<T, true>::NT, smem, s, a, box_stride);
     }
-    if (dense) return launch_smem(spread_v4_kernel<T, 0, 0>, nitems, Blk4<T, false>::NT, smem, s, a, box_stride);
+    if (dense) {
+      if constexpr (use_spread_v5<T>()) {
+        constexpr int W = v5s_w<T>();
+        return launch_smem(spread_v5_kernel<T, W>, nitems, Blk5s<T, W>::NT, smem, s, a, box_stride);
+      } else {
+        return launch_smem(spread_v4_kernel<T, 0, 0>, nitems, Blk4<T, false>::NT, smem, s, a, box_stride);
+      }
+    }
   }
   constexpr int NT = Blk<D, T>::NT;
   if (interp)

@@ -199,3 +199,154 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v5_kernel(PassArgs a, i
 }
 
 }  // namespace fgsb
+
+namespace fgsb {
+
+// ---------------------------------------------------------------------------
+// d = 3 spread, 2m in {12, 16}: W warps share every K-step of a run and each
+// warp owns the item-box rows x0 = w (mod W).  In a run with footprint
+// origin o0 the warp's a-values are a = (w - o0 mod W) + W i, i < 2m / W, so
+// its accumulators (2m/W a-rows x 2m c x 2m e of the footprint) flush into
+// box rows no other warp ever writes: no barrier per run (the v4 kernel's
+// warps owned footprint-relative a-rows, which overlap between consecutive
+// runs, and needed a CTA barrier around every flush).
+//   G[(a,c)][e] += sum_j (wa_j[a] wc_j[c]) (x_j we_j[e])   M = 8 pairs, K = 4 points, N = 8 e
+// The chunk staging (cp.async, double buffer) is the v4 kernel's.
+// ---------------------------------------------------------------------------
+template <int T, int W>
+struct Blk5s {
+  static constexpr int NT = 32 * W;
+  static constexpr int RW = T / W;      // a-rows per warp
+  static constexpr int TAW = RW / 2;    // a-tiles (2 rows) per warp
+  static constexpr int TC = T / 4;      // c-tiles (4 c)
+  static constexpr int NE = (T + 7) / 8;  // e-tiles (2m = 12 pads 12 -> 16)
+  static constexpr int TW = TAW * TC;
+  static constexpr int QS = 64;
+  static constexpr int TAPS = 3 * T;
+  static constexpr int STRIDE = Blk4<T, false>::STRIDE;
+  static_assert(T % W == 0 && RW % 2 == 0, "each warp owns whole a-tiles");
+};
+
+template <int T, int W>
+constexpr size_t v5s_extra_doubles() {
+  using B = Blk5s<T, W>;
+  return 2 * static_cast<size_t>(B::QS) * B::STRIDE + 2 * B::QS;
+}
+
+template <int T, int W>
+__global__ void __launch_bounds__(Blk5s<T, W>::NT, 2) spread_v5_kernel(PassArgs a, int box_stride_smem) {
+  pdl_wait();
+  using B = Blk5s<T, W>;
+  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, SR = B::STRIDE;
+  constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, NE = B::NE;
+  extern __shared__ __align__(16) double smem[];
+  double* S = smem;
+  double* stg = smem + box_stride_smem;
+  double* xs = stg + 2 * QS * SR;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, r8 = lane >> 2;
+  const DItem it = a.items[blockIdx.x];
+  const int bx1 = it.e1, bx2 = it.e2;
+  const int V = it.e0 * it.e1 * it.e2;
+  const int64_t p_begin = it.p_begin, p_end = it.p_end;
+  const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
+
+  for (int vec = 0; vec < a.nvec; ++vec) {
+    const double* xv = a.x + vec * a.ldx;
+    for (int v = tid; v < V; v += NT) S[v] = 0.0;
+    v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
+    cp_async_commit();
+    if (tid < QS && p_begin + tid < p_end) xs[tid] = v2_x(a, xv, p_begin + tid);
+    int r = it.run_begin;
+    DRun run = a.runs[r];
+    double C[TW][NE][2];
+#pragma unroll
+    for (int t = 0; t < TW; ++t)
+#pragma unroll
+      for (int ne = 0; ne < NE; ++ne) C[t][ne][0] = C[t][ne][1] = 0.0;
+    // this warp's first a-row of the run's footprint (box row = warp mod W)
+    auto first_a = [&](const DRun& rn) { return ((warp - (rn.off & 1023)) % W + W) % W; };
+    int a0 = first_a(run);
+
+    auto flush = [&]() {
+      const int o0 = run.off & 1023, o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
+#pragma unroll
+      for (int t = 0; t < TW; ++t) {
+        const int ta = t / TC, tc = t % TC;
+        const int aa = a0 + W * (2 * ta + (r8 >> 2)), cc = 4 * tc + (r8 & 3);
+        double* row = S + ((o0 + aa) * bx1 + (o1 + cc)) * bx2 + o2;
+#pragma unroll
+        for (int ne = 0; ne < NE; ++ne)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int e = 8 * ne + 2 * q + i;
+            if (e < T) row[e] += C[t][ne][i];
+            C[t][ne][i] = 0.0;
+          }
+      }
+    };
+
+    for (int k = 0; k < nch; ++k) {
+      const int64_t c0 = p_begin + static_cast<int64_t>(k) * QS;
+      const int64_t c1 = lmin(c0 + QS, p_end);
+      const int buf = k & 1;
+      cp_async_wait_0();
+      __syncthreads();
+      const bool more = k + 1 < nch;
+      double xnext = 0.0;
+      int qn = 0;
+      if (more) {
+        qn = static_cast<int>(lmin(QS, p_end - c1));
+        v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, qn, tid, NT);
+        cp_async_commit();
+        if (tid < qn) xnext = v2_x(a, xv, c1 + tid);
+      }
+      const double* sb = stg + buf * QS * SR;
+      const double* xb = xs + buf * QS;
+      while (true) {
+        const int64_t rs = run.pstart, re_ = static_cast<int64_t>(run.pstart) + run.pcount;
+        const int64_t s0 = rs > c0 ? rs : c0, s1 = lmin(re_, c1);
+        // K-steps of 4 points aligned to the chunk, from the one holding s0
+        for (int64_t k0 = c0 + ((s0 - c0) & ~int64_t{3}); k0 < s1; k0 += 4) {
+          const int64_t jp = k0 + q;  // this lane's point of the K-step
+          const bool ok = jp >= s0 && jp < s1;
+          const double* w = sb + (ok ? (jp - c0) : 0) * SR;
+          const double xj = ok ? xb[jp - c0] : 0.0;
+          double wa[TAW], wc[TC];
+#pragma unroll
+          for (int t = 0; t < TAW; ++t) wa[t] = w[a0 + W * (2 * t + (r8 >> 2))];
+#pragma unroll
+          for (int t = 0; t < TC; ++t) wc[t] = w[T + 4 * t + (r8 & 3)];
+          double bF[NE];  // x_j we_j[e], e = 8 ne + lane/4
+#pragma unroll
+          for (int ne = 0; ne < NE; ++ne) {
+            const int e = 8 * ne + r8;
+            bF[ne] = e < T ? xj * w[2 * T + e] : 0.0;
+          }
+          double af[TW];  // wa wc of pair (lane/4 row)
+#pragma unroll
+          for (int t = 0; t < TW; ++t) af[t] = wa[t / TC] * wc[t % TC];
+#pragma unroll
+          for (int ne = 0; ne < NE; ++ne)
+#pragma unroll
+            for (int t = 0; t < TW; ++t) dmma(C[t][ne][0], C[t][ne][1], af[t], bF[ne]);
+        }
+        if (re_ <= c1) {  // run ends inside this chunk
+          flush();
+          if (++r >= it.run_end) break;
+          run = a.runs[r];
+          a0 = first_a(run);
+          continue;
+        }
+        break;
+      }
+      if (more && tid < qn) xs[(buf ^ 1) * QS + tid] = xnext;
+    }
+    __syncthreads();
+    double* out = a.priv + (static_cast<int64_t>(vec) * gridDim.x + blockIdx.x) * a.box_stride;
+    for (int v = tid; v < V; v += NT) out[v] = S[v];
+    __syncthreads();
+  }
+}
+
+}  // namespace fgsb
