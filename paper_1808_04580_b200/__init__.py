@@ -442,6 +442,13 @@ def measure_fp64_peak(device=0) -> float:
     return out.value
 
 
+def measure_dmma_peak(device=0) -> float:
+    """fp64 tensor-core (DMMA m8n8k4) peak of `device` in TFLOP/s."""
+    out = C.c_double()
+    _check(lib().fgs_measure_dmma_peak(int(device), C.byref(out)))
+    return out.value
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().fgs_nccl_unique_id(buf))

@@ -19,6 +19,7 @@
 #include "kernels_v4.cuh"
 #include "kernels_v5.cuh"
 #include "conv2d.cuh"
+#include "conv3d.cuh"
 #include "direct.cuh"
 #include "nccl_shim.hpp"
 
@@ -450,7 +451,7 @@ Core::Core(const double* nodes_colmajor, int64_t n_, int d_, Kind kind_, const K
 
   build_plan(nodes_colmajor);
   if (kind == FASTSUM) build_coefficients();
-  if (kind == FASTSUM && d == 2) {  // twiddles e^{-2 pi i j / M} for the pruned 2-D convolution
+  if (kind == FASTSUM && (d == 2 || d == 3)) {  // twiddles e^{-2 pi i j / M} for the pruned convolutions
     std::vector<double2> tw(static_cast<size_t>(M));
     for (int j = 0; j < M; ++j) {
       const double ang = 2.0 * kPi * static_cast<double>(j) / M;
@@ -795,6 +796,37 @@ void Core::build_plan(const double* nodes_colmajor) {
   }
   box_stride = (box_stride + 1) / 2 * 2;  // keep the staging area 16-byte aligned
   box_pad = (box_pad + 1) / 2 * 2;
+  // dim-0 planes this rank's boxes cover: the smallest cyclic interval
+  // holding them (sharded handles convolve only those planes)
+  conv_plane0 = 0;
+  conv_planes = M;
+  if (d == 3 && world > 1 && !ditems.empty()) {
+    std::vector<char> used(static_cast<size_t>(M), 0);
+    for (const DItem& it : ditems)
+      for (int x0 = 0; x0 < it.e0; ++x0) used[static_cast<size_t>((it.a0 + x0) % M)] = 1;
+    int best_len = M, best_start = 0;  // longest cyclic run of unused planes -> its complement
+    int run = 0, run_start = 0, bl = 0, bs = 0;
+    for (int t = 0; t < 2 * M; ++t) {
+      if (!used[static_cast<size_t>(t % M)]) {
+        if (run == 0) run_start = t;
+        if (++run > bl && run <= M) {
+          bl = run;
+          bs = run_start;
+        }
+      } else {
+        run = 0;
+      }
+    }
+    if (bl > 0 && bl < M) {
+      best_start = (bs + bl) % M;
+      best_len = M - bl;
+    }
+    // the kernels take a non-wrapping range: wrap-around slabs convolve all planes
+    if (best_start + best_len <= M) {
+      conv_plane0 = best_start;
+      conv_planes = best_len;
+    }
+  }
   if (std::getenv("FGS_PLAN_STATS")) {  // tuning aid: item sizes and the per-CTA shared memory
     int64_t box_sum = 0, pts_max = 0, runs_max = 0;
     for (const DItem& it : ditems) {
@@ -983,16 +1015,23 @@ Workspace& Core::workspace(int nvec) {
   FGS_CUDA(cudaMemsetAsync(w->grid.p, 0, sizeof(double) * grid_elems * nvec, stream));
   w->grid_out.alloc(static_cast<size_t>(grid_elems) * nvec);
   if (sharded && d == 2) w->grid_sum.alloc(static_cast<size_t>(grid_elems) * nvec);
-  w->spec.alloc(static_cast<size_t>(spec_elems) * nvec);
-  if (sharded) w->window.alloc(static_cast<size_t>(window_elems) * nvec);
-  int dims[3] = {M, M, M};
-  FGS_CUFFT(cufftPlanMany(&w->r2c, d, dims, nullptr, 1, static_cast<int>(grid_elems), nullptr, 1,
-                          static_cast<int>(spec_elems), CUFFT_D2Z, nvec));
-  FGS_CUFFT(cufftPlanMany(&w->c2r, d, dims, nullptr, 1, static_cast<int>(spec_elems), nullptr, 1,
-                          static_cast<int>(grid_elems), CUFFT_Z2D, nvec));
-  FGS_CUFFT(cufftSetStream(w->r2c, stream));
-  FGS_CUFFT(cufftSetStream(w->c2r, stream));
-  w->has_plans = true;
+  if (use_conv3d()) {  // plane-pass window buffer (+ the sharded window spectrum)
+    const int64_t nw = conv3_nw(M, N), H = N / 2 + 1;
+    w->win.alloc(static_cast<size_t>(M) * nw * H * nvec);
+    if (sharded) w->cspec.alloc(static_cast<size_t>(nw) * nw * H * nvec);
+  }
+  if (!use_conv2d() && !use_conv3d()) {  // cuFFT only where no hand-written convolution covers the grid
+    w->spec.alloc(static_cast<size_t>(spec_elems) * nvec);
+    if (sharded) w->window.alloc(static_cast<size_t>(window_elems) * nvec);
+    int dims[3] = {M, M, M};
+    FGS_CUFFT(cufftPlanMany(&w->r2c, d, dims, nullptr, 1, static_cast<int>(grid_elems), nullptr, 1,
+                            static_cast<int>(spec_elems), CUFFT_D2Z, nvec));
+    FGS_CUFFT(cufftPlanMany(&w->c2r, d, dims, nullptr, 1, static_cast<int>(spec_elems), nullptr, 1,
+                            static_cast<int>(grid_elems), CUFFT_Z2D, nvec));
+    FGS_CUFFT(cufftSetStream(w->r2c, stream));
+    FGS_CUFFT(cufftSetStream(w->c2r, stream));
+    w->has_plans = true;
+  }
   auto& ref = *w;
   ws_[nvec] = std::move(w);
   return ref;
@@ -1249,6 +1288,32 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
       mark(evs);
       mark(evs);
     }
+  } else if (use_conv3d()) {
+    // d = 3: pruned plane / line / plane passes (conv3d.cuh).  Sharded: this
+    // rank's planes only; the window spectra of the ranks are summed between
+    // the forward and the inverse line passes
+    Conv3Args ca{w.grid.p, w.grid_out.p, w.win.p, sharded ? w.cspec.p : nullptr, mult.p, tw2.p,
+                 M, N, nvec, conv_plane0, conv_planes, grid_elems};
+    conv3_launch(ca, 0, 1, 0, stream);
+    ++launches;
+    if (profile_) mark(evs);
+    if (!sharded) {
+      conv3_launch(ca, 1, 1, 0, stream);
+      ++launches;
+    } else {
+      conv3_launch(ca, 1, 1, 0, stream);
+      const int64_t nw = conv3_nw(M, N), H = N / 2 + 1;
+      nccl_check(nccl().all_reduce(w.cspec.p, w.cspec.p, static_cast<size_t>(nw * nw * H * nvec * 2), ncclDouble,
+                                   ncclSum, comm, stream),
+                 "ncclAllReduce of the window spectra");
+      conv3_launch(ca, 1, 1, 1, stream);
+      launches += 2;
+    }
+    if (profile_) mark(evs);
+    conv3_launch(ca, 2, 1, 0, stream);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+    if (profile_) mark(evs);
   } else {
     FGS_CUFFT(cufftExecD2Z(w.r2c, w.grid.p, w.spec.p));
     if (profile_) mark(evs);
@@ -1323,6 +1388,17 @@ bool Core::use_conv2d() const {
   }();
   return on && d == 2 && kind == FASTSUM && conv2_supported(M) &&
          conv2_smem(M, N) <= 200 * 1024 && tw2.p != nullptr;
+}
+
+// d = 3 grids: the pruned plane / line / plane convolution (conv3d.cuh)
+// instead of cuFFT D2Z + multiply + Z2D (FGS_CONV3D=0 selects cuFFT)
+bool Core::use_conv3d() const {
+  static const bool on = [] {
+    const char* e = std::getenv("FGS_CONV3D");
+    return !(e && std::string(e) == "0");
+  }();
+  return on && d == 3 && kind == FASTSUM && conv3_supported(M) && M > N && conv3_plane_smem(M, N) <= 200 * 1024 &&
+         tw2.p != nullptr;
 }
 
 void Core::compute_degrees(int64_t* bad_node) {

@@ -82,6 +82,7 @@ struct Workspace {
   // interpolation reads; grid_sum: d = 2 sharded, the ranks' summed grids
   DBuf<double> priv, grid, grid_out, grid_sum;
   DBuf<cufftDoubleComplex> spec, cgrid, window;
+  DBuf<double2> win, cspec;  // d = 3 pruned convolution: plane-pass window, sharded window spectrum
   cufftHandle r2c = 0, c2r = 0, z2z = 0;
   bool has_plans = false, has_z2z = false;
 };
@@ -129,6 +130,10 @@ class Core {
   DBuf<double2> tw2;  // d = 2 pruned-convolution twiddles
   DBuf<double> nodes_d;  // DIRECT: raw nodes [d][n], caller order
   bool use_conv2d() const;
+  bool use_conv3d() const;
+  // d = 3 convolution planes of this rank: [conv_plane0, conv_plane0 + conv_planes)
+  // (all M unsharded; sharded: the dim-0 planes its items' boxes cover)
+  int conv_plane0 = 0, conv_planes = 0;
   int nitems = 0;
   double mean_run = 0.0;  // points per run (cell piece) of this shard: picks the spread kernel
   bool tensor_spread() const;  // the DMMA spread runs (dense runs, 2m in {8, 12, 16}, d in {2, 3})
