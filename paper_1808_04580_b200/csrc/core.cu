@@ -485,6 +485,9 @@ Core::~Core() {
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   for (cudaEvent_t e : lz_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
+  if (cp_in) cudaStreamDestroy(cp_in);
+  if (cp_out) cudaStreamDestroy(cp_out);
   if (comm) nccl().comm_destroy(comm);
   if (bounce) cudaFreeHost(bounce);
   if (own_stream && stream) cudaStreamDestroy(stream);
@@ -1165,6 +1168,22 @@ static bool is_pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
+// sub-blocks of a host-vector block: the largest divisor of nvec with at
+// most nvec / 8 vectors (16 -> 2: the exposed copies are one sub-block's
+// H2D + D2H, 2 x 160 MB at config 5, instead of the whole 2 x 1.28 GB);
+// FGS_PIPE_BLOCK=k forces k vectors per sub-block
+static int pipe_sub_block(int nvec) {
+  static const int forced = [] {
+    const char* e = std::getenv("FGS_PIPE_BLOCK");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0 && nvec % forced == 0) return forced;
+  const int target = std::max(1, nvec / 8);
+  for (int b = target; b >= 1; --b)
+    if (nvec % b == 0) return b;
+  return 1;
+}
+
 bool Core::apply_host_graph(int epilogue, const double* hx, double* hy, int64_t ld, int nvec, bool scale_input) {
   static const bool graphs_on = [] {
     const char* e = std::getenv("FGS_GRAPHS");
@@ -1186,21 +1205,71 @@ bool Core::apply_host_graph(int epilogue, const double* hx, double* hy, int64_t 
       return true;
     }
   }
-  workspace(nvec);
+  const int nb = pipe_sub_block(nvec);
+  const int nsub = nvec / nb;
+  workspace(nb);
+  if (nsub > 1) {
+    if (!cp_in) FGS_CUDA(cudaStreamCreateWithFlags(&cp_in, cudaStreamNonBlocking));
+    if (!cp_out) FGS_CUDA(cudaStreamCreateWithFlags(&cp_out, cudaStreamNonBlocking));
+    while (pipe_ev.size() < static_cast<size_t>(2 * nsub + 3)) {
+      cudaEvent_t e;
+      FGS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      pipe_ev.push_back(e);
+    }
+  }
+  // vectors [v0, v0 + cnt) between the pinned host block and xbuf / ybuf
+  auto h2d = [&](int v0, int cnt, cudaStream_t s) {
+    double* dst = xbuf.p + static_cast<int64_t>(v0) * n;
+    const double* src = hx + static_cast<int64_t>(v0) * ld;
+    if (ld == n)
+      FGS_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * n * cnt, cudaMemcpyHostToDevice, s));
+    else
+      FGS_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * n, src, sizeof(double) * ld, sizeof(double) * n, cnt,
+                                 cudaMemcpyHostToDevice, s));
+  };
+  auto d2h = [&](int v0, int cnt, cudaStream_t s) {
+    const double* src = ybuf.p + static_cast<int64_t>(v0) * n;
+    double* dst = hy + static_cast<int64_t>(v0) * ld;
+    if (ld == n)
+      FGS_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * n * cnt, cudaMemcpyDeviceToHost, s));
+    else
+      FGS_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ld, src, sizeof(double) * n, sizeof(double) * n, cnt,
+                                 cudaMemcpyDeviceToHost, s));
+  };
   const int64_t before = launches;
   FGS_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
   try {
-    if (ld == n)
-      FGS_CUDA(cudaMemcpyAsync(xbuf.p, hx, sizeof(double) * n * nvec, cudaMemcpyHostToDevice, stream));
-    else
-      FGS_CUDA(cudaMemcpy2DAsync(xbuf.p, sizeof(double) * n, hx, sizeof(double) * ld, sizeof(double) * n, nvec,
-                                 cudaMemcpyHostToDevice, stream));
-    apply_launches(epilogue, xbuf.p, n, ybuf.p, n, nvec, true, scale_input);
-    if (ld == n)
-      FGS_CUDA(cudaMemcpyAsync(hy, ybuf.p, sizeof(double) * n * nvec, cudaMemcpyDeviceToHost, stream));
-    else
-      FGS_CUDA(cudaMemcpy2DAsync(hy, sizeof(double) * ld, ybuf.p, sizeof(double) * n, sizeof(double) * n, nvec,
-                                 cudaMemcpyDeviceToHost, stream));
+    if (nsub == 1) {
+      h2d(0, nvec, stream);
+      apply_launches(epilogue, xbuf.p, n, ybuf.p, n, nvec, true, scale_input);
+      d2h(0, nvec, stream);
+    } else {
+      // fork: copy-in stream uploads sub-block k while the compute stream
+      // applies sub-block k - 1 and the copy-out stream downloads k - 2
+      // (H2D and D2H use separate copy engines; the sub-block applies are
+      // the same kernels as one block apply, vectors being independent)
+      cudaEvent_t fork = pipe_ev[0];
+      FGS_CUDA(cudaEventRecord(fork, stream));
+      FGS_CUDA(cudaStreamWaitEvent(cp_in, fork, 0));
+      FGS_CUDA(cudaStreamWaitEvent(cp_out, fork, 0));
+      for (int k = 0; k < nsub; ++k) {
+        cudaEvent_t in_done = pipe_ev[static_cast<size_t>(3 + 2 * k)];
+        cudaEvent_t ap_done = pipe_ev[static_cast<size_t>(4 + 2 * k)];
+        h2d(k * nb, nb, cp_in);
+        FGS_CUDA(cudaEventRecord(in_done, cp_in));
+        FGS_CUDA(cudaStreamWaitEvent(stream, in_done, 0));
+        apply_launches(epilogue, xbuf.p + static_cast<int64_t>(k) * nb * n, n,
+                       ybuf.p + static_cast<int64_t>(k) * nb * n, n, nb, true, scale_input);
+        FGS_CUDA(cudaEventRecord(ap_done, stream));
+        FGS_CUDA(cudaStreamWaitEvent(cp_out, ap_done, 0));
+        d2h(k * nb, nb, cp_out);
+      }
+      // join both copy streams back into the capture stream
+      FGS_CUDA(cudaEventRecord(pipe_ev[1], cp_in));
+      FGS_CUDA(cudaEventRecord(pipe_ev[2], cp_out));
+      FGS_CUDA(cudaStreamWaitEvent(stream, pipe_ev[1], 0));
+      FGS_CUDA(cudaStreamWaitEvent(stream, pipe_ev[2], 0));
+    }
   } catch (...) {
     cudaGraph_t broken = nullptr;
     cudaStreamEndCapture(stream, &broken);

@@ -149,6 +149,10 @@ class Core {
 
   // staging buffers for host-vector calls
   DBuf<double> xbuf, ybuf;
+  // host-vector graphs of multi-vector blocks: copy-in / copy-out streams
+  // forked from `stream` inside the capture, and the capture's events
+  cudaStream_t cp_in = nullptr, cp_out = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
   // Lanczos workspace, reused across solves (lanczos.cu)
   DBuf<double> lz_basis, lz_z, lz_partial, lz_hbuf, lz_scal, lz_qin;
   DBuf<double> lz_alpha, lz_nrm, lz_beta, lz_st;  // run-ahead recurrence scalars
@@ -172,7 +176,8 @@ class Core {
              bool caller_order, bool scale_input);
   // y_host = op(x_host) as ONE graph (H2D into xbuf, the apply, D2H from
   // ybuf) when both host buffers are pinned; false -> caller stages itself.
-  // Does not synchronise.
+  // Blocks of several vectors are cut into sub-blocks whose copies overlap
+  // the other sub-blocks' applies (pipe_blocks).  Does not synchronise.
   bool apply_host_graph(int epilogue, const double* hx, double* hy, int64_t ld, int nvec, bool scale_input);
   // Contiguous host <-> device copy ordered after the work queued on
   // `stream`; returns when the data has landed.  Large copies to or from

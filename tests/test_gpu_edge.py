@@ -148,3 +148,34 @@ def test_sharded_exchange_path_with_one_rank(orc):
     a = fgs.lanczos_largest(plain, 4, fgs.LanczosOptions(tol=1e-10))
     b = fgs.lanczos_largest(shard, 4, fgs.LanczosOptions(tol=1e-10))
     assert np.max(np.abs(a.values - b.values)) <= 1e-12
+
+
+def test_pinned_host_block_pipelined_graph(orc):
+    # Pinned host blocks of several vectors run as one graph whose sub-block
+    # H2D / apply / D2H overlap on three streams (Core::apply_host_graph):
+    # every column equals the same vector applied alone from device memory
+    # (bitwise: the kernels are the same, vectors are independent) and the
+    # oracle; the padding of the leading dimension stays untouched.
+    import torch
+    X = np.random.default_rng(14).uniform(-0.1, 0.1, (5000, 3))
+    op, ref = _pair(orc, X, 0, 0.05, 32, 8)
+    n, ld, nvec = 5000, 5003, 16
+    xv = np.random.default_rng(15).standard_normal((nvec, n))
+    hx = torch.zeros(nvec * ld, dtype=torch.float64).pin_memory()
+    for j in range(nvec):
+        hx[j * ld:j * ld + n] = torch.from_numpy(xv[j])
+    hy = torch.full((nvec * ld,), 7.0, dtype=torch.float64).pin_memory()
+    dp = lambda t: C.cast(t.data_ptr(), C.POINTER(C.c_double))  # noqa: E731
+    for _ in range(2):  # capture, then replay of the cached graph
+        st = fgs.lib().fgs_adjacency_apply(op.handle, fgs.OP_SYM_LAPLACIAN, dp(hx), dp(hy), nvec, C.c_int64(ld))
+        assert st == 0, fgs.lib().fgs_last_error()
+    y = hy.numpy()
+    for j in range(nvec):
+        dx = torch.from_numpy(xv[j]).cuda()
+        dy = torch.empty_like(dx)
+        op.apply_device(fgs.OP_SYM_LAPLACIAN, dx.data_ptr(), dy.data_ptr(), internal_order=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(y[j * ld:j * ld + n], dy.cpu().numpy())
+        assert np.all(y[j * ld + n:(j + 1) * ld] == 7.0)
+    for j in (0, nvec - 1):
+        assert rel(y[j * ld:j * ld + n], ref.apply_sym_laplacian(xv[j])) <= 1e-10
