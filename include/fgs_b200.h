@@ -161,6 +161,10 @@ fgs_status fgs_adjacency_geometry(fgs_adjacency_t h, int* d, int* N, int* M, int
  * fp64 tensor-core (DMMA) spread / interpolation is used, 0 for the scalar
  * kernels. */
 fgs_status fgs_adjacency_plan_stats(fgs_adjacency_t h, double* mean_run, int* tensor_spread, int* tensor_interp);
+/* 1 when the plan uses the run-aligned slot layout (d = 3, 2m = 16 dense
+ * plans: every footprint run starts on a multiple of 8 slots), and the
+ * number of slots (points + pad slots); 0 / the point count otherwise. */
+fgs_status fgs_adjacency_plan_layout(fgs_adjacency_t h, int* slot_layout, int64_t* slots);
 /* fp64 FMA-pipe peak of `device` in TFLOP/s (independent DFMA chains, CUDA
  * events), the denominator of the spread/interp roofline. */
 fgs_status fgs_measure_fp64_peak(int device, double* tflops);

@@ -420,7 +420,10 @@ class AdjacencyOperator:
         """mean points per run and whether the DMMA spread / interpolation run."""
         mr, ts, ti = C.c_double(), C.c_int(), C.c_int()
         _check(lib().fgs_adjacency_plan_stats(self._h, C.byref(mr), C.byref(ts), C.byref(ti)))
-        return dict(mean_run=mr.value, tensor_spread=bool(ts.value), tensor_interp=bool(ti.value))
+        sl, ns = C.c_int(), C.c_int64()
+        _check(lib().fgs_adjacency_plan_layout(self._h, C.byref(sl), C.byref(ns)))
+        return dict(mean_run=mr.value, tensor_spread=bool(ts.value), tensor_interp=bool(ti.value),
+                    slot_layout=bool(sl.value), slots=ns.value)
 
     def lanczos_stats(self) -> dict:
         out = np.zeros(4)

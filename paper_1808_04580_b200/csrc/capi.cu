@@ -474,6 +474,15 @@ fgs_status fgs_adjacency_plan_stats(fgs_adjacency_t h, double* mean_run, int* te
   });
 }
 
+fgs_status fgs_adjacency_plan_layout(fgs_adjacency_t h, int* slot_layout, int64_t* slots) {
+  return guard([&] {
+    need(h, "handle");
+    const Core& c = *h->core;
+    if (slot_layout) *slot_layout = c.use_slots ? 1 : 0;
+    if (slots) *slots = c.use_slots ? static_cast<int64_t>(c.slot_map.n) : c.n_local;
+  });
+}
+
 fgs_status fgs_measure_fp64_peak(int device, double* tflops) {
   return guard([&] {
     need(tflops, "tflops");

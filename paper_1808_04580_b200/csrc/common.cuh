@@ -135,6 +135,9 @@ struct PassArgs {
   unsigned long long* bad_flag;  // EPI_DEGREE: min caller index with d <= 0
   const int* caller;   // internal -> caller index of this shard's slice (always set)
   int defer_epilogue;  // v4 interp, one warp per footprint: epilogue per staged chunk (large plans)
+  const int* slots;    // v6 kernels: slot -> local internal point (-1: pad); items / runs in slots
+  const double* xs;    // v6 spread: the vectors gathered into slot order (pads 0, s applied)
+  int64_t ldxs;
 };
 
 }  // namespace fgsb

@@ -17,7 +17,7 @@
 #include "kernels.cuh"
 #include "kernels_v2.cuh"
 #include "kernels_v4.cuh"
-#include "kernels_v5.cuh"
+#include "kernels_v6.cuh"
 #include "conv2d.cuh"
 #include "conv3d.cuh"
 #include "direct.cuh"
@@ -219,6 +219,15 @@ constexpr int v5s_w() {
   return T == 16 ? FGS_V5S_W16 : T / 2;
 }
 constexpr int kSpread2dP = 1;
+// d = 3, 2m = 16 dense plans: run-aligned slot layout + kernels_v6.cuh
+// (FGS_V6=0: the v5 kernels over the plain point order)
+bool v6_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FGS_V6");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
 // staged input window (Blk4d2::XW) of the d = 2 variant with P streams
 constexpr size_t xw2d(int p) { return static_cast<size_t>(p * 32 > 64 ? p * 32 : 64); }
 
@@ -302,6 +311,12 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
       return launch_smem(interp_v4_2d_kernel<T, kInterp2dP>, nitems, Blk4d2<T, kInterp2dP>::NT, smem, s, a, box_stride);
     if (dense)
       return launch_smem(spread_v4_2d_kernel<T, kSpread2dP>, nitems, Blk4d2<T, kSpread2dP>::NT, smem, s, a, box_stride);
+  }
+  if constexpr (D == 3 && T == 16) {
+    if (a.slots != nullptr) {
+      if (interp) return launch_smem(interp_v6_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+      return launch_smem(spread_v6_kernel, nitems, Blk6s::NT, smem, s, a, box_stride);
+    }
   }
   if constexpr (has_v4_3d<D, T>()) {
     if (interp && kInterpV5)
@@ -900,17 +915,63 @@ void Core::build_plan(const double* nodes_colmajor) {
     ditems.push_back(DItem{0, 0, 0, 0, 0, 1, 1, 1, 0, 0});
     nitems = 0;
   }
+  // run-aligned slot layout (kernels_v6.cuh): every run starts on a
+  // multiple of kSlotAlign slots, items are consecutive; same item order and
+  // boxes as the point layout, so the assembly map serves both
+  use_slots = false;
+  if (kind == FASTSUM && d == 3 && T == 16 && nitems > 0 && mean_run >= kDenseRun && v6_enabled()) {
+    std::vector<DItem> sitems(ditems);
+    std::vector<DRun> sruns(druns);
+    std::vector<int>& smap = slot_host;
+    smap.clear();
+    smap.reserve(static_cast<size_t>(n_local + (n_local / 8) + 8 * druns.size()));
+    int64_t sl = 0;
+    for (DItem& it : sitems) {
+      it.p_begin = static_cast<int>(sl);
+      for (int r = it.run_begin; r < it.run_end; ++r) {
+        const DRun& pr = druns[static_cast<size_t>(r)];
+        sruns[static_cast<size_t>(r)].pstart = static_cast<int>(sl);
+        const int padded = (pr.pcount + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
+        for (int j = 0; j < padded; ++j) smap.push_back(j < pr.pcount ? pr.pstart + j : -1);
+        sl += padded;
+      }
+      it.p_end = static_cast<int>(sl);
+    }
+    if (sl >= (int64_t{1} << 31)) fail(FGS_ERESOURCE, "slot layout exceeds 2^31 entries");
+    items6.upload(sitems.data(), sitems.size(), stream);
+    runs6.upload(sruns.data(), sruns.size(), stream);
+    slot_map.upload(smap.data(), smap.size(), stream);
+    use_slots = true;
+  }
   items.upload(ditems.data(), ditems.size(), stream);
   if (druns.empty()) druns.push_back(DRun{0, 0, 0});
   runs.upload(druns.data(), druns.size(), stream);
 
-  // window taps of the local slice in internal order
+  // window taps of the local slice in internal order, or (slot layout) in
+  // slot order with rows padded to kSlotRow doubles, pad slots zero
+  if (use_slots) {
+    std::vector<int> rows(slot_host.size());
+    for (size_t i = 0; i < rows.size(); ++i)
+      rows[i] = slot_host[i] < 0 ? -1 : host_perm[static_cast<size_t>(offset + slot_host[i])];
+    DBuf<int> drows;
+    drows.upload(rows.data(), rows.size(), stream);
+    const int64_t ns = static_cast<int64_t>(rows.size());
+    taps.alloc(static_cast<size_t>(ns) * kSlotRow);
+    TapArgs ta{dnodes.p, n, ns, perm.p + offset, d, M, m, rho, b_kb, kind == FASTSUM ? 1 : 0, taps.p, drows.p, kSlotRow};
+    taps_kernel<<<ceil_div(ns, 128), 128, 0, stream>>>(ta);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaStreamSynchronize(stream));  // before drows is freed
+    slot_host.clear();
+    slot_host.shrink_to_fit();
+  } else {
   taps.alloc(static_cast<size_t>(std::max<int64_t>(n_local, 1)) * d * T);
   if (n_local > 0) {
-    TapArgs ta{dnodes.p, n, n_local, perm.p + offset, d, M, m, rho, b_kb, kind == FASTSUM ? 1 : 0, taps.p};
+    TapArgs ta{dnodes.p, n, n_local, perm.p + offset, d, M, m, rho, b_kb, kind == FASTSUM ? 1 : 0, taps.p, nullptr, 0};
     taps_kernel<<<ceil_div(n_local, 128), 128, 0, stream>>>(ta);
     ++launches;
     FGS_CUDA(cudaGetLastError());
+  }
   }
   FGS_CUDA(cudaStreamSynchronize(stream));
 }
@@ -1017,6 +1078,7 @@ Workspace& Core::workspace(int nvec) {
   w->grid.alloc(static_cast<size_t>(grid_elems) * nvec);
   FGS_CUDA(cudaMemsetAsync(w->grid.p, 0, sizeof(double) * grid_elems * nvec, stream));
   w->grid_out.alloc(static_cast<size_t>(grid_elems) * nvec);
+  if (use_slots) w->xs.alloc(slot_map.n * nvec);
   if (sharded && d == 2) w->grid_sum.alloc(static_cast<size_t>(grid_elems) * nvec);
   if (use_conv3d()) {  // plane-pass window buffer (+ the sharded window spectrum)
     const int64_t nw = conv3_nw(M, N), H = N / 2 + 1;
@@ -1045,6 +1107,8 @@ size_t Core::smem_bytes(bool interp) const {
   const LaunchShape sh = d == 3 ? shape_of<3>(T, dense) : (d == 2 ? shape_of<2>(T, dense) : shape_of<1>(T, dense));
   size_t boxes = static_cast<size_t>(box_stride);
   if (interp && d == 3 && kInterpV5 && (T == 8 || T == 12 || T == 16)) boxes = static_cast<size_t>(box_pad);
+  if (use_slots && interp) return (boxes + v6i_extra_doubles<16>()) * sizeof(double);
+  if (use_slots && !interp) return (boxes + v6s_extra_doubles()) * sizeof(double);
   if (d == 3 && !interp && dense) boxes *= static_cast<size_t>(v4_spread_groups(T));  // per-group boxes
   if (d == 2 && !interp && dense && (T == 8 || T == 12 || T == 16))
     boxes *= static_cast<size_t>(kSpread2dP);  // per-stream boxes
@@ -1292,6 +1356,18 @@ bool Core::apply_host_graph(int epilogue, const double* hx, double* hy, int64_t 
   return true;
 }
 
+void Core::pass_layout(PassArgs& a) const {
+  if (use_slots) {
+    a.items = items6.p;
+    a.runs = runs6.p;
+    a.slots = slot_map.p;
+  } else {
+    a.items = items.p;
+    a.runs = runs.p;
+    a.slots = nullptr;
+  }
+}
+
 void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
                           bool caller_order, bool scale_input) {
   Workspace& w = workspace(nvec);
@@ -1300,8 +1376,7 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
     return;
   }
   PassArgs a{};
-  a.items = items.p;
-  a.runs = runs.p;
+  pass_layout(a);
   a.taps = taps.p;
   a.perm = caller_order ? perm.p + offset : nullptr;
   a.point_base = offset;
@@ -1327,6 +1402,15 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
 
   std::vector<cudaEvent_t> evs;
   if (profile_) mark(evs);
+  if (use_slots && nitems > 0) {  // the vectors in slot order for the v6 spread (pads 0, s applied)
+    const int64_t ns = static_cast<int64_t>(slot_map.n);
+    a.xs = w.xs.p;
+    a.ldxs = ns;
+    launch_ex(slot_gather_kernel, dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div(ns * nvec, 256), 148 * 16))),
+              dim3(256), 0, stream, a, ns, w.xs.p);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+  }
   launch_spread(a);
   if (profile_) mark(evs);
   launch_assemble(w, nvec);
@@ -1506,8 +1590,7 @@ void Core::nfft_adjoint(const double* x_planar, double* fhat_out) {
   // x_planar: device [2][n] (re, im) in caller order; fhat_out: device interleaved N^d
   Workspace& w = workspace(2);
   PassArgs a{};
-  a.items = items.p;
-  a.runs = runs.p;
+  pass_layout(a);
   a.taps = taps.p;
   a.perm = perm.p + offset;
   a.x = x_planar;
@@ -1557,8 +1640,7 @@ void Core::nfft_forward(const double* fhat_in, double* y_planar) {
                                                                       w.grid_out.p + grid_elems, grid_elems);
   ++launches;
   PassArgs a{};
-  a.items = items.p;
-  a.runs = runs.p;
+  pass_layout(a);
   a.taps = taps.p;
   a.perm = perm.p + offset;
   a.x = nullptr;

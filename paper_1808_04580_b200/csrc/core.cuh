@@ -83,6 +83,7 @@ struct Workspace {
   DBuf<double> priv, grid, grid_out, grid_sum;
   DBuf<cufftDoubleComplex> spec, cgrid, window;
   DBuf<double2> win, cspec;  // d = 3 pruned convolution: plane-pass window, sharded window spectrum
+  DBuf<double> xs;           // slot layout: the block's vectors gathered into slot order
   cufftHandle r2c = 0, c2r = 0, z2z = 0;
   bool has_plans = false, has_z2z = false;
 };
@@ -122,6 +123,15 @@ class Core {
   DBuf<double> taps;  // [n_local][d][T]
   DBuf<DItem> items;
   DBuf<DRun> runs;
+  // run-aligned slot layout of the d = 3, 2m = 16 tensor kernels
+  // (kernels_v6.cuh): items / runs in slot coordinates and slot -> local
+  // internal point (-1: pad slot); empty when the plan does not use it
+  DBuf<DItem> items6;
+  DBuf<DRun> runs6;
+  DBuf<int> slot_map;
+  std::vector<int> slot_host;  // plan-time copy (freed once the taps are built)
+  bool use_slots = false;
+  void pass_layout(PassArgs& a) const;
   DBuf<int> asm_ptr, asm_idx;  // grid cell -> private-box entries (CSR, item order)
   DBuf<int> asm_cells;  // nonempty cells by list-length class: > 64 | 9..64 | <= 8 entries
   int64_t asm_class_n[3] = {0, 0, 0};

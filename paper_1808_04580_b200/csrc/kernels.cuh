@@ -98,15 +98,22 @@ struct TapArgs {
   double rho, b;
   int apply_rho;
   double* taps;    // [count][d][2m]
+  const int* rows; // slot layout: row -> caller index (-1: pad row, zero taps); nullable
+  int stride;      // doubles per row (0: d 2m)
 };
 
 // Window taps of every point in internal order (nfft.cpp:355-365).
 __global__ void taps_kernel(TapArgs a) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (p >= a.count) return;
-  const int j = a.perm[p];
   const int T = 2 * a.m;
-  double* out = a.taps + p * a.d * T;
+  const int stride = a.stride ? a.stride : a.d * T;
+  double* out = a.taps + p * stride;
+  const int j = a.rows ? a.rows[p] : a.perm[p];
+  if (j < 0) {  // pad slot of the run-aligned layout: zero taps
+    for (int k = 0; k < stride; ++k) out[k] = 0.0;
+    return;
+  }
   for (int t = 0; t < a.d; ++t) {
     double v = a.nodes[t * a.n + j];
     if (a.apply_rho) v = __dmul_rn(a.rho, v);
@@ -118,6 +125,7 @@ __global__ void taps_kernel(TapArgs a) {
       out[t * T + k] = kb_window(diff, a.m, a.M, a.b);
     }
   }
+  for (int k = a.d * T; k < stride; ++k) out[k] = 0.0;
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,364 @@
+// kernels_v6.cuh -- d = 3, 2m = 16 spread and interpolation over the
+// run-aligned slot layout (config 5: ~73 points per footprint).
+//
+// The plan lays every item's runs (points sharing one footprint) out in a
+// slot space where each run starts on a multiple of 8 slots; the pad slots
+// map to no point (slots[s] = -1: zero taps, x = 0, no output).  K-steps of
+// 4 slots (spread) and batches of 8 slots (interpolation) then never
+// straddle two runs, so the inner loops carry no per-lane run masks, no run
+// cursor compares and no partial-batch re-runs (v5: a batch crossing a run
+// boundary ran the whole footprint twice; ~10 % of the interpolation's
+// DMMAs at config 5).
+//
+// Spread, per run and K-step of 4 slots (points k):
+//   G[a][(c, e)] += sum_k wa_k[a] * ((x_k wc_k[c]) we_k[e])
+//   A = wa (8 a x 4 points, straight from the staged taps, no product),
+//   B = (x wc) we (4 points x 8 e of one c): one DMUL per fragment.
+// x is folded into wc once per staged slot (in place, after the chunk lands),
+// so a warp's K-step is 6 LDS + 4 DMUL +
+// 8 DMMA (v5: 8 LDS + 6 DMUL, plus the lane masks).  Warp w owns the box
+// c-rows = w (mod 8): in a run with origin o1 its two c values are
+// c0 = (w - o1) mod 8 and c0 + 8, both a-tiles and both e-halves (16
+// accumulators per lane); flushes of consecutive runs never touch another
+// warp's rows, so no barrier per run.
+//
+// Interpolation: the v5 kernel (per-warp 8-point batches, B fragments from
+// the bank-padded box) with one run per batch.
+//
+// Staging is TMA bulk copies (cp.async.bulk, completion on mbarriers): the
+// plan stores the taps in slot order with rows padded to the staged row
+// stride (52 doubles), so a spread chunk (64 slots, 26.6 KB) and an
+// interpolation batch (8 slots, 3.3 KB) are one contiguous copy each, issued
+// by one thread, with no per-thread address math and no dependent index
+// loads in the staging path.  The spread's x comes pre-gathered in slot order
+// (slot_gather_kernel: one pass over the block, pads 0, s applied).
+#pragma once
+
+#include "kernels_v5.cuh"
+
+namespace fgsb {
+
+constexpr int kSlotAlign = 8;  // run starts in the slot space
+constexpr int kSlotRow = 52;   // doubles per slot-ordered taps row: wa | wc | we | 4 pad (= 4 mod 16)
+
+// ---- bulk-copy (TMA) staging with mbarrier completion ----------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// generic-proxy shared-memory accesses before -> async-proxy (bulk copy) after
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// global -> shared bulk copy (bytes % 16 == 0, both addresses 16-byte aligned), completes on mbar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+
+struct Blk6s {
+  static constexpr int T = 16;
+  static constexpr int W = 8;       // warps; warp w owns box c-rows = w (mod 8)
+  static constexpr int NT = 32 * W;
+  static constexpr int QS = 64;     // slots per staged chunk (multiple of kSlotAlign)
+  // staged slot row = the global slot-ordered taps row: wa[16] | wc[16] |
+  // we[16] | pad; 52 = 4 (mod 16) doubles -> the 4 slots of a K-step sit on
+  // distinct bank groups
+  static constexpr int SR = kSlotRow;
+};
+
+// staging doubles beyond the box: taps [2][QS][SR] | x [2][QS] | 2 mbarriers
+constexpr size_t v6s_extra_doubles() {
+  return 2 * static_cast<size_t>(Blk6s::QS) * Blk6s::SR + 2 * Blk6s::QS + 2;
+}
+
+// the vectors gathered into slot order for the spread: xs[v][s] = s[src] x[src]
+// (scale_input) or x[src], 0 on pad slots (v2_x over the slot map)
+__global__ void slot_gather_kernel(PassArgs a, int64_t nslots, double* out) {
+  pdl_wait();
+  const int64_t total = nslots * a.nvec;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = i / nslots, sl = i - v * nslots;
+    const int src = a.slots[sl];
+    double val = 0.0;
+    if (src >= 0) {
+      const int64_t ix = a.perm ? static_cast<int64_t>(a.perm[src]) : src;
+      val = a.x[v * a.ldx + ix];
+      if (a.scale_input) val = __dmul_rn(a.s[src], val);
+    }
+    out[v * nslots + sl] = val;
+  }
+}
+
+__global__ void __launch_bounds__(Blk6s::NT, 2) spread_v6_kernel(PassArgs a, int box_stride_smem) {
+  pdl_wait();
+  using B = Blk6s;
+  constexpr int T = B::T, NT = B::NT, QS = B::QS, SR = B::SR;
+  extern __shared__ __align__(16) double smem[];
+  double* S = smem;
+  double* stg = smem + box_stride_smem;
+  double* xst = stg + 2 * QS * SR;
+  unsigned long long* mb = reinterpret_cast<unsigned long long*>(xst + 2 * QS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, r8 = lane >> 2;
+  const DItem it = a.items[blockIdx.x];
+  const int bx1 = it.e1, bx2 = it.e2;
+  const int V = it.e0 * bx1 * bx2;
+  const int s_begin = it.p_begin, s_end = it.p_end;  // slots, multiples of kSlotAlign
+  const int nch = (s_end - s_begin + QS - 1) / QS;
+  const int fs = tid >> 2, fq = tid & 3;  // fold: slot fs of the chunk, wc quarter fq
+
+  if (tid == 0) {
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  // one bulk copy of the chunk's taps rows and one of its slot-ordered x
+  auto issue = [&](unsigned g, const double* xsv, int c0, int cnt) {
+    const int b = static_cast<int>(g & 1u);
+    fence_proxy_async();
+    mbar_expect_tx(&mb[b], static_cast<unsigned>(cnt) * (SR + 1) * 8u);
+    bulk_g2s(stg + b * QS * SR, a.taps + static_cast<int64_t>(c0) * SR, static_cast<unsigned>(cnt) * SR * 8u, &mb[b]);
+    bulk_g2s(xst + b * QS, xsv + c0, static_cast<unsigned>(cnt) * 8u, &mb[b]);
+  };
+
+  unsigned g = 0;  // chunks consumed so far (all vectors): buffer g & 1, phase (g >> 1) & 1
+  for (int vec = 0; vec < a.nvec; ++vec) {
+    const double* xsv = a.xs + vec * a.ldxs;
+    if (vec > 0) __syncthreads();  // the previous vector's box has been written out
+    if (tid == 0) issue(g, xsv, s_begin, min(QS, s_end - s_begin));
+    for (int v = tid; v < V; v += NT) S[v] = 0.0;
+    int r = it.run_begin;
+    DRun run = a.runs[r];
+    int cur = run.pstart;                             // K-step cursor (slots)
+    int kend = run.pstart + ((run.pcount + 3) & ~3);  // the run's last K-step end
+    int cw = (warp - ((run.off >> 10) & 1023)) & 7;   // this warp's first c in the run
+    double C[2][2][2][2];  // [a-tile][c][e-half][pair]
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) C[t][c][h][0] = C[t][c][h][1] = 0.0;
+
+    auto flush = [&]() {
+      const int o0 = run.off & 1023, o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          double* row = S + ((o0 + 8 * t + r8) * bx1 + (o1 + cw + 8 * c)) * bx2 + o2 + 2 * q;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            row[8 * h] += C[t][c][h][0];
+            row[8 * h + 1] += C[t][c][h][1];
+            C[t][c][h][0] = C[t][c][h][1] = 0.0;
+          }
+        }
+    };
+
+    bool done = false;
+    for (int k = 0; k < nch; ++k, ++g) {
+      const int c0 = s_begin + k * QS;
+      const int cend = min(c0 + QS, s_end);
+      const int b = static_cast<int>(g & 1u);
+      double* buf = stg + b * QS * SR;
+      mbar_wait(&mb[b], (g >> 1) & 1u);
+      if (fs < cend - c0) {  // x wc, in place: this thread's 4 wc taps of slot fs
+        double2* w2 = reinterpret_cast<double2*>(buf + fs * SR + T + 4 * fq);
+        const double xv = xst[b * QS + fs];
+        const double2 lo = w2[0], hi = w2[1];
+        w2[0] = make_double2(xv * lo.x, xv * lo.y);
+        w2[1] = make_double2(xv * hi.x, xv * hi.y);
+      }
+      fence_proxy_async();
+      __syncthreads();  // chunk k folded; chunk k-1's buffer free
+      if (tid == 0 && k + 1 < nch) issue(g + 1, xsv, cend, min(QS, s_end - cend));
+      if (done) continue;
+      while (true) {
+        const int stop = min(kend, cend);
+        const double* row = buf + (cur - c0 + q) * SR;
+        for (; cur < stop; cur += 4, row += 4 * SR) {
+          const double a0 = row[r8], a1 = row[8 + r8];
+          const double x0 = row[T + cw], x1 = row[T + cw + 8];
+          const double e0 = row[2 * T + r8], e1 = row[2 * T + 8 + r8];
+          const double b00 = x0 * e0, b01 = x0 * e1, b10 = x1 * e0, b11 = x1 * e1;
+          dmma(C[0][0][0][0], C[0][0][0][1], a0, b00);
+          dmma(C[1][0][0][0], C[1][0][0][1], a1, b00);
+          dmma(C[0][0][1][0], C[0][0][1][1], a0, b01);
+          dmma(C[1][0][1][0], C[1][0][1][1], a1, b01);
+          dmma(C[0][1][0][0], C[0][1][0][1], a0, b10);
+          dmma(C[1][1][0][0], C[1][1][0][1], a1, b10);
+          dmma(C[0][1][1][0], C[0][1][1][1], a0, b11);
+          dmma(C[1][1][1][0], C[1][1][1][1], a1, b11);
+        }
+        if (cur < kend) break;  // the run continues in the next chunk
+        flush();
+        if (++r >= it.run_end) {
+          done = true;
+          break;
+        }
+        run = a.runs[r];
+        cur = run.pstart;
+        kend = run.pstart + ((run.pcount + 3) & ~3);
+        cw = (warp - ((run.off >> 10) & 1023)) & 7;
+        if (cur >= cend) break;
+      }
+    }
+    __syncthreads();
+    double* out = a.priv + (static_cast<int64_t>(vec) * gridDim.x + blockIdx.x) * a.box_stride;
+    for (int v = tid; v < V; v += NT) out[v] = S[v];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// interpolation over run-aligned 8-slot batches (see kernels_v5.cuh for the
+// fragment layout); each warp stages its next batch's 8 taps rows with one
+// bulk copy on its own mbarrier pair (double buffer)
+// ---------------------------------------------------------------------------
+template <int T>
+constexpr size_t v6i_extra_doubles() {
+  return v5_extra_doubles<T>() + 2 * static_cast<size_t>(Blk5<T>::W);
+}
+
+template <int T>
+__global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a, int box_doubles) {
+  pdl_wait();
+  using B = Blk5<T>;
+  constexpr int TA = B::TA, TC = B::TC, KS = B::KS, W = B::W, NT = B::NT, SR = B::STRIDE;
+  static_assert(SR == kSlotRow, "staged row = global slot-ordered row");
+  extern __shared__ __align__(16) double smem[];
+  double* S = smem;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, r8 = lane >> 2;
+  double* slots = smem + box_doubles + static_cast<size_t>(warp) * 2 * B::SLOT;
+  unsigned long long* mb =
+      reinterpret_cast<unsigned long long*>(smem + box_doubles + static_cast<size_t>(W) * 2 * B::SLOT) + 2 * warp;
+  const DItem it = a.items[blockIdx.x];
+  const int bx1 = it.e1, e2 = it.e2, sp2 = v5_pad(e2);
+  const int rows = it.e0 * it.e1;
+  const int M = a.M;
+  const int s_begin = it.p_begin;
+  const int nb = (it.p_end - s_begin) / 8;  // 8-slot batches of the item
+  const int ra = 2 * bx1 * sp2, rc = 4 * sp2;
+  if (lane == 0) {
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  auto issue = [&](unsigned g, int batch) {  // lane 0
+    const int b = static_cast<int>(g & 1u);
+    fence_proxy_async();
+    mbar_expect_tx(&mb[b], 8u * SR * 8u);
+    bulk_g2s(slots + b * B::SLOT, a.taps + static_cast<int64_t>(s_begin + 8 * batch) * SR, 8u * SR * 8u, &mb[b]);
+  };
+
+  unsigned g = 0;  // batches this warp consumed (all vectors): buffer g & 1, phase (g >> 1) & 1
+  for (int vec = 0; vec < a.nvec; ++vec) {
+    const double* gv = a.grid + vec * a.grid_stride;
+    const double* xv = a.x ? a.x + vec * a.ldx : nullptr;
+    double* yv = a.y ? a.y + vec * a.ldy : nullptr;
+    if (warp < nb && lane == 0) issue(g, warp);
+    if (vec > 0) __syncthreads();  // every warp is done with the previous vector's box
+    for (int v = tid; v < rows * e2; v += NT) {
+      const int row = v / e2, x2 = v - row * e2;
+      const int x0 = row / bx1, x1 = row - x0 * bx1;
+      S[row * sp2 + x2] = gv[(static_cast<int64_t>((it.a0 + x0) % M) * M + (it.a1 + x1) % M) * M + (it.a2 + x2) % M];
+    }
+    __syncthreads();
+
+    int r = it.run_begin;
+    for (int bt = warp; bt < nb; bt += W, ++g) {
+      const int b0 = s_begin + 8 * bt;
+      if (bt + W < nb && lane == 0) issue(g + 1, bt + W);
+      // the run holding this batch (runs are 8-aligned in slot order; the
+      // cursor only moves forward with the warp's batches)
+      while (a.runs[r].pstart + a.runs[r].pcount <= b0) ++r;
+      const DRun run = a.runs[r];
+      const int src = a.slots[b0 + r8];  // this lane's point (-1: pad slot)
+      double xin = 0.0, sin_ = 1.0;
+      if (q == 0 && src >= 0) {
+        if (xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE)
+          xin = xv[a.perm ? static_cast<int64_t>(a.perm[src]) : src];
+        if (a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN) sin_ = a.s[src];
+      }
+      mbar_wait(&mb[g & 1u], (g >> 1) & 1u);
+      const double* w = slots + (g & 1u) * B::SLOT + r8 * SR;
+      double wa[TA], wc[TC][2], aF[KS];
+#pragma unroll
+      for (int t = 0; t < TA; ++t) wa[t] = w[2 * t + (q >> 1)];
+#pragma unroll
+      for (int t = 0; t < TC; ++t) {
+        wc[t][0] = w[T + 4 * t + 2 * (q & 1)];
+        wc[t][1] = w[T + 4 * t + 2 * (q & 1) + 1];
+      }
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) aF[ks] = w[2 * T + 4 * ks + q];  // zero on pad slots
+      const int o0 = run.off & 1023, o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
+      const double* gb = S + ((o0 + (r8 >> 2)) * bx1 + (o1 + (r8 & 3))) * sp2 + o2 + q;
+      double yacc = 0.0;
+#pragma unroll
+      for (int ta = 0; ta < TA; ++ta) {
+        double z[TC][2];
+#pragma unroll
+        for (int tc = 0; tc < TC; ++tc) z[tc][0] = z[tc][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+          for (int tc = 0; tc < TC; ++tc) dmma(z[tc][0], z[tc][1], aF[ks], gb[ta * ra + tc * rc + 4 * ks]);
+        double K = 0.0;
+#pragma unroll
+        for (int tc = 0; tc < TC; ++tc) {
+          K = fma(wc[tc][0], z[tc][0], K);
+          K = fma(wc[tc][1], z[tc][1], K);
+        }
+        yacc = fma(wa[ta], K, yacc);
+      }
+      yacc += __shfl_xor_sync(0xffffffffu, yacc, 1);
+      yacc += __shfl_xor_sync(0xffffffffu, yacc, 2);
+      if (q == 0 && src >= 0) {
+        const double val = yacc;
+        if (a.epilogue == EPI_DEGREE) {
+          const double dg = val - a.k0;  // graphop.cpp:55-56
+          a.degrees[src] = dg;
+          a.inv_sqrt[src] = 1.0 / sqrt(dg);
+          if (!(dg > 0.0)) atomicMin(a.bad_flag, static_cast<unsigned long long>(a.caller[src]));
+        } else {
+          double out;
+          switch (a.epilogue) {
+            case EPI_KERNEL: out = val; break;
+            case EPI_WEIGHT: out = val - a.k0 * xin; break;
+            case EPI_NORMALIZED: out = sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
+            default: out = xin - sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
+          }
+          yv[a.perm ? static_cast<int64_t>(a.perm[src]) : src] = out;
+        }
+      }
+      __syncwarp();  // the buffer is restaged by the next-but-one batch
+    }
+  }
+}
+
+}  // namespace fgsb

@@ -1,8 +1,8 @@
 """Full-size GPU parity against the reference path on the production kernels.
 
 * Config 5 at its full size (10M points, 2m = 16): the production fp64
-  tensor-core spread / interpolation (`spread_v4_kernel<16>` with two point
-  streams, `interp_v4_kernel<16>`) in a multi-vector block, against the CPU
+  tensor-core spread / interpolation over the run-aligned slot layout
+  (`spread_v6_kernel`, `interp_v6_kernel<16>`) in a multi-vector block, against the CPU
   oracle (pinned bit for bit to the reference binary, tests/test_ref_pin.py)
   at the north-star matvec tolerance rel-l2 <= 1e-10.  The oracle's NFFT loops
   run on all host cores here (orc.threads; per-thread spread grids summed in
@@ -47,6 +47,7 @@ def test_config5_full_size_block_matches_oracle(orc):
     op = _op(X, info)
     st = op.plan_stats()
     assert st["tensor_spread"] and st["tensor_interp"], st  # the production DMMA kernels
+    assert st["slot_layout"] and st["slots"] < 1.1 * X.shape[0], st  # run-aligned slots (kernels_v6.cuh)
     xs = fgs.workload_vectors(X.shape[0], 2, 99)
     Y = op.apply_sym_laplacian(xs)  # one 2-vector block through the multi-vector kernels
     deg = op.degrees()
@@ -70,6 +71,7 @@ def test_dense_cells_block_matches_oracle(orc, m, N):
     op = _op(X, info)
     st = op.plan_stats()
     assert st["tensor_spread"] and st["tensor_interp"] and st["mean_run"] >= 12.0, st
+    assert st["slot_layout"] == (m == 8), st
     xs = rng.standard_normal((n, 4))
     Y = op.apply_sym_laplacian(np.asfortranarray(xs))
     # the block equals its column-wise applies bit for bit
