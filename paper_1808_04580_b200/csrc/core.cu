@@ -941,6 +941,15 @@ void Core::build_plan(const double* nodes_colmajor) {
     items6.upload(sitems.data(), sitems.size(), stream);
     runs6.upload(sruns.data(), sruns.size(), stream);
     slot_map.upload(smap.data(), smap.size(), stream);
+    std::vector<int> boff(static_cast<size_t>(sl / kSlotAlign));
+    for (const DItem& it : sitems)
+      for (int r = it.run_begin; r < it.run_end; ++r) {
+        const DRun& sr = sruns[static_cast<size_t>(r)];
+        const int padded = (sr.pcount + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
+        for (int b = sr.pstart / kSlotAlign; b < (sr.pstart + padded) / kSlotAlign; ++b)
+          boff[static_cast<size_t>(b)] = sr.off;
+      }
+    batch_off.upload(boff.data(), boff.size(), stream);
     use_slots = true;
   }
   items.upload(ditems.data(), ditems.size(), stream);
@@ -1361,6 +1370,7 @@ void Core::pass_layout(PassArgs& a) const {
     a.items = items6.p;
     a.runs = runs6.p;
     a.slots = slot_map.p;
+    a.boff = batch_off.p;
   } else {
     a.items = items.p;
     a.runs = runs.p;

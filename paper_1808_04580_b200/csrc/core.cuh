@@ -129,6 +129,7 @@ class Core {
   DBuf<DItem> items6;
   DBuf<DRun> runs6;
   DBuf<int> slot_map;
+  DBuf<int> batch_off;  // per 8-slot batch: its run's packed footprint offset
   std::vector<int> slot_host;  // plan-time copy (freed once the taps are built)
   bool use_slots = false;
   void pass_layout(PassArgs& a) const;

@@ -65,6 +65,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
 // generic-proxy shared-memory accesses before -> async-proxy (bulk copy) after
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 // global -> shared bulk copy (bytes % 16 == 0, both addresses 16-byte aligned), completes on mbar
@@ -79,16 +82,17 @@ struct Blk6s {
   static constexpr int T = 16;
   static constexpr int W = 8;       // warps; warp w owns box c-rows = w (mod 8)
   static constexpr int NT = 32 * W;
-  static constexpr int QS = 64;     // slots per staged chunk (multiple of kSlotAlign)
+  static constexpr int QS = 32;     // slots per staged chunk (multiple of kSlotAlign)
+  static constexpr int NS = 4;      // ring stages
   // staged slot row = the global slot-ordered taps row: wa[16] | wc[16] |
   // we[16] | pad; 52 = 4 (mod 16) doubles -> the 4 slots of a K-step sit on
   // distinct bank groups
   static constexpr int SR = kSlotRow;
 };
 
-// staging doubles beyond the box: taps [2][QS][SR] | x [2][QS] | 2 mbarriers
+// staging doubles beyond the box: taps [NS][QS][SR] | x [NS][QS] | full[NS] | empty[NS]
 constexpr size_t v6s_extra_doubles() {
-  return 2 * static_cast<size_t>(Blk6s::QS) * Blk6s::SR + 2 * Blk6s::QS + 2;
+  return static_cast<size_t>(Blk6s::NS) * Blk6s::QS * (Blk6s::SR + 1) + 2 * Blk6s::NS;
 }
 
 // the vectors gathered into slot order for the spread: xs[v][s] = s[src] x[src]
@@ -113,12 +117,13 @@ __global__ void slot_gather_kernel(PassArgs a, int64_t nslots, double* out) {
 __global__ void __launch_bounds__(Blk6s::NT, 2) spread_v6_kernel(PassArgs a, int box_stride_smem) {
   pdl_wait();
   using B = Blk6s;
-  constexpr int T = B::T, NT = B::NT, QS = B::QS, SR = B::SR;
+  constexpr int T = B::T, NT = B::NT, QS = B::QS, SR = B::SR, NS = B::NS, W = B::W;
   extern __shared__ __align__(16) double smem[];
   double* S = smem;
   double* stg = smem + box_stride_smem;
-  double* xst = stg + 2 * QS * SR;
-  unsigned long long* mb = reinterpret_cast<unsigned long long*>(xst + 2 * QS);
+  double* xst = stg + NS * QS * SR;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(xst + NS * QS);
+  unsigned long long* empty = full + NS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = lane & 3, r8 = lane >> 2;
   const DItem it = a.items[blockIdx.x];
@@ -126,29 +131,34 @@ __global__ void __launch_bounds__(Blk6s::NT, 2) spread_v6_kernel(PassArgs a, int
   const int V = it.e0 * bx1 * bx2;
   const int s_begin = it.p_begin, s_end = it.p_end;  // slots, multiples of kSlotAlign
   const int nch = (s_end - s_begin + QS - 1) / QS;
-  const int fs = tid >> 2, fq = tid & 3;  // fold: slot fs of the chunk, wc quarter fq
+  const int total = nch * a.nvec;  // chunks of the whole kernel (vector-major)
 
   if (tid == 0) {
-    mbar_init(&mb[0], 1);
-    mbar_init(&mb[1], 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], W);
+    }
     mbar_init_fence();
   }
   __syncthreads();
-  // one bulk copy of the chunk's taps rows and one of its slot-ordered x
-  auto issue = [&](unsigned g, const double* xsv, int c0, int cnt) {
-    const int b = static_cast<int>(g & 1u);
+  // producer (thread 0): chunk g = (vector g / nch, chunk g % nch) -> stage g % NS
+  auto issue = [&](int g) {
+    const int st = g % NS, vec = g / nch, c0 = s_begin + (g - vec * nch) * QS;
+    const int cnt = min(QS, s_end - c0);
     fence_proxy_async();
-    mbar_expect_tx(&mb[b], static_cast<unsigned>(cnt) * (SR + 1) * 8u);
-    bulk_g2s(stg + b * QS * SR, a.taps + static_cast<int64_t>(c0) * SR, static_cast<unsigned>(cnt) * SR * 8u, &mb[b]);
-    bulk_g2s(xst + b * QS, xsv + c0, static_cast<unsigned>(cnt) * 8u, &mb[b]);
+    mbar_expect_tx(&full[st], static_cast<unsigned>(cnt) * (SR + 1) * 8u);
+    bulk_g2s(stg + st * QS * SR, a.taps + static_cast<int64_t>(c0) * SR, static_cast<unsigned>(cnt) * SR * 8u,
+             &full[st]);
+    bulk_g2s(xst + st * QS, a.xs + vec * a.ldxs + c0, static_cast<unsigned>(cnt) * 8u, &full[st]);
   };
+  if (tid == 0)
+    for (int g = 0; g < NS - 1 && g < total; ++g) issue(g);
 
-  unsigned g = 0;  // chunks consumed so far (all vectors): buffer g & 1, phase (g >> 1) & 1
+  int g = 0;  // chunk being consumed
   for (int vec = 0; vec < a.nvec; ++vec) {
-    const double* xsv = a.xs + vec * a.ldxs;
     if (vec > 0) __syncthreads();  // the previous vector's box has been written out
-    if (tid == 0) issue(g, xsv, s_begin, min(QS, s_end - s_begin));
     for (int v = tid; v < V; v += NT) S[v] = 0.0;
+    __syncthreads();  // flushes of this vector may start as soon as a warp finishes its first run
     int r = it.run_begin;
     DRun run = a.runs[r];
     int cur = run.pstart;                             // K-step cursor (slots)
@@ -180,53 +190,55 @@ __global__ void __launch_bounds__(Blk6s::NT, 2) spread_v6_kernel(PassArgs a, int
 
     bool done = false;
     for (int k = 0; k < nch; ++k, ++g) {
+      // keep NS - 1 chunks in flight: chunk g + NS - 1 reuses the stage of
+      // chunk g - 1, free once every warp has released it
+      if (tid == 0 && g + NS - 1 < total) {
+        if (g >= 1) mbar_wait(&empty[(g - 1) % NS], ((g - 1) / NS) & 1);
+        issue(g + NS - 1);
+      }
       const int c0 = s_begin + k * QS;
       const int cend = min(c0 + QS, s_end);
-      const int b = static_cast<int>(g & 1u);
-      double* buf = stg + b * QS * SR;
-      mbar_wait(&mb[b], (g >> 1) & 1u);
-      if (fs < cend - c0) {  // x wc, in place: this thread's 4 wc taps of slot fs
-        double2* w2 = reinterpret_cast<double2*>(buf + fs * SR + T + 4 * fq);
-        const double xv = xst[b * QS + fs];
-        const double2 lo = w2[0], hi = w2[1];
-        w2[0] = make_double2(xv * lo.x, xv * lo.y);
-        w2[1] = make_double2(xv * hi.x, xv * hi.y);
-      }
-      fence_proxy_async();
-      __syncthreads();  // chunk k folded; chunk k-1's buffer free
-      if (tid == 0 && k + 1 < nch) issue(g + 1, xsv, cend, min(QS, s_end - cend));
-      if (done) continue;
-      while (true) {
-        const int stop = min(kend, cend);
-        const double* row = buf + (cur - c0 + q) * SR;
-        for (; cur < stop; cur += 4, row += 4 * SR) {
-          const double a0 = row[r8], a1 = row[8 + r8];
-          const double x0 = row[T + cw], x1 = row[T + cw + 8];
-          const double e0 = row[2 * T + r8], e1 = row[2 * T + 8 + r8];
-          const double b00 = x0 * e0, b01 = x0 * e1, b10 = x1 * e0, b11 = x1 * e1;
-          dmma(C[0][0][0][0], C[0][0][0][1], a0, b00);
-          dmma(C[1][0][0][0], C[1][0][0][1], a1, b00);
-          dmma(C[0][0][1][0], C[0][0][1][1], a0, b01);
-          dmma(C[1][0][1][0], C[1][0][1][1], a1, b01);
-          dmma(C[0][1][0][0], C[0][1][0][1], a0, b10);
-          dmma(C[1][1][0][0], C[1][1][0][1], a1, b10);
-          dmma(C[0][1][1][0], C[0][1][1][1], a0, b11);
-          dmma(C[1][1][1][0], C[1][1][1][1], a1, b11);
+      const int st = g % NS;
+      const double* buf = stg + st * QS * SR;
+      const double* xb = xst + st * QS;
+      mbar_wait(&full[st], (g / NS) & 1);
+      if (!done) {
+        while (true) {
+          const int stop = min(kend, cend);
+          const double* row = buf + (cur - c0 + q) * SR;
+          const double* xr = xb + (cur - c0 + q);
+          for (; cur < stop; cur += 4, row += 4 * SR, xr += 4) {
+            const double xv = *xr;
+            const double a0 = row[r8], a1 = row[8 + r8];
+            const double x0 = row[T + cw] * xv, x1 = row[T + cw + 8] * xv;
+            const double e0 = row[2 * T + r8], e1 = row[2 * T + 8 + r8];
+            const double b00 = x0 * e0, b01 = x0 * e1, b10 = x1 * e0, b11 = x1 * e1;
+            dmma(C[0][0][0][0], C[0][0][0][1], a0, b00);
+            dmma(C[1][0][0][0], C[1][0][0][1], a1, b00);
+            dmma(C[0][0][1][0], C[0][0][1][1], a0, b01);
+            dmma(C[1][0][1][0], C[1][0][1][1], a1, b01);
+            dmma(C[0][1][0][0], C[0][1][0][1], a0, b10);
+            dmma(C[1][1][0][0], C[1][1][0][1], a1, b10);
+            dmma(C[0][1][1][0], C[0][1][1][1], a0, b11);
+            dmma(C[1][1][1][0], C[1][1][1][1], a1, b11);
+          }
+          if (cur < kend) break;  // the run continues in the next chunk
+          flush();
+          if (++r >= it.run_end) {
+            done = true;
+            break;
+          }
+          run = a.runs[r];
+          cur = run.pstart;
+          kend = run.pstart + ((run.pcount + 3) & ~3);
+          cw = (warp - ((run.off >> 10) & 1023)) & 7;
+          if (cur >= cend) break;
         }
-        if (cur < kend) break;  // the run continues in the next chunk
-        flush();
-        if (++r >= it.run_end) {
-          done = true;
-          break;
-        }
-        run = a.runs[r];
-        cur = run.pstart;
-        kend = run.pstart + ((run.pcount + 3) & ~3);
-        cw = (warp - ((run.off >> 10) & 1023)) & 7;
-        if (cur >= cend) break;
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
-    __syncthreads();
+    __syncthreads();  // every warp's flushes are in the box
     double* out = a.priv + (static_cast<int64_t>(vec) * gridDim.x + blockIdx.x) * a.box_stride;
     for (int v = tid; v < V; v += NT) out[v] = S[v];
   }
@@ -289,21 +301,27 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a, i
     }
     __syncthreads();
 
-    int r = it.run_begin;
+    // per batch: its run's footprint offset (plan array, one per 8 slots) and
+    // this lane's point, loaded one batch ahead with the epilogue operands
+    const bool need_x = xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE;
+    const bool need_s = a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN;
+    int src_n = -1, off_n = 0;
+    if (warp < nb) {
+      src_n = a.slots[s_begin + 8 * warp + r8];
+      off_n = a.boff[(s_begin >> 3) + warp];
+    }
     for (int bt = warp; bt < nb; bt += W, ++g) {
-      const int b0 = s_begin + 8 * bt;
-      if (bt + W < nb && lane == 0) issue(g + 1, bt + W);
-      // the run holding this batch (runs are 8-aligned in slot order; the
-      // cursor only moves forward with the warp's batches)
-      while (a.runs[r].pstart + a.runs[r].pcount <= b0) ++r;
-      const DRun run = a.runs[r];
-      const int src = a.slots[b0 + r8];  // this lane's point (-1: pad slot)
-      double xin = 0.0, sin_ = 1.0;
-      if (q == 0 && src >= 0) {
-        if (xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE)
-          xin = xv[a.perm ? static_cast<int64_t>(a.perm[src]) : src];
-        if (a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN) sin_ = a.s[src];
+      const int src = src_n, off = off_n;
+      if (bt + W < nb) {
+        if (lane == 0) issue(g + 1, bt + W);
+        src_n = a.slots[s_begin + 8 * (bt + W) + r8];
+        off_n = a.boff[(s_begin >> 3) + bt + W];
       }
+      // epilogue operands (lane q == 0 of each real point; others read index 0)
+      const bool mine = q == 0 && src >= 0;
+      const int64_t ix = mine ? (a.perm ? static_cast<int64_t>(a.perm[src]) : src) : 0;
+      const double xin = need_x && mine ? xv[ix] : 0.0;
+      const double sin_ = need_s && mine ? a.s[src] : 1.0;
       mbar_wait(&mb[g & 1u], (g >> 1) & 1u);
       const double* w = slots + (g & 1u) * B::SLOT + r8 * SR;
       double wa[TA], wc[TC][2], aF[KS];
@@ -316,7 +334,7 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a, i
       }
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) aF[ks] = w[2 * T + 4 * ks + q];  // zero on pad slots
-      const int o0 = run.off & 1023, o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
+      const int o0 = off & 1023, o1 = (off >> 10) & 1023, o2 = (off >> 20) & 1023;
       const double* gb = S + ((o0 + (r8 >> 2)) * bx1 + (o1 + (r8 & 3))) * sp2 + o2 + q;
       double yacc = 0.0;
 #pragma unroll
@@ -338,7 +356,7 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a, i
       }
       yacc += __shfl_xor_sync(0xffffffffu, yacc, 1);
       yacc += __shfl_xor_sync(0xffffffffu, yacc, 2);
-      if (q == 0 && src >= 0) {
+      if (mine) {
         const double val = yacc;
         if (a.epilogue == EPI_DEGREE) {
           const double dg = val - a.k0;  // graphop.cpp:55-56
@@ -353,7 +371,7 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a, i
             case EPI_NORMALIZED: out = sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
             default: out = xin - sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
           }
-          yv[a.perm ? static_cast<int64_t>(a.perm[src]) : src] = out;
+          yv[ix] = out;
         }
       }
       __syncwarp();  // the buffer is restaged by the next-but-one batch
