@@ -174,6 +174,27 @@ fgs_status fgs_measure_dmma_peak(int device, double* tflops);
 fgs_status fgs_adjacency_launch_count(fgs_adjacency_t h, int64_t* out);
 void fgs_adjacency_destroy(fgs_adjacency_t h);
 
+/* ---- single-GPU emulation of the N-rank sharded path ---------------------
+ * `world` shards of one operator (the plan slices, slab-pruned convolutions
+ * and exchange buffers that fgs_adjacency_create_sharded ranks 0..world-1
+ * build) on one device; every apply runs phase 1 on each shard, sums the
+ * shards' exchange buffers with a device kernel in place of ncclAllReduce,
+ * then phase 2.  Validation of the multi-GPU data path where fewer GPUs than
+ * ranks exist (no kernels that wait on one another share the GPU).  No
+ * reference counterpart: the reference is serial (README.md:85-91). */
+typedef struct fgs_shard_group* fgs_shard_group_t;
+fgs_status fgs_shard_group_create(const double* nodes_colmajor, int64_t n, int d, fgs_kernel kernel, double shape,
+                                  const fgs_fastsum_params* params, int device, int world, fgs_shard_group_t* out,
+                                  int64_t* bad_node);
+/* y = op(x), full-length device vectors in caller order, column j at x + j ld */
+fgs_status fgs_shard_group_apply_device(fgs_shard_group_t g, fgs_op op, const double* dx, double* dy, int nvec,
+                                        int64_t ld);
+/* shard `rank`: points owned, first dim-0 plane and plane count of its
+ * pruned convolution (M planes when unpruned), work items */
+fgs_status fgs_shard_group_stats(fgs_shard_group_t g, int rank, int64_t* n_local, int* conv_plane0,
+                                 int* conv_planes, int* items);
+void fgs_shard_group_destroy(fgs_shard_group_t g);
+
 /* ---- lanczos_largest (spectral.hpp:68-70, spectral.cpp:141-256) ---------
  * Device-resident Lanczos with full two-pass reorthogonalisation on the
  * operator `which` (0: A = apply_normalized as adjacency_handle does,

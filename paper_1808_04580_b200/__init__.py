@@ -459,6 +459,43 @@ def nccl_unique_id() -> bytes:
 
 
 # ---- spectral (spectral.hpp:33-70) --------------------------------------
+class ShardGroup:
+    """Single-GPU emulation of the N-rank sharded path (fgs_shard_group_*):
+    `world` shards of one operator on one device, the ranks' exchange summed
+    by a device kernel between the two apply phases.  Validates the
+    multi-GPU data path (plan slices, slab-pruned convolutions, exchange
+    layout) where fewer GPUs than ranks exist."""
+
+    def __init__(self, nodes, kernel: KernelSpec, params: FastsumParams = None, device=0, world=2):
+        params = params or FastsumParams()
+        nd, n, d = _nodes(nodes)
+        h = C.c_void_p()
+        bad = C.c_int64(-1)
+        cp = params._c()
+        st = lib().fgs_shard_group_create(_dp(nd), C.c_int64(n), int(d), int(kernel.family),
+                                          C.c_double(kernel.shape), C.byref(cp), int(device), int(world),
+                                          C.byref(h), C.byref(bad))
+        _check(st, bad.value)
+        self._h = h
+        self._n, self.world = n, world
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().fgs_shard_group_destroy(self._h)
+            self._h = None
+
+    def apply_device(self, op, dx_ptr: int, dy_ptr: int, nvec=1, ld=None):
+        """y = op(x) for full-length device vectors in caller order."""
+        ld = ld if ld is not None else self._n
+        _check(lib().fgs_shard_group_apply_device(self._h, int(op), C.c_void_p(dx_ptr), C.c_void_p(dy_ptr),
+                                                  int(nvec), C.c_int64(ld)))
+
+    def stats(self, rank: int) -> dict:
+        nl, p0, pn, it = C.c_int64(), C.c_int(), C.c_int(), C.c_int()
+        _check(lib().fgs_shard_group_stats(self._h, int(rank), C.byref(nl), C.byref(p0), C.byref(pn), C.byref(it)))
+        return dict(n_local=nl.value, conv_plane0=p0.value, conv_planes=pn.value, items=it.value)
+
+
 @dataclass
 class LanczosOptions:
     max_iter: int = 1000

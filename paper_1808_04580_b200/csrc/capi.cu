@@ -26,6 +26,9 @@ struct fgs_fastsum {
 struct fgs_adjacency {
   std::unique_ptr<Core> core;
 };
+struct fgs_shard_group {
+  std::unique_ptr<fgsb::ShardGroup> group;
+};
 
 namespace {
 
@@ -506,6 +509,55 @@ fgs_status fgs_lanczos_stats(fgs_adjacency_t h, double* out4) {
 }
 
 void fgs_adjacency_destroy(fgs_adjacency_t h) { delete h; }
+
+// ---- single-GPU shard-group emulation of the N-rank path --------------------
+fgs_status fgs_shard_group_create(const double* nodes, int64_t n, int d, fgs_kernel kernel, double shape,
+                                  const fgs_fastsum_params* params, int device, int world, fgs_shard_group_t* out,
+                                  int64_t* bad_node) {
+  return guard([&] {
+    need(out, "out");
+    *out = nullptr;
+    if (bad_node) *bad_node = -1;
+    if (n < 2) fail(FGS_ESHAPE, "adjacency operator needs at least two nodes");  // graphop.cpp:39-42
+    if (d < 1 || d > 3) fail(FGS_EPARAM, "node dimension must be 1, 2, or 3");
+    need(nodes, "nodes");
+    auto g = std::make_unique<fgs_shard_group>();
+    g->group = std::make_unique<fgsb::ShardGroup>(nodes, n, d, spec_of(kernel, shape), to_params(params), device,
+                                                  world, bad_node);
+    *out = g.release();
+  });
+}
+
+fgs_status fgs_shard_group_apply_device(fgs_shard_group_t g, fgs_op op, const double* dx, double* dy, int nvec,
+                                        int64_t ld) {
+  return guard([&] {
+    need(g, "group");
+    if (nvec < 1) fail(FGS_ESHAPE, "nvec must be >= 1");
+    if (ld < g->group->n) fail(FGS_ESHAPE, "input length does not match operator dimension");
+    need(dx, "x");
+    need(dy, "y");
+    bool scale = false;
+    const int epi = epilogue_of(op, &scale);
+    FGS_CUDA(cudaSetDevice(g->group->device));
+    g->group->apply(epi, dx, dy, ld, nvec, scale);
+    FGS_CUDA(cudaStreamSynchronize(g->group->stream));
+  });
+}
+
+fgs_status fgs_shard_group_stats(fgs_shard_group_t g, int rank, int64_t* n_local, int* conv_plane0,
+                                 int* conv_planes, int* items) {
+  return guard([&] {
+    need(g, "group");
+    if (rank < 0 || rank >= static_cast<int>(g->group->shards.size())) fail(FGS_EPARAM, "rank out of range");
+    const Core& c = *g->group->shards[static_cast<size_t>(rank)];
+    if (n_local) *n_local = c.n_local;
+    if (conv_plane0) *conv_plane0 = c.conv_plane0;
+    if (conv_planes) *conv_planes = c.conv_planes;
+    if (items) *items = c.nitems;
+  });
+}
+
+void fgs_shard_group_destroy(fgs_shard_group_t g) { delete g; }
 
 // ---- lanczos_largest -------------------------------------------------------
 fgs_status fgs_lanczos_largest(fgs_adjacency_t h, int which, int k, int max_iter, double tol, uint64_t seed,

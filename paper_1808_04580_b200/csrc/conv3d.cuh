@@ -35,7 +35,7 @@ struct Conv3Args {
   const cufftDoubleComplex* mult; // compact window multiplier [N+1][N+1][H]
   const double2* tw;              // tw[j] = e^{-2 pi i j / M}
   int M, N, nvec;
-  int plane0, planes;             // planes [plane0, plane0 + planes) of this launch
+  int plane0, planes;             // planes plane0 .. plane0 + planes - 1 (mod M) of this launch
   int64_t grid_stride;
 };
 
@@ -65,7 +65,7 @@ template <int M>
 __global__ void __launch_bounds__(kConv3Threads) conv3_planes_fwd_kernel(Conv3Args a) {
   extern __shared__ double2 sm3[];
   const int N = a.N, H = N / 2 + 1, hN = N / 2, NW = conv3_nw(M, N);
-  const int u0 = a.plane0 + static_cast<int>(blockIdx.x) % a.planes;
+  const int u0 = (a.plane0 + static_cast<int>(blockIdx.x) % a.planes) & (M - 1);  // cyclic slab
   const int v = static_cast<int>(blockIdx.x) / a.planes;
   double2* tws = sm3;
   double2* X = tws + M;
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kConv3Threads) conv3_lines_kernel(Conv3Args a,
     fft_batch<M, false>(
         scr, nl, tws,
         [&](int s, int u) {
-          return (u >= a.plane0 && u < a.plane0 + a.planes) ? w[static_cast<int64_t>(u) * L + l0 + s]
+          return (((u - a.plane0) & (M - 1)) < a.planes) ? w[static_cast<int64_t>(u) * L + l0 + s]
                                                             : make_double2(0.0, 0.0);
         },
         [&](int s, int q, double2 f) {
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kConv3Threads) conv3_lines_kernel(Conv3Args a,
   fft_batch<M, true>(
       scr, nl, tws, [&](int s, int q) { return buf[s * M + q]; },
       [&](int s, int u, double2 y) {
-        if (u >= a.plane0 && u < a.plane0 + a.planes) w[static_cast<int64_t>(u) * L + l0 + s] = y;
+        if (((u - a.plane0) & (M - 1)) < a.planes) w[static_cast<int64_t>(u) * L + l0 + s] = y;
       });
 }
 
@@ -171,7 +171,7 @@ template <int M>
 __global__ void __launch_bounds__(kConv3Threads) conv3_planes_inv_kernel(Conv3Args a) {
   extern __shared__ double2 sm3[];
   const int N = a.N, H = N / 2 + 1, hN = N / 2, NW = conv3_nw(M, N);
-  const int u0 = a.plane0 + static_cast<int>(blockIdx.x) % a.planes;
+  const int u0 = (a.plane0 + static_cast<int>(blockIdx.x) % a.planes) & (M - 1);  // cyclic slab
   const int v = static_cast<int>(blockIdx.x) / a.planes;
   double2* tws = sm3;
   double2* X = tws + M;

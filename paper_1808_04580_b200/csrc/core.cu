@@ -839,11 +839,9 @@ void Core::build_plan(const double* nodes_colmajor) {
       best_start = (bs + bl) % M;
       best_len = M - bl;
     }
-    // the kernels take a non-wrapping range: wrap-around slabs convolve all planes
-    if (best_start + best_len <= M) {
-      conv_plane0 = best_start;
-      conv_planes = best_len;
-    }
+    // cyclic plane range (a point cloud centred on 0 wraps around plane 0)
+    conv_plane0 = best_start;
+    conv_planes = best_len;
   }
   if (std::getenv("FGS_PLAN_STATS")) {  // tuning aid: item sizes and the per-CTA shared memory
     int64_t box_sum = 0, pts_max = 0, runs_max = 0;
@@ -1379,7 +1377,13 @@ void Core::pass_layout(PassArgs& a) const {
 }
 
 void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
-                          bool caller_order, bool scale_input) {
+                          bool caller_order, bool scale_input, int phases) {
+  // phases: 1 = up to the sharded exchange (spread, assembly, forward
+  // convolution part), 2 = after it (rest of the convolution, interpolation),
+  // 3 = both with the NCCL exchange between (emulated shard groups run 1 on
+  // every shard, sum the exchange buffers on the device, then run 2)
+  const bool pre = (phases & 1) != 0, post = (phases & 2) != 0;
+  const bool nccl_exchange = sharded && !emulated && pre && post;
   Workspace& w = workspace(nvec);
   if (kind == DIRECT) {
     direct_launches(w, epilogue, x, ldx, y, ldy, nvec, scale_input);
@@ -1412,7 +1416,7 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
 
   std::vector<cudaEvent_t> evs;
   if (profile_) mark(evs);
-  if (use_slots && nitems > 0) {  // the vectors in slot order for the v6 spread (pads 0, s applied)
+  if (pre && use_slots && nitems > 0) {  // the vectors in slot order for the v6 spread (pads 0, s applied)
     const int64_t ns = static_cast<int64_t>(slot_map.n);
     a.xs = w.xs.p;
     a.ldxs = ns;
@@ -1421,10 +1425,12 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
     ++launches;
     FGS_CUDA(cudaGetLastError());
   }
-  launch_spread(a);
-  if (profile_) mark(evs);
-  launch_assemble(w, nvec);
-  if (profile_) mark(evs);
+  if (pre) {
+    launch_spread(a);
+    if (profile_) mark(evs);
+    launch_assemble(w, nvec);
+    if (profile_) mark(evs);
+  }
   if (use_conv2d()) {
     // d = 2: one cluster launch (row FFTs / kept-column FFT + multiply +
     // inverse through DSMEM / inverse row FFTs), conv2d.cuh.  Sharded: the
@@ -1433,19 +1439,22 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
     // instead of the spectrum window: one launch instead of four)
     const double* conv_in = w.grid.p;
     if (sharded) {  // out of place: this rank's spread grid keeps its zero cells
-      nccl_check(nccl().all_reduce(w.grid.p, w.grid_sum.p, static_cast<size_t>(grid_elems) * nvec, ncclDouble,
-                                   ncclSum, comm, stream),
-                 "ncclAllReduce of the partial grids");
+      if (nccl_exchange)
+        nccl_check(nccl().all_reduce(w.grid.p, w.grid_sum.p, static_cast<size_t>(grid_elems) * nvec, ncclDouble,
+                                     ncclSum, comm, stream),
+                   "ncclAllReduce of the partial grids");
       conv_in = w.grid_sum.p;
     }
-    int logM = 0;
-    while ((1 << logM) < M) ++logM;
-    Conv2Args ca{conv_in, w.grid_out.p, mult.p, tw2.p, M, logM, N, nvec, grid_elems};
-    const size_t smem = conv2_smem(M, N);
-    set_smem(conv2_kernel_ptr(M), smem);
-    conv2_launch(ca, smem, stream);
-    ++launches;
-    FGS_CUDA(cudaGetLastError());
+    if (post) {
+      int logM = 0;
+      while ((1 << logM) < M) ++logM;
+      Conv2Args ca{conv_in, w.grid_out.p, mult.p, tw2.p, M, logM, N, nvec, grid_elems};
+      const size_t smem = conv2_smem(M, N);
+      set_smem(conv2_kernel_ptr(M), smem);
+      conv2_launch(ca, smem, stream);
+      ++launches;
+      FGS_CUDA(cudaGetLastError());
+    }
     if (profile_) {
       mark(evs);
       mark(evs);
@@ -1457,50 +1466,65 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
     // the forward and the inverse line passes
     Conv3Args ca{w.grid.p, w.grid_out.p, w.win.p, sharded ? w.cspec.p : nullptr, mult.p, tw2.p,
                  M, N, nvec, conv_plane0, conv_planes, grid_elems};
-    conv3_launch(ca, 0, 1, 0, stream);
-    ++launches;
-    if (profile_) mark(evs);
-    if (!sharded) {
-      conv3_launch(ca, 1, 1, 0, stream);
+    if (pre) {
+      conv3_launch(ca, 0, 1, 0, stream);
       ++launches;
-    } else {
-      conv3_launch(ca, 1, 1, 0, stream);
-      const int64_t nw = conv3_nw(M, N), H = N / 2 + 1;
-      nccl_check(nccl().all_reduce(w.cspec.p, w.cspec.p, static_cast<size_t>(nw * nw * H * nvec * 2), ncclDouble,
-                                   ncclSum, comm, stream),
-                 "ncclAllReduce of the window spectra");
-      conv3_launch(ca, 1, 1, 1, stream);
-      launches += 2;
+      if (profile_) mark(evs);
+      conv3_launch(ca, 1, 1, 0, stream);  // sharded: forward line pass into the window spectrum
+      ++launches;
     }
-    if (profile_) mark(evs);
-    conv3_launch(ca, 2, 1, 0, stream);
-    ++launches;
-    FGS_CUDA(cudaGetLastError());
-    if (profile_) mark(evs);
-  } else {
-    FGS_CUFFT(cufftExecD2Z(w.r2c, w.grid.p, w.spec.p));
-    if (profile_) mark(evs);
-    if (!sharded) {
-      MultiplyArgs ma{w.spec.p, mult.p, spec_elems, spec_elems, nvec, d, M, N};
-      multiply_kernel<<<ceil_div(spec_elems, 256), 256, 0, stream>>>(ma);
+    if (sharded) {
+      if (nccl_exchange) {
+        const int64_t nw = conv3_nw(M, N), H = N / 2 + 1;
+        nccl_check(nccl().all_reduce(w.cspec.p, w.cspec.p, static_cast<size_t>(nw * nw * H * nvec * 2), ncclDouble,
+                                     ncclSum, comm, stream),
+                   "ncclAllReduce of the window spectra");
+      }
+      if (post) {
+        conv3_launch(ca, 1, 1, 1, stream);
+        ++launches;
+      }
+    }
+    if (post) {
+      if (profile_) mark(evs);
+      conv3_launch(ca, 2, 1, 0, stream);
       ++launches;
       FGS_CUDA(cudaGetLastError());
-    } else {
-      WindowArgs wa{w.spec.p, w.window.p, mult.p, spec_elems, window_elems, window_elems, nvec, d, M, N};
+      if (profile_) mark(evs);
+    }
+  } else {
+    if (pre) {
+      FGS_CUFFT(cufftExecD2Z(w.r2c, w.grid.p, w.spec.p));
+      if (profile_) mark(evs);
+      if (!sharded) {
+        MultiplyArgs ma{w.spec.p, mult.p, spec_elems, spec_elems, nvec, d, M, N};
+        multiply_kernel<<<ceil_div(spec_elems, 256), 256, 0, stream>>>(ma);
+        ++launches;
+        FGS_CUDA(cudaGetLastError());
+      }
+    }
+    WindowArgs wa{w.spec.p, w.window.p, mult.p, spec_elems, window_elems, window_elems, nvec, d, M, N};
+    if (sharded && pre) {
       pack_window_kernel<<<ceil_div(window_elems, 256), 256, 0, stream>>>(wa);
       ++launches;
+    }
+    if (nccl_exchange)
       nccl_check(nccl().all_reduce(w.window.p, w.window.p, static_cast<size_t>(window_elems) * nvec * 2, ncclDouble,
                                    ncclSum, comm, stream),
                  "ncclAllReduce of the truncated spectrum");
+    if (sharded && post) {
       FGS_CUDA(cudaMemsetAsync(w.spec.p, 0, sizeof(cufftDoubleComplex) * spec_elems * nvec, stream));
       unpack_multiply_kernel<<<ceil_div(window_elems, 256), 256, 0, stream>>>(wa);
       ++launches;
       FGS_CUDA(cudaGetLastError());
     }
-    if (profile_) mark(evs);
-    FGS_CUFFT(cufftExecZ2D(w.c2r, w.spec.p, w.grid_out.p));
-    if (profile_) mark(evs);
+    if (post) {
+      if (profile_) mark(evs);
+      FGS_CUFFT(cufftExecZ2D(w.c2r, w.spec.p, w.grid_out.p));
+      if (profile_) mark(evs);
+    }
   }
+  if (!post) return;
   launch_interp(a);
   if (profile_) {
     mark(evs);
@@ -1564,16 +1588,34 @@ bool Core::use_conv3d() const {
          tw2.p != nullptr;
 }
 
-void Core::compute_degrees(int64_t* bad_node) {
+void Core::degrees_prepare(DBuf<double>& ones) {
   degrees.alloc(static_cast<size_t>(std::max<int64_t>(n_local, 1)));
   inv_sqrt.alloc(static_cast<size_t>(std::max<int64_t>(n_local, 1)));
   flag.alloc(1);
-  DBuf<double> ones;
   ones.alloc(static_cast<size_t>(std::max<int64_t>(n_local, 1)));
   fill_kernel<<<ceil_div(std::max<int64_t>(n_local, 1), 256), 256, 0, stream>>>(ones.p, n_local, 1.0);
   ++launches;
   unsigned long long init = ULLONG_MAX;
   FGS_CUDA(cudaMemcpyAsync(flag.p, &init, sizeof(init), cudaMemcpyHostToDevice, stream));
+  FGS_CUDA(cudaStreamSynchronize(stream));  // `init` is a host stack value
+}
+
+void Core::degrees_fail(unsigned long long bad, int64_t* bad_node) {
+  const int64_t j = static_cast<int64_t>(bad);
+  if (bad_node) *bad_node = j;
+  double val = std::nan("");
+  // locate the value when this shard owns the node
+  std::vector<double> hdeg(static_cast<size_t>(n_local));
+  FGS_CUDA(cudaMemcpy(hdeg.data(), degrees.p, sizeof(double) * n_local, cudaMemcpyDeviceToHost));
+  for (int64_t p = 0; p < n_local; ++p)
+    if (host_perm[static_cast<size_t>(offset + p)] == j) val = hdeg[static_cast<size_t>(p)];
+  fail(FGS_ENUMERIC, "computed degree of node " + std::to_string(j) + " is not positive (" + std::to_string(val) +
+                         "); increase the fast-summation bandwidth/cutoff or widen the kernel");
+}
+
+void Core::compute_degrees(int64_t* bad_node) {
+  DBuf<double> ones;
+  degrees_prepare(ones);
   apply(EPI_DEGREE, ones.p, n_local, nullptr, 0, 1, false, false);
   if (sharded) {
     nccl_check(nccl().all_reduce(flag.p, flag.p, 1, ncclUint64, ncclMin, comm, stream),
@@ -1582,18 +1624,129 @@ void Core::compute_degrees(int64_t* bad_node) {
   unsigned long long bad = 0;
   FGS_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(bad), cudaMemcpyDeviceToHost, stream));
   FGS_CUDA(cudaStreamSynchronize(stream));
-  if (bad != ULLONG_MAX) {
-    const int64_t j = static_cast<int64_t>(bad);
-    if (bad_node) *bad_node = j;
-    double val = std::nan("");
-    // locate the value when this shard owns the node
-    std::vector<double> hdeg(static_cast<size_t>(n_local));
-    FGS_CUDA(cudaMemcpy(hdeg.data(), degrees.p, sizeof(double) * n_local, cudaMemcpyDeviceToHost));
-    for (int64_t p = 0; p < n_local; ++p)
-      if (host_perm[static_cast<size_t>(offset + p)] == j) val = hdeg[static_cast<size_t>(p)];
-    fail(FGS_ENUMERIC, "computed degree of node " + std::to_string(j) + " is not positive (" + std::to_string(val) +
-                           "); increase the fast-summation bandwidth/cutoff or widen the kernel");
+  if (bad != ULLONG_MAX) degrees_fail(bad, bad_node);
+}
+
+void Core::exchange_buffers(int nvec, double** src, double** dst, size_t* count) {
+  Workspace& w = workspace(nvec);
+  if (use_conv2d()) {
+    *src = w.grid.p;
+    *dst = w.grid_sum.p;
+    *count = static_cast<size_t>(grid_elems) * nvec;
+  } else if (use_conv3d()) {
+    const int64_t nw = conv3_nw(M, N), H = N / 2 + 1;
+    *src = *dst = reinterpret_cast<double*>(w.cspec.p);
+    *count = static_cast<size_t>(nw * nw * H * nvec * 2);
+  } else {
+    *src = *dst = reinterpret_cast<double*>(w.window.p);
+    *count = static_cast<size_t>(window_elems) * nvec * 2;
   }
+}
+
+// ---- ShardGroup -------------------------------------------------------------
+namespace {
+constexpr int kMaxGroup = 16;
+struct GroupSum {
+  const double* src[kMaxGroup];
+  double* dst[kMaxGroup];
+  int world;
+  int64_t count;
+};
+// the ranks' allreduce on one device: every shard's buffer <- sum over shards
+// (in place safe: element i is read and written by one thread)
+__global__ void group_sum_kernel(GroupSum g) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < g.count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double v = 0.0;
+    for (int r = 0; r < g.world; ++r) v += g.src[r][i];
+    for (int r = 0; r < g.world; ++r) g.dst[r][i] = v;
+  }
+}
+__global__ void group_min_kernel(unsigned long long* const* flags, int world) {
+  unsigned long long v = ULLONG_MAX;
+  for (int r = 0; r < world; ++r) v = min(v, *flags[r]);
+  for (int r = 0; r < world; ++r) *flags[r] = v;
+}
+}  // namespace
+
+ShardGroup::ShardGroup(const double* nodes_colmajor, int64_t n_, int d, const KernelSpec& kernel,
+                       const Params& params, int device_, int world, int64_t* bad_node)
+    : device(device_), n(n_) {
+  if (world < 1 || world > kMaxGroup) fail(FGS_EPARAM, "shard group world must be in [1, 16]");
+  FGS_CUDA(cudaSetDevice(device));
+  FGS_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  for (int r = 0; r < world; ++r) {
+    shards.push_back(std::make_unique<Core>(nodes_colmajor, n, d, Core::FASTSUM, kernel, params, device, r, world));
+    shards.back()->sharded = true;
+    shards.back()->emulated = true;
+    shards.back()->set_stream(stream);
+  }
+  // degrees: one group apply of the ones vectors (internal order per shard)
+  std::vector<DBuf<double>> ones(static_cast<size_t>(world));
+  std::vector<const double*> xs;
+  std::vector<double*> ys;
+  std::vector<int64_t> lds;
+  for (int r = 0; r < world; ++r) {
+    shards[static_cast<size_t>(r)]->degrees_prepare(ones[static_cast<size_t>(r)]);
+    xs.push_back(ones[static_cast<size_t>(r)].p);
+    ys.push_back(nullptr);
+    lds.push_back(shards[static_cast<size_t>(r)]->n_local);
+  }
+  run(EPI_DEGREE, xs, lds, ys, lds, 1, false, false);
+  DBuf<unsigned long long*> fl;
+  std::vector<unsigned long long*> hf;
+  for (auto& c : shards) hf.push_back(c->flag.p);
+  fl.upload(hf.data(), hf.size(), stream);
+  group_min_kernel<<<1, 1, 0, stream>>>(fl.p, world);
+  FGS_CUDA(cudaGetLastError());
+  unsigned long long bad = 0;
+  FGS_CUDA(cudaMemcpyAsync(&bad, hf[0], sizeof(bad), cudaMemcpyDeviceToHost, stream));
+  FGS_CUDA(cudaStreamSynchronize(stream));
+  if (bad != ULLONG_MAX) {
+    for (auto& c : shards) {  // the shard owning the node reports its value
+      for (int64_t p = 0; p < c->n_local; ++p)
+        if (c->host_perm[static_cast<size_t>(c->offset + p)] == static_cast<int>(bad)) c->degrees_fail(bad, bad_node);
+    }
+    shards[0]->degrees_fail(bad, bad_node);
+  }
+}
+
+ShardGroup::~ShardGroup() {
+  if (stream) cudaStreamSynchronize(stream);
+  shards.clear();
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void ShardGroup::run(int epilogue, const std::vector<const double*>& x, const std::vector<int64_t>& ldx,
+                     const std::vector<double*>& y, const std::vector<int64_t>& ldy, int nvec, bool caller_order,
+                     bool scale_input) {
+  const int world = static_cast<int>(shards.size());
+  for (int r = 0; r < world; ++r)
+    shards[static_cast<size_t>(r)]->apply_launches(epilogue, x[static_cast<size_t>(r)], ldx[static_cast<size_t>(r)],
+                                                   y[static_cast<size_t>(r)], ldy[static_cast<size_t>(r)], nvec,
+                                                   caller_order, scale_input, 1);
+  GroupSum g{};
+  g.world = world;
+  for (int r = 0; r < world; ++r) {
+    double *src = nullptr, *dst = nullptr;
+    size_t count = 0;
+    shards[static_cast<size_t>(r)]->exchange_buffers(nvec, &src, &dst, &count);
+    g.src[r] = src;
+    g.dst[r] = dst;
+    g.count = static_cast<int64_t>(count);
+  }
+  group_sum_kernel<<<static_cast<unsigned>(std::min<int64_t>((g.count + 255) / 256, 148 * 8)), 256, 0, stream>>>(g);
+  FGS_CUDA(cudaGetLastError());
+  for (int r = 0; r < world; ++r)
+    shards[static_cast<size_t>(r)]->apply_launches(epilogue, x[static_cast<size_t>(r)], ldx[static_cast<size_t>(r)],
+                                                   y[static_cast<size_t>(r)], ldy[static_cast<size_t>(r)], nvec,
+                                                   caller_order, scale_input, 2);
+}
+
+void ShardGroup::apply(int epilogue, const double* x, double* y, int64_t ld, int nvec, bool scale_input) {
+  const size_t world = shards.size();
+  run(epilogue, std::vector<const double*>(world, x), std::vector<int64_t>(world, ld), std::vector<double*>(world, y),
+      std::vector<int64_t>(world, ld), nvec, true, scale_input);
 }
 
 void Core::nfft_adjoint(const double* x_planar, double* fhat_out) {

@@ -115,6 +115,7 @@ class Core {
   bool own_stream = true;
   ncclComm_t comm = nullptr;
   bool sharded = false;  // created through fgs_adjacency_create_sharded (owns an NCCL communicator)
+  bool emulated = false; // a shard of a ShardGroup: sharded data path, exchange done by the group
   int64_t launches = 0;
   double lanczos_stats[4] = {0, 0, 0, 0};  // last run: apply ms, reorth ms, loop wall ms, iterations
 
@@ -197,6 +198,16 @@ class Core {
   // arrays) runs on several cores while the copy engine streams.
   void host_copy(bool to_device, void* dst, const void* src, size_t bytes);
   void compute_degrees(int64_t* bad_node);
+  // the launch sequence of one apply; phases 1 / 2 split it at the sharded
+  // exchange (ShardGroup), 3 = whole apply (NCCL exchange when sharded)
+  void apply_launches(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
+                      bool caller_order, bool scale_input, int phases = 3);
+  // device buffer a sharded apply exchanges between its phases, and the
+  // buffer the summed exchange lands in (== src except d = 2: grid_sum)
+  void exchange_buffers(int nvec, double** src, double** dst, size_t* count);
+  // degree pass split for ShardGroup: prepare (ones, flag), check the flag
+  void degrees_prepare(DBuf<double>& ones);
+  void degrees_fail(unsigned long long bad, int64_t* bad_node);
 
   // complex NFFT transforms (NfftPlan), interleaved complex on device
   void nfft_adjoint(const double* x_re_im_planar, double* fhat_interleaved);
@@ -238,8 +249,6 @@ class Core {
     int64_t launches;
   };
   std::vector<GraphEntry> graphs_;
-  void apply_launches(int epilogue, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
-                      bool caller_order, bool scale_input);
   bool profile_ = false;
   std::vector<cudaEvent_t> ev_pool_;
   std::vector<std::vector<cudaEvent_t>> ev_pending_;
@@ -263,5 +272,33 @@ void validate_params(const Params& p);
 // fp64 FMA peak of a device in TFLOP/s (peak.cu)
 double measure_fp64_peak(int device);
 double measure_dmma_peak(int device);
+
+// Single-GPU emulation of the N-rank sharded path (validation of the
+// multi-GPU data path on one device): `world` shards (Core rank r of world
+// W: the same plan slices, slab-pruned convolutions and exchange buffers as
+// the NCCL ranks) on one device and stream.  An apply runs phase 1 on every
+// shard, sums the shards' exchange buffers with one device kernel (what
+// ncclAllReduce computes across the ranks), then phase 2 on every shard.
+// Ranks that wait on one another are never separate launches on one GPU
+// (B200_PROFILING.md): the exchange is a plain kernel between the phases.
+class ShardGroup {
+ public:
+  ShardGroup(const double* nodes_colmajor, int64_t n, int d, const KernelSpec& kernel, const Params& params,
+             int device, int world, int64_t* bad_node);
+  ~ShardGroup();
+  ShardGroup(const ShardGroup&) = delete;
+  ShardGroup& operator=(const ShardGroup&) = delete;
+  // y = op(x) for full-length device vectors in caller order (column j at x + j ld)
+  void apply(int epilogue, const double* x, double* y, int64_t ld, int nvec, bool scale_input);
+  std::vector<std::unique_ptr<Core>> shards;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int64_t n = 0;
+
+ private:
+  void run(int epilogue, const std::vector<const double*>& x, const std::vector<int64_t>& ldx,
+           const std::vector<double*>& y, const std::vector<int64_t>& ldy, int nvec, bool caller_order,
+           bool scale_input);
+};
 
 }  // namespace fgsb
