@@ -10,7 +10,7 @@ n = 10M points in 3-D, N = 64, m = 8); configs 2 and 4 are reported under
 "also" with their Lanczos time-to-k.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--weak]
-                  [--impl b200|reference]
+                  [--impl b200|reference] [--emulate N]
 
 Multi-GPU: one process per GPU.  `--gpus N` without a torchrun environment
 re-launches itself under `torch.distributed.run` with N ranks.  Points are
@@ -64,6 +64,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=8.0)
     p.add_argument("--also", default="2,4", help="comma list of extra configs measured after the main line "
                    "(device matvecs/s + Lanczos time-to-k), '' to skip")
+    p.add_argument("--emulate", type=int, default=0,
+                   help="single GPU: time the N-rank sharded path as an emulated shard group (per-rank compute "
+                        "measured, NVLink allreduce modelled) and print a projected N-GPU line")
     p.add_argument("--force-sharded", action="store_true",
                    help=argparse.SUPPRESS)  # run the sharded (NCCL) path even at world size 1 (under torchrun)
     return p.parse_args()
@@ -297,6 +300,59 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": value, "unit": "matvecs/s", "cores": 1, "kind": kind, "sample": desc,
                          "cpu": cpu_model(), "host_cores": os.cpu_count(), "setup_s": setup},
         "e2e": {"value": value, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- emulated N-rank path on one GPU (projection, not a measurement) -------
+ALLREDUCE_BUSBW = 300e9   # B/s, conservative NCCL allreduce bus bandwidth on 8x B200 NVLink 5 / NVSwitch
+ALLREDUCE_LAT = 20e-6     # s per allreduce (launch + ring/NVLS latency)
+
+
+def run_emulated(args):
+    """`--emulate N`: the sharded data path of N ranks as one ShardGroup on
+    this GPU.  Every shard's two apply phases are timed with CUDA events (what
+    rank r computes on its own GPU: its slice's spread / interpolation, its
+    slab-pruned convolution, its assembly); the exchange is the window
+    spectrum allreduce, modelled at ALLREDUCE_BUSBW.  Projected whole-job
+    matvecs/s = nvec / (max over shards + modelled allreduce)."""
+    import torch
+
+    import paper_1808_04580_b200 as fgs
+    world = args.emulate
+    cfg, n, nvec, info = workload(args, world)
+    X = nodes_for(args, n)
+    params = fgs.FastsumParams(info["N"], info["m"], info["p"], 0.0)
+    kern = fgs.KernelSpec.gaussian(info["sigma"])
+    t0 = time.perf_counter()
+    grp = fgs.ShardGroup(X, kern, params, world=world)
+    setup_s = time.perf_counter() - t0
+    x = torch.from_numpy(np.ascontiguousarray(fgs.workload_vectors(n, nvec, VEC_SEED).T)).cuda()
+    y = torch.empty_like(x)
+    grp.profile(fgs.OP_SYM_LAPLACIAN, x.data_ptr(), y.data_ptr(), nvec=nvec, ld=n, reps=max(1, args.warmup))
+    shard_ms, ex_ms = grp.profile(fgs.OP_SYM_LAPLACIAN, x.data_ptr(), y.data_ptr(), nvec=nvec, ld=n,
+                                  reps=max(1, args.steps))
+    N, M, d = info["N"], 2 * info["N"], info["d"]
+    if d == 3:
+        nw = N if M == N else N + 1
+        ex_bytes = nw * nw * (N // 2 + 1) * 16 * nvec
+    elif d == 2:
+        ex_bytes = M * M * 8 * nvec
+    else:
+        ex_bytes = (N // 2 + 1) * 16 * nvec
+    ar_ms = 1e3 * (ALLREDUCE_LAT + 2.0 * (world - 1) / world * ex_bytes / ALLREDUCE_BUSBW) if world > 1 else 0.0
+    step_ms = float(np.max(shard_ms)) + ar_ms
+    stats = [grp.stats(r) for r in range(world)]
+    line = {
+        "metric": METRIC, "mode": "emulated shard group on 1 GPU (projection, not a measured N-GPU run)",
+        "projected_value": nvec / (step_ms * 1e-3), "unit": "matvecs/s", "n_gpus_projected": world,
+        "scaling": "weak" if args.weak else "strong", "dtype": "f64", "config": cfg,
+        "shard_ms": [float(v) for v in shard_ms], "max_shard_ms": float(np.max(shard_ms)),
+        "mean_shard_ms": float(np.mean(shard_ms)), "allreduce_bytes": ex_bytes,
+        "allreduce_ms_model": ar_ms, "allreduce_model": f"{ALLREDUCE_LAT * 1e6:.0f} us + 2(N-1)/N bytes / "
+                                                         f"{ALLREDUCE_BUSBW / 1e9:.0f} GB/s",
+        "device_sum_exchange_ms": ex_ms, "conv_planes": [s["conv_planes"] for s in stats],
+        "n_local": [s["n_local"] for s in stats], "setup_s": setup_s,
     }
     print(json.dumps(line), flush=True)
 
@@ -626,6 +682,9 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.emulate:
+        run_emulated(args)
         return
     import torch
     import torch.distributed as dist

@@ -193,6 +193,12 @@ fgs_status fgs_shard_group_apply_device(fgs_shard_group_t g, fgs_op op, const do
  * pruned convolution (M planes when unpruned), work items */
 fgs_status fgs_shard_group_stats(fgs_shard_group_t g, int rank, int64_t* n_local, int* conv_plane0,
                                  int* conv_planes, int* items);
+/* `reps` applies timed with CUDA events around each shard's two phases:
+ * shard_ms[world] = mean ms per apply of shard r (what rank r computes on
+ * its own GPU), exchange_ms = the device-sum exchange on one GPU (not an
+ * NVLink figure) */
+fgs_status fgs_shard_group_profile(fgs_shard_group_t g, fgs_op op, const double* dx, double* dy, int nvec, int64_t ld,
+                                   int reps, double* shard_ms, double* exchange_ms);
 void fgs_shard_group_destroy(fgs_shard_group_t g);
 
 /* ---- lanczos_largest (spectral.hpp:68-70, spectral.cpp:141-256) ---------

@@ -490,6 +490,16 @@ class ShardGroup:
         _check(lib().fgs_shard_group_apply_device(self._h, int(op), C.c_void_p(dx_ptr), C.c_void_p(dy_ptr),
                                                   int(nvec), C.c_int64(ld)))
 
+    def profile(self, op, dx_ptr: int, dy_ptr: int, nvec=1, ld=None, reps=3):
+        """(per-shard ms per apply, exchange ms): CUDA events around each
+        shard's phases -- what rank r computes on its own GPU."""
+        ld = ld if ld is not None else self._n
+        ms = np.zeros(self.world)
+        ex = C.c_double()
+        _check(lib().fgs_shard_group_profile(self._h, int(op), C.c_void_p(dx_ptr), C.c_void_p(dy_ptr), int(nvec),
+                                             C.c_int64(ld), int(reps), _dp(ms), C.byref(ex)))
+        return ms, ex.value
+
     def stats(self, rank: int) -> dict:
         nl, p0, pn, it = C.c_int64(), C.c_int(), C.c_int(), C.c_int()
         _check(lib().fgs_shard_group_stats(self._h, int(rank), C.byref(nl), C.byref(p0), C.byref(pn), C.byref(it)))

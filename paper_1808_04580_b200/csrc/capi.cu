@@ -557,6 +557,23 @@ fgs_status fgs_shard_group_stats(fgs_shard_group_t g, int rank, int64_t* n_local
   });
 }
 
+fgs_status fgs_shard_group_profile(fgs_shard_group_t g, fgs_op op, const double* dx, double* dy, int nvec, int64_t ld,
+                                   int reps, double* shard_ms, double* exchange_ms) {
+  return guard([&] {
+    need(g, "group");
+    need(dx, "x");
+    need(dy, "y");
+    need(shard_ms, "shard_ms");
+    need(exchange_ms, "exchange_ms");
+    if (nvec < 1 || reps < 1) fail(FGS_ESHAPE, "nvec and reps must be >= 1");
+    if (ld < g->group->n) fail(FGS_ESHAPE, "input length does not match operator dimension");
+    bool scale = false;
+    const int epi = epilogue_of(op, &scale);
+    FGS_CUDA(cudaSetDevice(g->group->device));
+    g->group->profile(epi, dx, dy, ld, nvec, scale, reps, shard_ms, exchange_ms);
+  });
+}
+
 void fgs_shard_group_destroy(fgs_shard_group_t g) { delete g; }
 
 // ---- lanczos_largest -------------------------------------------------------

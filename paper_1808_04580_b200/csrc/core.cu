@@ -604,7 +604,34 @@ void Core::build_plan(const double* nodes_colmajor) {
   // keys -> stable radix sort by (tile, cell) -> run-length encode; returns
   // the number of nonempty cells (independent of the tile edge B)
   auto sort_cells = [&]() {
-    PointArgs pa{dnodes.p, n, d, M, m, B, nt, rho, kind == FASTSUM ? 1 : 0, keys.p, idx.p, bad.p};
+    PointArgs pa{dnodes.p, n, d, M, m, B, nt, rho, kind == FASTSUM ? 1 : 0, keys.p, idx.p, bad.p, 0};
+    rot0 = 0;
+    if (world > 1) {
+      // start the dim-0 tile order after the widest empty gap of the cloud:
+      // a cloud centred on 0 wraps around plane 0, and without the rotation
+      // the rank whose slice spans the wrap gets two far-apart slabs
+      DBuf<int> occ;
+      occ.alloc(static_cast<size_t>(nt));
+      FGS_CUDA(cudaMemsetAsync(occ.p, 0, sizeof(int) * nt, stream));
+      tile0_occupancy_kernel<<<ceil_div(n, 256), 256, 0, stream>>>(pa, occ.p);
+      ++launches;
+      FGS_CUDA(cudaGetLastError());
+      std::vector<int> ho(static_cast<size_t>(nt));
+      FGS_CUDA(cudaMemcpyAsync(ho.data(), occ.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, stream));
+      FGS_CUDA(cudaStreamSynchronize(stream));
+      int best = 0, run = 0;
+      for (int t = 0; t < 2 * nt; ++t) {
+        if (!ho[static_cast<size_t>(t % nt)]) {
+          if (++run > best && run < nt) {
+            best = run;
+            rot0 = (t + 1) % nt;  // first tile after the gap
+          }
+        } else {
+          run = 0;
+        }
+      }
+      pa.rot0 = rot0;
+    }
     point_keys_kernel<<<ceil_div(n, 256), 256, 0, stream>>>(pa);
     ++launches;
     FGS_CUDA(cudaGetLastError());
@@ -671,7 +698,10 @@ void Core::build_plan(const double* nodes_colmajor) {
   // ---- work items: runs of cells inside one tile, <= chunk points ---------
   // items (CTAs) per pass: enough to fill every SM several times over; small
   // problems get short items (their cost is the serial staging chain)
-  int64_t target_items = n_local < 300000 ? 16 * 148 : 4 * 148;
+  // (sharded plans: by the whole problem's size -- a C4 rank of 250k points
+  // runs 592 items of ~420 points: 0.195 ms vs 0.244 ms with 2368 small ones,
+  // whose box zero / write-out / assembly overhead does not shrink with n)
+  int64_t target_items = n < 300000 ? 16 * 148 : 4 * 148;
   if (const char* e = std::getenv("FGS_ITEM_TARGET")) target_items = std::max<int64_t>(1, std::atoll(e));
   int chunk = static_cast<int>(std::max<int64_t>(32, std::min<int64_t>(4096, (n_local + target_items - 1) / target_items)));
   chunk = (chunk + 31) / 32 * 32;
@@ -703,6 +733,7 @@ void Core::build_plan(const double* nodes_colmajor) {
         cc[t] = static_cast<int>(cell % B);
         cell /= B;
         tcoord[t] = static_cast<int>(tile % nt);
+        if (t == 3 - d) tcoord[t] = (tcoord[t] + rot0) % nt;  // undo the dim-0 tile rotation
         tile /= nt;
       } else {
         cc[t] = 0;
@@ -1719,12 +1750,21 @@ ShardGroup::~ShardGroup() {
 
 void ShardGroup::run(int epilogue, const std::vector<const double*>& x, const std::vector<int64_t>& ldx,
                      const std::vector<double*>& y, const std::vector<int64_t>& ldy, int nvec, bool caller_order,
-                     bool scale_input) {
+                     bool scale_input, std::vector<cudaEvent_t>* ev) {
   const int world = static_cast<int>(shards.size());
-  for (int r = 0; r < world; ++r)
+  // ev (profiling): [2 world + 2] events, shard r phase 1 between ev[r] and
+  // ev[r + 1], the exchange between ev[world] and ev[world + 1], shard r
+  // phase 2 between ev[world + 1 + r] and ev[world + 2 + r]
+  auto mark = [&](int i) {
+    if (ev) FGS_CUDA(cudaEventRecord((*ev)[static_cast<size_t>(i)], stream));
+  };
+  mark(0);
+  for (int r = 0; r < world; ++r) {
     shards[static_cast<size_t>(r)]->apply_launches(epilogue, x[static_cast<size_t>(r)], ldx[static_cast<size_t>(r)],
                                                    y[static_cast<size_t>(r)], ldy[static_cast<size_t>(r)], nvec,
                                                    caller_order, scale_input, 1);
+    mark(r + 1);
+  }
   GroupSum g{};
   g.world = world;
   for (int r = 0; r < world; ++r) {
@@ -1737,10 +1777,37 @@ void ShardGroup::run(int epilogue, const std::vector<const double*>& x, const st
   }
   group_sum_kernel<<<static_cast<unsigned>(std::min<int64_t>((g.count + 255) / 256, 148 * 8)), 256, 0, stream>>>(g);
   FGS_CUDA(cudaGetLastError());
-  for (int r = 0; r < world; ++r)
+  mark(world + 1);
+  for (int r = 0; r < world; ++r) {
     shards[static_cast<size_t>(r)]->apply_launches(epilogue, x[static_cast<size_t>(r)], ldx[static_cast<size_t>(r)],
                                                    y[static_cast<size_t>(r)], ldy[static_cast<size_t>(r)], nvec,
                                                    caller_order, scale_input, 2);
+    mark(world + 2 + r);
+  }
+}
+
+void ShardGroup::profile(int epilogue, const double* x, double* y, int64_t ld, int nvec, bool scale_input, int reps,
+                         double* shard_ms, double* exchange_ms) {
+  const size_t world = shards.size();
+  std::vector<cudaEvent_t> ev(2 * world + 2);
+  for (auto& e : ev) FGS_CUDA(cudaEventCreate(&e));
+  for (size_t r = 0; r < world; ++r) shard_ms[r] = 0.0;
+  *exchange_ms = 0.0;
+  for (int it = 0; it < reps; ++it) {
+    run(epilogue, std::vector<const double*>(world, x), std::vector<int64_t>(world, ld),
+        std::vector<double*>(world, y), std::vector<int64_t>(world, ld), nvec, true, scale_input, &ev);
+    FGS_CUDA(cudaStreamSynchronize(stream));
+    float t = 0.f;
+    for (size_t r = 0; r < world; ++r) {
+      FGS_CUDA(cudaEventElapsedTime(&t, ev[r], ev[r + 1]));
+      shard_ms[r] += t / reps;
+      FGS_CUDA(cudaEventElapsedTime(&t, ev[world + 1 + r], ev[world + 2 + r]));
+      shard_ms[r] += t / reps;
+    }
+    FGS_CUDA(cudaEventElapsedTime(&t, ev[world], ev[world + 1]));
+    *exchange_ms += t / reps;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
 }
 
 void ShardGroup::apply(int epilogue, const double* x, double* y, int64_t ld, int nvec, bool scale_input) {

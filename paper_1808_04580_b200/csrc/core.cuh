@@ -101,6 +101,7 @@ class Core {
   // geometry / plan scalars
   Kind kind;
   int d = 0, N = 0, m = 0, T = 0, M = 0, B = 0, nt = 0, ntiles = 0;
+  int rot0 = 0;  // dim-0 tile rotation of the cell keys (sharded plans)
   int64_t n = 0, n_local = 0, offset = 0;
   int rank = 0, world = 1;
   double b_kb = 0.0;
@@ -290,6 +291,11 @@ class ShardGroup {
   ShardGroup& operator=(const ShardGroup&) = delete;
   // y = op(x) for full-length device vectors in caller order (column j at x + j ld)
   void apply(int epilogue, const double* x, double* y, int64_t ld, int nvec, bool scale_input);
+  // `reps` applies with CUDA events around every shard's two phases and the
+  // exchange: mean ms per apply of each shard (phase 1 + phase 2: what rank r
+  // computes on its own GPU) and of the device-sum exchange
+  void profile(int epilogue, const double* x, double* y, int64_t ld, int nvec, bool scale_input, int reps,
+               double* shard_ms, double* exchange_ms);
   std::vector<std::unique_ptr<Core>> shards;
   cudaStream_t stream = nullptr;
   int device = 0;
@@ -298,7 +304,7 @@ class ShardGroup {
  private:
   void run(int epilogue, const std::vector<const double*>& x, const std::vector<int64_t>& ldx,
            const std::vector<double*>& y, const std::vector<int64_t>& ldy, int nvec, bool caller_order,
-           bool scale_input);
+           bool scale_input, std::vector<cudaEvent_t>* ev = nullptr);
 };
 
 }  // namespace fgsb

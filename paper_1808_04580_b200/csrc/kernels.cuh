@@ -63,7 +63,21 @@ struct PointArgs {
   unsigned long long* keys;
   int* idx;
   unsigned long long* bad_range;  // min caller index with a scaled node outside [-1/2, 1/2)
+  int rot0;                        // dim-0 tile rotation: key tile t0' = (t0 - rot0) mod nt
 };
+
+// dim-0 tiles holding at least one point (sharded plans rotate the dim-0
+// tile order so the cloud is contiguous and every rank's slice is one slab)
+__global__ void tile0_occupancy_kernel(PointArgs a, int* occ) {
+  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (j >= a.n) return;
+  double v = a.nodes[j];
+  if (a.apply_rho) v = __dmul_rn(a.rho, v);
+  if (!(v >= -0.5 && v < 0.5)) v = 0.0;
+  const int u0 = first_tap(v, a.M, a.m);
+  const int w = ((u0 % a.M) + a.M) % a.M;
+  occ[w / a.B] = 1;
+}
 
 // Scaled node, cell key = (tile, cell-in-tile).  rho * v is the exact IEEE
 // product MatrixXd(rho * nodes) forms (fastsum.cpp:91).
@@ -80,7 +94,9 @@ __global__ void point_keys_kernel(PointArgs a) {
     }
     int u0 = first_tap(v, a.M, a.m);
     int w = ((u0 % a.M) + a.M) % a.M;
-    tile = tile * a.nt + w / a.B;
+    int tt = w / a.B;
+    if (t == 0) tt = (tt - a.rot0 + a.nt) % a.nt;
+    tile = tile * a.nt + tt;
     cell = cell * a.B + w % a.B;
   }
   unsigned long long bd = 1;
