@@ -1,6 +1,6 @@
 // fgs_b200_cli.cpp -- the reference's command-line drivers for the hot path
-// (tools/commands.cpp: gen, eigs, cluster, bench, ssl-kernel, krr) on the B200 library, with
-// the same flags, defaults, exit codes and `fgs-report-v1` JSON report
+// (tools/commands.cpp: eigs, cluster, bench) on the B200 library, with the
+// same flags, defaults, exit codes and `fgs-report-v1` JSON report
 // (report.cpp:97-112, schema/report.schema.json).
 //
 // Everything numeric goes through include/fgs/b200.hpp (the C ABI): plans,
@@ -11,10 +11,11 @@
 // Methods: nfft-lanczos (Fastsum backend), direct (Direct backend) and
 // nystrom-gauss-nfft (Gaussian sketch over the fast operator).  The sampled
 // "nystrom" method (dense kernel blocks, spectral.cpp:277-382) is not part of
-// this build and is rejected as a usage error, as is the command ssl-pf
-// (Allen-Cahn phase field).  segment reads and writes
-// binary PPM (PNG needs libpng, absent here).
-// ssl-kernel and krr (commands.cpp:531-713) run the device CG.
+// this build and is rejected as a usage error, as are the commands outside
+// the hot path's scope (gen, segment, ssl-kernel, krr, ssl-pf: data
+// generation, image I/O and the semi-supervised drivers; SURVEY.md section 2,
+// DESIGN.md section 7).  The library functions behind ssl-kernel / krr
+// (kernel_ssl_solve, krr_fit / krr_predict) remain in include/fgs/b200.hpp.
 #include <algorithm>
 #include <cctype>
 #include <array>
@@ -314,20 +315,6 @@ std::string fmt17(double v) {
   return b;
 }
 
-void save_points_csv(const PointCloud& c, const std::string& path) {
-  std::ofstream out(path, std::ios::binary);
-  if (!out) throw ParseError(path + ": cannot open for writing");
-  for (Index t = 0; t < c.coordinates.cols(); ++t) out << (t ? "," : "") << 'x' << t;
-  if (c.has_labels()) out << ",label";
-  out << '\n';
-  for (Index i = 0; i < c.size(); ++i) {
-    for (Index t = 0; t < c.coordinates.cols(); ++t) out << (t ? "," : "") << fmt17(c.coordinates(i, t));
-    if (c.has_labels()) out << ',' << c.labels[static_cast<size_t>(i)];
-    out << '\n';
-  }
-  if (!out) throw ParseError(path + ": write failed");
-}
-
 void save_labels_csv(const std::vector<int>& labels, const std::string& path) {
   std::ofstream out(path, std::ios::binary);
   if (!out) throw ParseError(path + ": cannot open for writing");
@@ -336,6 +323,7 @@ void save_labels_csv(const std::vector<int>& labels, const std::string& path) {
   if (!out) throw ParseError(path + ": write failed");
 }
 
+// ---- argument parsing (CLI11 subset: --name value, --flag) ----------------
 // dataset.cpp:184-211
 PointCloud gen_spiral(int classes, int per_class, double h, double r, std::uint64_t seed) {
   if (classes < 1) throw fgs::ParameterError("spiral needs at least one class");
@@ -360,38 +348,6 @@ PointCloud gen_spiral(int classes, int per_class, double h, double r, std::uint6
   return c;
 }
 
-// dataset.cpp:213-247
-PointCloud gen_crescent_fullmoon(Index n, double r1, double r2, double r3, std::uint64_t seed) {
-  if (n < 4) throw fgs::ParameterError("crescent-fullmoon needs at least 4 points");
-  if (r1 <= 0.0 || r2 <= 0.0 || r3 <= r2)
-    throw fgs::ParameterError("crescent-fullmoon radii must satisfy r1 > 0, r3 > r2 > 0");
-  const Index moon = n / 4;
-  PointCloud c;
-  c.coordinates = MatrixXd(n, 2);
-  c.labels.resize(static_cast<size_t>(n));
-  std::mt19937_64 rng(seed);
-  std::uniform_real_distribution<double> unit(0.0, 1.0);
-  for (Index i = 0; i < moon; ++i) {
-    const double phi = 2.0 * kPi * unit(rng);
-    const double dist = r1 * unit(rng);
-    c.coordinates(i, 0) = dist * std::cos(phi);
-    c.coordinates(i, 1) = dist * std::sin(phi);
-    c.labels[static_cast<size_t>(i)] = 0;
-  }
-  for (Index i = moon; i < n;) {
-    const double x = r3 * (2.0 * unit(rng) - 1.0);
-    const double y = -r3 * unit(rng);
-    const double dist = std::hypot(x, y);
-    if (dist <= r2 || dist > r3) continue;
-    c.coordinates(i, 0) = x;
-    c.coordinates(i, 1) = y;
-    c.labels[static_cast<size_t>(i)] = 1;
-    ++i;
-  }
-  return c;
-}
-
-// ---- argument parsing (CLI11 subset: --name value, --flag) ----------------
 class Args {
  public:
   Args(int argc, char** argv, int first) {
@@ -665,54 +621,6 @@ int guarded(Report& r, const std::string& path, Body&& body) {
   return 1;
 }
 
-// ---- gen (commands.cpp:294-335) --------------------------------------------
-int run_gen(Args& a) {
-  CommonOpts o;
-  bool spiral = false, crescent = false;
-  int classes = 5, per_class = 400;
-  double h = 10.0, r = 2.0, r1 = 5.0, r2 = 5.0, r3 = 8.0;
-  long long n = 10000;
-  a.get("spiral", &spiral);
-  a.get("crescent-fullmoon", &crescent);
-  a.get("classes", &classes);
-  a.get("per-class", &per_class);
-  a.get("height", &h);
-  a.get("radius", &r);
-  a.get("n", &n);
-  a.get("r1", &r1);
-  a.get("r2", &r2);
-  a.get("r3", &r3);
-  io_flags(a, &o, false);
-  a.finish();
-  if (spiral == crescent) throw fgs::ParameterError("choose exactly one of --spiral and --crescent-fullmoon");
-  Report rep;
-  rep.command = "gen";
-  rep.seed = o.seed;
-  PointCloud cloud;
-  Timer t;
-  if (spiral) {
-    rep.method = "spiral";
-    cloud = gen_spiral(classes, per_class, h, r, o.seed);
-    rep.parameters["classes"] = classes;
-    rep.parameters["per_class"] = per_class;
-    rep.parameters["h"] = h;
-    rep.parameters["r"] = r;
-  } else {
-    rep.method = "crescent-fullmoon";
-    cloud = gen_crescent_fullmoon(n, r1, r2, r3, o.seed);
-    rep.parameters["n"] = n;
-    rep.parameters["r1"] = r1;
-    rep.parameters["r2"] = r2;
-    rep.parameters["r3"] = r3;
-  }
-  rep.parameters["out"] = o.out;
-  save_points_csv(cloud, o.out);
-  rep.add_timing("generate", t.seconds());
-  rep.add_metric("n", static_cast<double>(cloud.size()), "number of generated points");
-  return finish(rep, o.out + ".report.json",
-                "generated " + std::to_string(cloud.size()) + " points -> " + o.out + '\n');
-}
-
 // ---- eigs (commands.cpp:339-358) -------------------------------------------
 int run_eigs(Args& a) {
   CommonOpts o;
@@ -887,396 +795,9 @@ int run_bench(Args& a) {
   });
 }
 
-// ---- learn.cpp:169-216 training selection / fidelity -----------------------
-std::vector<int> require_labels(const PointCloud& c) {
-  if (!c.has_labels()) throw fgs::ParameterError("this command needs a labeled input CSV (final `label` column)");
-  return c.labels;
-}
-
-int count_classes(const std::vector<int>& labels) {
-  int k = 0;
-  for (int l : labels) {
-    if (l < 0) throw fgs::RangeError("labels must be nonnegative");
-    k = std::max(k, l + 1);
-  }
-  return k;
-}
-
-// per_class_count indices per class, uniformly without replacement: each
-// class's member list shuffled by one std::mt19937_64(seed) in class order
-std::vector<std::vector<Index>> select_training(const std::vector<int>& labels, int n_classes, int per_class_count,
-                                                std::uint64_t seed) {
-  if (n_classes < 1) throw fgs::ParameterError("need at least one class");
-  if (per_class_count < 1) throw fgs::ParameterError("need at least one sample per class");
-  std::vector<std::vector<Index>> members(static_cast<size_t>(n_classes));
-  for (size_t i = 0; i < labels.size(); ++i) {
-    const int l = labels[i];
-    if (l < 0 || l >= n_classes)
-      throw fgs::RangeError("label " + std::to_string(l) + " at position " + std::to_string(i) +
-                            " is outside [0, n_classes)");
-    members[static_cast<size_t>(l)].push_back(static_cast<Index>(i));
-  }
-  std::mt19937_64 rng(seed);
-  std::vector<std::vector<Index>> out(static_cast<size_t>(n_classes));
-  for (int c = 0; c < n_classes; ++c) {
-    auto& pool = members[static_cast<size_t>(c)];
-    if (static_cast<int>(pool.size()) < per_class_count)
-      throw fgs::ParameterError("class " + std::to_string(c) + " has only " + std::to_string(pool.size()) +
-                                " members; cannot draw " + std::to_string(per_class_count));
-    std::shuffle(pool.begin(), pool.end(), rng);
-    out[static_cast<size_t>(c)].assign(pool.begin(), pool.begin() + per_class_count);
-  }
-  return out;
-}
-
-VectorXd fidelity_vector(const std::vector<std::vector<Index>>& sel, Index n, int positive) {
-  VectorXd f(n);
-  for (size_t c = 0; c < sel.size(); ++c)
-    for (Index i : sel[c]) f(i) = static_cast<int>(c) == positive ? 1.0 : -1.0;
-  return f;
-}
-
-std::vector<int> argmax_labels(const std::vector<VectorXd>& fields, Index n) {
-  std::vector<int> out(static_cast<size_t>(n));
-  for (Index i = 0; i < n; ++i) {
-    if (fields.size() == 1) {
-      out[static_cast<size_t>(i)] = fields[0](i) >= 0.0 ? 0 : 1;
-    } else {
-      int best = 0;
-      for (size_t c = 1; c < fields.size(); ++c)
-        if (fields[c](i) > fields[static_cast<size_t>(best)](i)) best = static_cast<int>(c);
-      out[static_cast<size_t>(i)] = best;
-    }
-  }
-  return out;
-}
-
-// ---- images (dataset.cpp:84-130, 340-460): binary PPM; PNG needs libpng ----
-struct ImageBuffer {
-  int width = 0, height = 0;
-  std::vector<unsigned char> rgb;
-};
-
-std::string ppm_token(std::istream& in) {
-  std::string tok;
-  int c = in.get();
-  while (c != EOF) {
-    if (c == '#') {
-      while (c != EOF && c != '\n') c = in.get();
-    } else if (std::isspace(c)) {
-      c = in.get();
-    } else {
-      break;
-    }
-  }
-  while (c != EOF && !std::isspace(c)) {
-    tok.push_back(static_cast<char>(c));
-    c = in.get();
-  }
-  return tok;
-}
-
-ImageBuffer load_image(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw ParseError(path + ": cannot open");
-  unsigned char magic[8] = {};
-  in.read(reinterpret_cast<char*>(magic), 8);
-  static const unsigned char png_sig[8] = {0x89, 'P', 'N', 'G', '\r', '\n', 0x1a, '\n'};
-  if (std::equal(magic, magic + 8, png_sig))
-    throw FormatError(path + ": PNG input needs libpng, which is not part of this build (use binary PPM)");
-  if (!(magic[0] == 'P' && magic[1] == '6'))
-    throw FormatError(path + ": unsupported image format (expected PNG or binary PPM)");
-  in.clear();
-  in.seekg(0);
-  ppm_token(in);
-  ImageBuffer img;
-  try {
-    img.width = std::stoi(ppm_token(in));
-    img.height = std::stoi(ppm_token(in));
-    if (std::stoi(ppm_token(in)) != 255) throw FormatError(path + ": only 8-bit images are supported");
-  } catch (const std::logic_error&) {
-    throw ParseError(path + ": malformed header");
-  }
-  if (img.width <= 0 || img.height <= 0) throw ParseError(path + ": malformed header");
-  const size_t bytes = 3u * static_cast<size_t>(img.width) * static_cast<size_t>(img.height);
-  img.rgb.resize(bytes);
-  in.read(reinterpret_cast<char*>(img.rgb.data()), static_cast<std::streamsize>(bytes));
-  if (static_cast<size_t>(in.gcount()) != bytes) throw ParseError(path + ": truncated pixel data");
-  return img;
-}
-
-bool ends_with(const std::string& s, const std::string& suf) {
-  return s.size() >= suf.size() && s.compare(s.size() - suf.size(), suf.size(), suf) == 0;
-}
-
-void save_image(const ImageBuffer& img, const std::string& path) {
-  if (ends_with(path, ".png")) throw FormatError(path + ": PNG output needs libpng, which is not part of this build");
-  if (!ends_with(path, ".ppm")) throw FormatError(path + ": unsupported image extension (expected .png or .ppm)");
-  std::ofstream out(path, std::ios::binary);
-  if (!out) throw ParseError(path + ": cannot open for writing");
-  out << "P6\n" << img.width << ' ' << img.height << "\n255\n";
-  out.write(reinterpret_cast<const char*>(img.rgb.data()), static_cast<std::streamsize>(img.rgb.size()));
-  if (!out) throw ParseError(path + ": write failed");
-}
-
-// pixels as RGB feature points, raster order (dataset.cpp:368-382)
-PointCloud image_to_nodes(const std::string& path, int* w, int* h) {
-  const ImageBuffer img = load_image(path);
-  *w = img.width;
-  *h = img.height;
-  const Index n = static_cast<Index>(img.width) * img.height;
-  PointCloud c;
-  c.coordinates = MatrixXd(n, 3);
-  for (Index p = 0; p < n; ++p)
-    for (int t = 0; t < 3; ++t) c.coordinates(p, t) = static_cast<double>(img.rgb[static_cast<size_t>(3 * p + t)]);
-  return c;
-}
-
-// dataset.cpp:384-410
-std::vector<std::array<double, 3>> default_palette(int k) {
-  if (k < 1) throw fgs::ParameterError("palette needs at least one color");
-  static const int base[10][3] = {{31, 119, 180}, {255, 127, 14}, {44, 160, 44},   {214, 39, 40}, {148, 103, 189},
-                                  {140, 86, 75},  {227, 119, 194}, {127, 127, 127}, {188, 189, 34}, {23, 190, 207}};
-  std::vector<std::array<double, 3>> pal(static_cast<size_t>(k));
-  for (int i = 0; i < k; ++i) {
-    if (i < 10) {
-      for (int c = 0; c < 3; ++c) pal[static_cast<size_t>(i)][static_cast<size_t>(c)] = base[i][c];
-    } else {
-      const double hue = 6.0 * (i - 10) / std::max(1, k - 10);
-      const int sector = static_cast<int>(hue) % 6;
-      const double frac = hue - std::floor(hue);
-      const double table[6][3] = {{1, frac, 0}, {1 - frac, 1, 0}, {0, 1, frac},
-                                  {0, 1 - frac, 1}, {frac, 0, 1}, {1, 0, 1 - frac}};
-      for (int c = 0; c < 3; ++c) pal[static_cast<size_t>(i)][static_cast<size_t>(c)] = std::round(255.0 * table[sector][c]);
-    }
-  }
-  return pal;
-}
-
-void labels_to_image(const std::vector<int>& labels, int w, int h, const std::vector<std::array<double, 3>>& pal,
-                     const std::string& path) {
-  if (labels.size() != static_cast<size_t>(w) * static_cast<size_t>(h))
-    throw fgs::ShapeError("label count does not fill the raster");
-  ImageBuffer img;
-  img.width = w;
-  img.height = h;
-  img.rgb.resize(labels.size() * 3u);
-  for (size_t p = 0; p < labels.size(); ++p) {
-    const int l = labels[p];
-    if (l < 0 || l >= static_cast<int>(pal.size())) throw fgs::RangeError("label " + std::to_string(l) + " has no palette entry");
-    for (int c = 0; c < 3; ++c)
-      img.rgb[3 * p + static_cast<size_t>(c)] =
-          static_cast<unsigned char>(std::clamp(pal[static_cast<size_t>(l)][static_cast<size_t>(c)], 0.0, 255.0));
-  }
-  save_image(img, path);
-}
-
-void difference_image(const std::vector<int>& a, const std::vector<int>& b, int w, int h, const std::string& path) {
-  ImageBuffer img;
-  img.width = w;
-  img.height = h;
-  img.rgb.assign(a.size() * 3u, 0);
-  for (size_t p = 0; p < a.size(); ++p)
-    if (a[p] != b[p]) img.rgb[3 * p] = img.rgb[3 * p + 1] = img.rgb[3 * p + 2] = 255;
-  save_image(img, path);
-}
-
-std::string with_suffix(const std::string& path, const std::string& suffix) {
-  const size_t dot = path.find_last_of('.');
-  if (dot == std::string::npos) return path + suffix;
-  return path.substr(0, dot) + suffix + path.substr(dot);
-}
-
-// ---- segment (commands.cpp:400-448) ----------------------------------------
-int run_segment(Args& a) {
-  CommonOpts o;
-  o.sigma = 90.0;
-  o.k = 4;
-  io_flags(a, &o, true);
-  kernel_flags(a, &o);
-  fastsum_flags(a, &o);
-  method_flags(a, &o);
-  a.finish();
-  Report rep;
-  rep.command = "segment";
-  rep.method = o.method;
-  rep.seed = o.seed;
-  rep.parameters = echo_common(o);
-  const std::string rpath = o.out + ".report.json";
-  return guarded(rep, rpath, [&] {
-    int w = 0, h = 0;
-    const PointCloud cloud = image_to_nodes(o.in, &w, &h);
-    const KernelSpec kernel = make_kernel(o);
-    const EigenPairs pairs = solve_pairs(cloud, kernel, make_params(o), o, &rep);
-    fgs::KMeansOptions ko;
-    ko.seed = o.seed;
-    Timer t;
-    const std::vector<int> labels = fgs::spectral_cluster(pairs, o.k, ko, o.device);
-    rep.add_timing("cluster", t.seconds());
-    labels_to_image(labels, w, h, default_palette(o.k), o.out);
-    std::string summary = "segment: " + std::to_string(w) + "x" + std::to_string(h) + " -> " + o.out + '\n';
-    if (o.with_reference) {
-      if (cloud.size() > kReferenceBudget) {
-        rep.extra["reference_skipped"] = "pixel count exceeds the dense-reference budget";
-      } else {
-        AdjacencyOperator exact(cloud.coordinates, kernel, FastsumParams{}, AdjacencyBackend::Direct, o.device);
-        const EigenPairs dense = dense_reference_eig(exact, o.k);
-        const std::vector<int> dl = fgs::spectral_cluster(dense, o.k, ko, o.device);
-        double diff = 0.0;
-        for (size_t p = 0; p < labels.size(); ++p) diff += labels[p] != dl[p];
-        const double frac = diff / static_cast<double>(labels.size());
-        rep.add_metric("label_difference_fraction", frac,
-                       "fraction of pixels labeled differently from the dense-reference segmentation (same clustering "
-                       "seed)");
-        difference_image(labels, dl, w, h, with_suffix(o.out, ".diff"));
-        summary += "difference vs dense reference: " + std::to_string(frac) + '\n';
-      }
-    }
-    return finish(rep, rpath, summary);
-  });
-}
-
-// ---- ssl-kernel (commands.cpp:531-652) -------------------------------------
-int run_ssl_kernel(Args& a) {
-  CommonOpts o;
-  int per_class = 25, truncate_k = 0, max_iter = 1000;
-  double beta = 1e4;
-  io_flags(a, &o, true);
-  kernel_flags(a, &o);
-  fastsum_flags(a, &o);
-  a.get("method", &o.method);
-  if (o.method != "nfft-lanczos" && o.method != "direct")
-    throw UsageError("--method: " + o.method + " not in {nfft-lanczos, direct}");
-  a.get("samples-per-class", &per_class);
-  a.get("beta", &beta);
-  a.get("k", &truncate_k);
-  a.get("tol", &o.tol);
-  a.get("max-iter", &max_iter);
-  a.finish();
-  Report rep;
-  rep.command = "ssl-kernel";
-  rep.method = truncate_k > 0 ? "truncated-eig" : "cg";
-  rep.seed = o.seed;
-  rep.parameters = echo_common(o);
-  rep.parameters["samples_per_class"] = per_class;
-  rep.parameters["beta"] = beta;
-  rep.parameters["truncate_k"] = truncate_k;
-  rep.parameters["max_iter"] = max_iter;
-  return guarded(rep, o.out, [&] {
-    const PointCloud cloud = load_points_csv(o.in);
-    const std::vector<int> truth = require_labels(cloud);
-    const int n_classes = count_classes(truth);
-    if (n_classes < 2) throw fgs::ParameterError("kernel SSL needs at least two classes");
-    const double tol = o.tol > 0.0 ? o.tol : 1e-4;
-    const auto sel = select_training(truth, n_classes, per_class, o.seed);
-    Timer setup;
-    AdjacencyOperator op(cloud.coordinates, make_kernel(o), make_params(o),
-                         o.method == "direct" ? AdjacencyBackend::Direct : AdjacencyBackend::Fastsum, o.device);
-    rep.add_timing("setup", setup.seconds());
-    std::optional<EigenPairs> basis;
-    fgs::LanczosInfo binfo;
-    if (truncate_k > 0) {  // commands.cpp:573-587
-      fgs::LanczosOptions lo;
-      lo.seed = o.seed;
-      lo.tol = 1e-8;
-      lo.max_iter = 6000;
-      Timer eig;
-      basis = fgs::lanczos_largest(op, truncate_k, lo, &binfo);
-      rep.add_timing("eig", eig.seconds());
-    }
-    const int channels = n_classes == 2 ? 1 : n_classes;
-    std::vector<VectorXd> fields;
-    int max_its = 0;
-    bool all_conv = true;
-    Timer solve;
-    for (int ch = 0; ch < channels; ++ch) {
-      const VectorXd f = fidelity_vector(sel, cloud.size(), ch);
-      if (basis) {
-        fields.push_back(fgs::kernel_ssl_truncated(*basis, f, beta));
-      } else {
-        fgs::CgResult r = fgs::kernel_ssl_solve(op, f, beta, tol, max_iter);
-        max_its = std::max(max_its, r.iterations);
-        all_conv = all_conv && r.converged();
-        fields.push_back(r.x);
-      }
-    }
-    rep.add_timing("solve", solve.seconds());
-    const std::vector<int> pred = argmax_labels(fields, cloud.size());
-    save_labels_csv(pred, o.out + ".labels.csv");
-    const double rate = fgs::misclassification_rate(pred, truth);
-    rep.add_metric("misclassification_rate", rate,
-                   "fraction of points labeled differently from the ground-truth labels of the input");
-    if (!basis) {
-      rep.add_metric("cg_iterations", max_its, "largest conjugate-gradient iteration count over channels");
-      rep.add_metric("cg_converged", all_conv ? 1.0 : 0.0, "1 if every channel met the CG tolerance");
-      if (!all_conv) {
-        rep.status = "numerical-failure";
-        rep.diagnostic = "conjugate gradients hit the iteration cap before meeting the tolerance";
-      }
-    } else {
-      rep.add_metric("basis_iterations", binfo.iterations, "Krylov steps spent computing the truncated eigenbasis");
-      rep.add_metric("basis_converged", binfo.converged ? 1.0 : 0.0,
-                     "1 if every basis pair met the residual tolerance");
-      if (!binfo.converged) {
-        rep.status = "numerical-failure";
-        rep.diagnostic = "the truncated eigenbasis hit the iteration cap before meeting the residual tolerance";
-      }
-    }
-    return finish(rep, o.out, "ssl-kernel: misclassification " + std::to_string(rate) + '\n');
-  });
-}
-
-// ---- krr (commands.cpp:654-713) --------------------------------------------
-int run_krr(Args& a) {
-  CommonOpts o;
-  double beta = 1e-3;
-  int max_iter = 1000;
-  io_flags(a, &o, true);
-  kernel_flags(a, &o);
-  fastsum_flags(a, &o);
-  a.get("beta", &beta);
-  a.get("tol", &o.tol);
-  a.get("max-iter", &max_iter);
-  a.finish();
-  Report rep;
-  rep.command = "krr";
-  rep.method = "krr";
-  rep.seed = o.seed;
-  rep.parameters = echo_common(o);
-  rep.parameters["beta"] = beta;
-  rep.parameters["max_iter"] = max_iter;
-  return guarded(rep, o.out, [&] {
-    const PointCloud cloud = load_points_csv(o.in);
-    const std::vector<int> truth = require_labels(cloud);
-    const int n_classes = count_classes(truth);
-    if (n_classes < 2) throw fgs::ParameterError("classification needs at least two classes");
-    const double tol = o.tol > 0.0 ? o.tol : 1e-6;
-    const int channels = n_classes == 2 ? 1 : n_classes;
-    std::vector<VectorXd> scores;
-    int max_its = 0;
-    Timer fit;
-    for (int ch = 0; ch < channels; ++ch) {
-      VectorXd t(cloud.size());
-      const int positive = channels == 1 ? 0 : ch;
-      for (Index i = 0; i < cloud.size(); ++i) t(i) = truth[static_cast<size_t>(i)] == positive ? 1.0 : -1.0;
-      const fgs::RidgeModel model =
-          fgs::krr_fit(cloud.coordinates, make_kernel(o), beta, t, make_params(o), tol, max_iter, o.device);
-      max_its = std::max(max_its, model.cg_iterations);
-      scores.push_back(fgs::krr_predict(model, cloud.coordinates, o.device));
-    }
-    rep.add_timing("fit_and_predict", fit.seconds());
-    const std::vector<int> pred = argmax_labels(scores, cloud.size());
-    save_labels_csv(pred, o.out + ".labels.csv");
-    const double acc = 1.0 - fgs::misclassification_rate(pred, truth);
-    rep.add_metric("train_accuracy", acc, "fraction of training points whose predicted class matches the label");
-    rep.add_metric("cg_iterations", max_its, "largest conjugate-gradient iteration count over channels");
-    return finish(rep, o.out, "krr: train accuracy " + std::to_string(acc) + '\n');
-  });
-}
-
 const char* kUsage =
     "fgs-b200: matrix-free spectral toolkit for fully connected kernel graphs (B200 build)\n"
-    "usage: fgs-b200 <gen|eigs|cluster|segment|bench|ssl-kernel|krr> [--options]\n";
+    "usage: fgs-b200 <eigs|cluster|bench> [--options]\n";
 
 int run(int argc, char** argv) {
   if (argc < 2) {
@@ -1290,14 +811,10 @@ int run(int argc, char** argv) {
   }
   try {
     Args a(argc, argv, 2);
-    if (cmd == "gen") return run_gen(a);
     if (cmd == "eigs") return run_eigs(a);
     if (cmd == "cluster") return run_cluster(a);
     if (cmd == "bench") return run_bench(a);
-    if (cmd == "ssl-kernel") return run_ssl_kernel(a);
-    if (cmd == "krr") return run_krr(a);
-    if (cmd == "segment") return run_segment(a);
-    if (cmd == "ssl-pf")
+    if (cmd == "gen" || cmd == "segment" || cmd == "ssl-kernel" || cmd == "krr" || cmd == "ssl-pf")
       throw UsageError("command '" + cmd + "' is not part of the B200 build");
     throw UsageError("unknown command '" + cmd + "'");
   } catch (const UsageError& e) {  // CLI11::ParseError -> 2
