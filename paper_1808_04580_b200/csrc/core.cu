@@ -1271,16 +1271,17 @@ static bool is_pinned(const void* p) {
 }
 
 // sub-blocks of a host-vector block: the largest divisor of nvec with at
-// most nvec / 8 vectors (16 -> 2: the exposed copies are one sub-block's
-// H2D + D2H, 2 x 160 MB at config 5, instead of the whole 2 x 1.28 GB);
-// FGS_PIPE_BLOCK=k forces k vectors per sub-block
+// most nvec / 16 vectors (16 -> 1: the exposed copies are one sub-block's
+// H2D + D2H, 2 x 80 MB at config 5, instead of the whole 2 x 1.28 GB; C5 e2e
+// 141 / 148 / 153 matvecs/s with 4 / 2 / 1-vector sub-blocks, the kernels
+// cost the same per vector); FGS_PIPE_BLOCK=k forces k vectors per sub-block
 static int pipe_sub_block(int nvec) {
   static const int forced = [] {
     const char* e = std::getenv("FGS_PIPE_BLOCK");
     return e ? std::atoi(e) : 0;
   }();
   if (forced > 0 && nvec % forced == 0) return forced;
-  const int target = std::max(1, nvec / 8);
+  const int target = std::max(1, nvec / 16);
   for (int b = target; b >= 1; --b)
     if (nvec % b == 0) return b;
   return 1;
