@@ -167,7 +167,7 @@ class Core {
   cudaStream_t cp_in = nullptr, cp_out = nullptr;
   std::vector<cudaEvent_t> pipe_ev;
   // Lanczos workspace, reused across solves (lanczos.cu)
-  DBuf<double> lz_basis, lz_z, lz_partial, lz_hbuf, lz_scal, lz_qin;
+  DBuf<double> lz_basis, lz_z, lz_partial, lz_partial3, lz_hbuf, lz_scal, lz_qin;
   DBuf<double> lz_alpha, lz_nrm, lz_beta, lz_st;  // run-ahead recurrence scalars
   std::vector<cudaEvent_t> lz_events;              // per-step timing events
   char* bounce = nullptr;  // pinned staging for host_copy (bounce_threads x kBounceChunk)

@@ -20,6 +20,7 @@
 #include "core.cuh"
 #include "lanczos.cuh"
 #include "nccl_shim.hpp"
+#include "tma.cuh"
 
 namespace fgsb {
 
@@ -333,6 +334,98 @@ __global__ void update_kernel(const double* __restrict__ Q, int64_t ldq, int m, 
   z[r] -= acc;
 }
 
+// The first CGS pass's update and the second pass's projection in ONE read
+// of the basis (3 basis sweeps per step instead of 4): each block stages its
+// kTile3 rows of all m columns in shared memory (m bulk copies on one
+// mbarrier), forms z' = z - Q h1 for its rows in update_kernel's exact
+// operation order, stores z', and writes its partials of Q^T z' column-major
+// (partial[j][block]) for reduce_colmajor_kernel.  m <= kTile3Cols.
+// (A persistent, double-buffered variant -- one or two blocks per SM walking
+// the tiles -- measured 18-21 ms per C4 solve against 10.8 ms for this one:
+// four warps per SM cannot hide the tile's compute.)
+constexpr int kTile3 = 128;       // rows per block (= threads)
+constexpr int kTile3Cols = 128;   // basis columns the tile holds (128 KB of shared memory)
+
+__global__ void __launch_bounds__(kTile3) update_multidot_kernel(const double* __restrict__ Q, int64_t ldq, int m,
+                                                                 const double* __restrict__ h, double* __restrict__ z,
+                                                                 int64_t n, double* __restrict__ partial) {
+  pdl_wait();  // PDL launches in the fused step: predecessor complete
+  extern __shared__ __align__(16) double tile[];  // [m][kTile3] | z'[kTile3] | h[m] | mbarrier
+  double* zs = tile + static_cast<size_t>(m) * kTile3;
+  double* hs = zs + kTile3;
+  unsigned long long* mb = reinterpret_cast<unsigned long long*>(hs + ((m + 1) & ~1));
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kTile3;
+  const int rows = static_cast<int>(n - r0 < kTile3 ? n - r0 : kTile3);
+  const bool bulk = rows == kTile3 && (ldq & 1) == 0;  // 16-byte aligned full columns
+  if (bulk) {
+    if (t == 0) {
+      mbar_init(mb, 1);
+      mbar_init_fence();
+      mbar_expect_tx(mb, static_cast<unsigned>(m) * kTile3 * 8u);
+    }
+    __syncthreads();
+    for (int j = t; j < m; j += kTile3)  // one 1 KB copy per column
+      bulk_g2s(tile + static_cast<size_t>(j) * kTile3, Q + static_cast<int64_t>(j) * ldq + r0, kTile3 * 8u, mb);
+  } else {
+    for (int j = 0; j < m; ++j)
+      tile[static_cast<size_t>(j) * kTile3 + t] = t < rows ? Q[static_cast<int64_t>(j) * ldq + r0 + t] : 0.0;
+  }
+  for (int j = t; j < m; j += kTile3) hs[j] = h[j];
+  if (bulk) mbar_wait(mb, 0);
+  __syncthreads();
+  // z' = z - Q h (update_kernel's order: 4-column groups, fma chain over j)
+  double acc = 0.0;
+  int j = 0;
+  for (; j + 4 <= m; j += 4) {
+    acc = fma(tile[static_cast<size_t>(j) * kTile3 + t], hs[j], acc);
+    acc = fma(tile[static_cast<size_t>(j + 1) * kTile3 + t], hs[j + 1], acc);
+    acc = fma(tile[static_cast<size_t>(j + 2) * kTile3 + t], hs[j + 2], acc);
+    acc = fma(tile[static_cast<size_t>(j + 3) * kTile3 + t], hs[j + 3], acc);
+  }
+  for (; j < m; ++j) acc = fma(tile[static_cast<size_t>(j) * kTile3 + t], hs[j], acc);
+  double zv = 0.0;
+  if (t < rows) {
+    zv = z[r0 + t] - acc;
+    z[r0 + t] = zv;
+  }
+  zs[t] = zv;
+  __syncthreads();
+  // block partials of Q^T z': warp w takes columns j = w (mod 4), each lane
+  // rows lane + 32 i in increasing i, then a fixed shuffle tree
+  for (int c = warp; c < m; c += kTile3 / 32) {
+    const double* col = tile + static_cast<size_t>(c) * kTile3;
+    double sacc = 0.0;
+#pragma unroll
+    for (int i = 0; i < kTile3 / 32; ++i) sacc = fma(col[lane + 32 * i], zs[lane + 32 * i], sacc);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, off);
+    if (lane == 0) partial[static_cast<int64_t>(c) * gridDim.x + blockIdx.x] = sacc;
+  }
+}
+
+inline size_t update_multidot_smem(int m) {
+  return sizeof(double) * (static_cast<size_t>(m) * kTile3 + kTile3 + ((m + 1) & ~1) + 2);
+}
+
+// out[j] = sum_b partial[j][b] (column-major partials, one block per
+// column): thread t sums b = t, t + 256, ... in order, then a fixed tree
+__global__ void __launch_bounds__(256) reduce_colmajor_kernel(const double* __restrict__ partial, int nblocks,
+                                                               double* __restrict__ out) {
+  pdl_wait();  // PDL launches in the fused step: predecessor complete
+  __shared__ double red[256];
+  const double* col = partial + static_cast<int64_t>(blockIdx.x) * nblocks;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += 256) s += col[b];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w >= 1; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+}
+
 // z -= alpha q_{m-1} + beta q_{m-2}  (spectral.cpp:186-191); alpha and the
 // previous beta are read from device memory (the host runs ahead)
 __global__ void three_term_kernel(double* __restrict__ z, const double* __restrict__ qcur,
@@ -513,6 +606,19 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   const int nblk = std::max(1, ceil_div(nl, kRowsPerBlock));
   hbuf.alloc(static_cast<size_t>(std::min<int64_t>(n, max_iter) + 2));
   partial.alloc(static_cast<size_t>(nblk) * (std::min<int64_t>(n, max_iter) + 2));
+  // partials of the staged-tile update + projection (steps with <= kTile3Cols columns)
+  const int nblk3 = std::max(1, ceil_div(nl, kTile3));
+  DBuf<double>& partial3 = c.lz_partial3;
+  partial3.alloc(static_cast<size_t>(nblk3) * kTile3Cols);
+  {
+    static bool attr = false;
+    if (!attr) {
+      FGS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(update_multidot_kernel),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(update_multidot_smem(kTile3Cols))));
+      attr = true;
+    }
+  }
   scal.alloc(4);
   FGS_CUDA(cudaMemcpyAsync(basis.p, local.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, st));
 
@@ -534,6 +640,22 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   };
   auto cgs_pass = [&](int m, double* v) {  // v -= Q(Q^T v)
     multidot(basis.p, m, v, hbuf.p);
+    update(basis.p, m, hbuf.p, v);
+  };
+  // two CGS passes (spectral.cpp:193-195) in three basis sweeps: h1 = Q^T v;
+  // v -= Q h1 with h2 = Q^T v from the same staged tile; v -= Q h2
+  auto cgs2 = [&](int m, double* v) {
+    if (m > kTile3Cols) {
+      cgs_pass(m, v);
+      cgs_pass(m, v);
+      return;
+    }
+    multidot(basis.p, m, v, hbuf.p);
+    update_multidot_kernel<<<nblk3, kTile3, update_multidot_smem(m), st>>>(basis.p, nl, m, hbuf.p, v, nl,
+                                                                          partial3.p);
+    reduce_colmajor_kernel<<<m, 256, 0, st>>>(partial3.p, nblk3, hbuf.p);
+    c.launches += 2;
+    allreduce(hbuf.p, m);
     update(basis.p, m, hbuf.p, v);
   };
   auto norm_of = [&](const double* v) -> double {
@@ -630,11 +752,18 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
       launch_ex(reduce_partials_kernel, gr, tu, 0, st, partial.p, nblk, mm, hbuf.p, 0);
       ++c.launches;
     }
-    launch_ex(update_kernel, gu, tu, sizeof(double) * mm, st, basis.p, nl, mm, hbuf.p, z.p, nl);
-    launch_ex(multidot_reduce_kernel, gb, tb, 0, st, basis.p, nl, mm, z.p, nl, partial.p, tk, hbuf.p);
-    if (!tail) {
-      launch_ex(reduce_partials_kernel, gr, tu, 0, st, partial.p, nblk, mm, hbuf.p, 0);
+    if (mm <= kTile3Cols) {  // first update + second projection from one staged tile (cgs2)
+      launch_ex(update_multidot_kernel, dim3(nblk3), dim3(kTile3), update_multidot_smem(mm), st, basis.p, nl, mm,
+                hbuf.p, z.p, nl, partial3.p);
+      launch_ex(reduce_colmajor_kernel, dim3(mm), dim3(256), 0, st, partial3.p, nblk3, hbuf.p);
       ++c.launches;
+    } else {
+      launch_ex(update_kernel, gu, tu, sizeof(double) * mm, st, basis.p, nl, mm, hbuf.p, z.p, nl);
+      launch_ex(multidot_reduce_kernel, gb, tb, 0, st, basis.p, nl, mm, z.p, nl, partial.p, tk, hbuf.p);
+      if (!tail) {
+        launch_ex(reduce_partials_kernel, gr, tu, 0, st, partial.p, nblk, mm, hbuf.p, 0);
+        ++c.launches;
+      }
     }
     launch_ex(update_kernel, gu, tu, sizeof(double) * mm, st, basis.p, nl, mm, hbuf.p, z.p, nl);
     launch_ex(norm_scalars_kernel, gb, tb, 0, st, z.p, nl, partial.p, ticket.p, dalpha.p, dnrm.p, dbeta.p, dst.p, mm);
@@ -658,8 +787,7 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     multidot(qcur, 1, z.p, dalpha.p + (mm - 1));
     three_term_kernel<<<gsz, 256, 0, st>>>(z.p, qcur, mm >= 2 ? basis.p + static_cast<int64_t>(mm - 2) * nl : nullptr,
                                            dalpha.p + (mm - 1), mm >= 2 ? dbeta.p + (mm - 2) : dbeta.p, nl);
-    cgs_pass(mm, z.p);
-    cgs_pass(mm, z.p);
+    cgs2(mm, z.p);
     multidot(z.p, 1, z.p, dnrm.p + (mm - 1));
     lanczos_scalars_kernel<<<1, 1, 0, st>>>(dalpha.p, dnrm.p, dbeta.p, dst.p, mm);
     if (mm < cap) scale_dev_kernel<<<gsz, 256, 0, st>>>(z.p, dst.p + 1, basis.p + static_cast<int64_t>(mm) * nl, nl);
