@@ -14,9 +14,12 @@
 //   G[a][(c, e)] += sum_k wa_k[a] * ((x_k wc_k[c]) we_k[e])
 //   A = wa (8 a x 4 points, straight from the staged taps, no product),
 //   B = (x wc) we (4 points x 8 e of one c): one DMUL per fragment.
-// x is folded into wc once per staged slot (in place, after the chunk lands),
-// so a warp's K-step is 6 LDS + 4 DMUL +
-// 8 DMMA (v5: 8 LDS + 6 DMUL, plus the lane masks).  Warp w owns the box
+// x multiplies the staged wc per K-step (x0 = x wc[c0], x1 = x wc[c0 + 8]),
+// so a warp's K-step is 7 LDS + 6 DMUL +
+// 8 DMMA (v5: 8 LDS + 6 DMUL, plus the lane masks).  (Folding x into wc
+// once per slot cooperatively -- each warp a share of a chunk, one chunk
+// ahead, a `folded` mbarrier -- saves 2 DMUL per K-step but re-couples the
+// warps like a per-chunk barrier: C5 spread 48.9 -> 51.7 ms.)  Warp w owns the box
 // c-rows = w (mod 8): in a run with origin o1 its two c values are
 // c0 = (w - o1) mod 8 and c0 + 8, both a-tiles and both e-halves (16
 // accumulators per lane); flushes of consecutive runs never touch another
