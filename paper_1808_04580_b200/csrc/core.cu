@@ -312,10 +312,11 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
     if (dense)
       return launch_smem(spread_v4_2d_kernel<T, kSpread2dP>, nitems, Blk4d2<T, kSpread2dP>::NT, smem, s, a, box_stride);
   }
-  if constexpr (D == 3 && T == 16) {
-    if (a.slots != nullptr) {
+  if constexpr (D == 3 && (T == 16 || T == 12)) {
+    if (a.slots != nullptr) {  // run-aligned slot layout: v6 interpolation; 2m = 16 v6 spread
       if (interp) return launch_smem(interp_v6_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
-      return launch_smem(spread_v6_kernel, nitems, Blk6s::NT, smem, s, a, box_stride);
+      if constexpr (T == 16) return launch_smem(spread_v6_kernel, nitems, Blk6s::NT, smem, s, a, box_stride);
+      // 2m = 12: the v4 spread below reads the slot rows (stride 3 2m) and the slot-ordered x
     }
   }
   if constexpr (has_v4_3d<D, T>()) {
@@ -948,7 +949,7 @@ void Core::build_plan(const double* nodes_colmajor) {
   // multiple of kSlotAlign slots, items are consecutive; same item order and
   // boxes as the point layout, so the assembly map serves both
   use_slots = false;
-  if (kind == FASTSUM && d == 3 && T == 16 && nitems > 0 && mean_run >= kDenseRun && v6_enabled()) {
+  if (kind == FASTSUM && d == 3 && (T == 16 || T == 12) && nitems > 0 && mean_run >= kDenseRun && v6_enabled()) {
     std::vector<DItem> sitems(ditems);
     std::vector<DRun> sruns(druns);
     std::vector<int>& smap = slot_host;
@@ -986,7 +987,7 @@ void Core::build_plan(const double* nodes_colmajor) {
   runs.upload(druns.data(), druns.size(), stream);
 
   // window taps of the local slice in internal order, or (slot layout) in
-  // slot order with rows padded to kSlotRow doubles, pad slots zero
+  // slot order with rows padded to slot_row<2m>() doubles, pad slots zero
   if (use_slots) {
     std::vector<int> rows(slot_host.size());
     for (size_t i = 0; i < rows.size(); ++i)
@@ -994,8 +995,9 @@ void Core::build_plan(const double* nodes_colmajor) {
     DBuf<int> drows;
     drows.upload(rows.data(), rows.size(), stream);
     const int64_t ns = static_cast<int64_t>(rows.size());
-    taps.alloc(static_cast<size_t>(ns) * kSlotRow);
-    TapArgs ta{dnodes.p, n, ns, perm.p + offset, d, M, m, rho, b_kb, kind == FASTSUM ? 1 : 0, taps.p, drows.p, kSlotRow};
+    const int srow = slot_row_of(T);
+    taps.alloc(static_cast<size_t>(ns) * srow);
+    TapArgs ta{dnodes.p, n, ns, perm.p + offset, d, M, m, rho, b_kb, kind == FASTSUM ? 1 : 0, taps.p, drows.p, srow};
     taps_kernel<<<ceil_div(ns, 128), 128, 0, stream>>>(ta);
     ++launches;
     FGS_CUDA(cudaGetLastError());
@@ -1145,8 +1147,9 @@ size_t Core::smem_bytes(bool interp) const {
   const LaunchShape sh = d == 3 ? shape_of<3>(T, dense) : (d == 2 ? shape_of<2>(T, dense) : shape_of<1>(T, dense));
   size_t boxes = static_cast<size_t>(box_stride);
   if (interp && d == 3 && kInterpV5 && (T == 8 || T == 12 || T == 16)) boxes = static_cast<size_t>(box_pad);
-  if (use_slots && interp) return (boxes + v6i_extra_doubles<16>()) * sizeof(double);
-  if (use_slots && !interp) return (boxes + v6s_extra_doubles()) * sizeof(double);
+  if (use_slots && interp)
+    return (boxes + (T == 16 ? v6i_extra_doubles<16>() : v6i_extra_doubles<12>())) * sizeof(double);
+  if (use_slots && !interp && T == 16) return (boxes + v6s_extra_doubles()) * sizeof(double);
   if (d == 3 && !interp && dense) boxes *= static_cast<size_t>(v4_spread_groups(T));  // per-group boxes
   if (d == 2 && !interp && dense && (T == 8 || T == 12 || T == 16))
     boxes *= static_cast<size_t>(kSpread2dP);  // per-stream boxes

@@ -326,12 +326,13 @@ __global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
 
   for (int vec = 0; vec < a.nvec; ++vec) {
-    const double* xv = a.x + vec * a.ldx;
+    // slot layout (2m = 12 dense plans): x pre-gathered into slot order
+    const double* xv = a.xs ? a.xs + vec * a.ldxs : a.x + vec * a.ldx;
     for (int g = 0; g < NB; ++g)
       for (int v = tid; v < V; v += NT) S[g * box_stride_smem + v] = 0.0;
     v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
     cp_async_commit();
-    if (tid < QS && p_begin + tid < p_end) xs[tid] = v2_x(a, xv, p_begin + tid);
+    if (tid < QS && p_begin + tid < p_end) xs[tid] = a.xs ? xv[p_begin + tid] : v2_x(a, xv, p_begin + tid);
     int r = it.run_begin;
     DRun run = a.runs[r];
     double C[TW][NE][2];
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(Blk4<T, false, PS, QSZ>::NT) spread_v4_kernel(
         qn = static_cast<int>(lmin(QS, p_end - c1));
         v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, qn, tid, NT);
         cp_async_commit();
-        if (tid < qn) xnext = v2_x(a, xv, c1 + tid);
+        if (tid < qn) xnext = a.xs ? xv[c1 + tid] : v2_x(a, xv, c1 + tid);
       }
       const double* sb = stg + buf * QS * SR;
       const double* xb = xs + buf * QS;
@@ -673,7 +674,8 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) spread_v4_2d_kernel(PassArg
   const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
 
   for (int vec = 0; vec < a.nvec; ++vec) {
-    const double* xv = a.x + vec * a.ldx;
+    // slot layout (2m = 12 dense plans): x pre-gathered into slot order
+    const double* xv = a.xs ? a.xs + vec * a.ldxs : a.x + vec * a.ldx;
     for (int g = 0; g < NB; ++g)
       for (int v = tid; v < V; v += NT) S[g * box_stride_smem + v] = 0.0;
     v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);

@@ -43,7 +43,16 @@
 namespace fgsb {
 
 constexpr int kSlotAlign = 8;  // run starts in the slot space
-constexpr int kSlotRow = 52;   // doubles per slot-ordered taps row: wa | wc | we | 4 pad (= 4 mod 16)
+// doubles per slot-ordered taps row: wa | wc | we | pad, = 4 (mod 16) -- the
+// interpolation's staged row (Blk5<T>::STRIDE): 52 for 2m = 16, 36 for 2m = 12
+// (= 3 2m, the v4 spread's staging stride, so it reads the slot rows as is)
+template <int T>
+constexpr int slot_row() {
+  return Blk5<T>::STRIDE;
+}
+constexpr int kSlotRow = slot_row<16>();
+inline int slot_row_of(int T) { return T == 16 ? slot_row<16>() : slot_row<12>(); }
+static_assert(slot_row<12>() == 36, "2m = 12 slot rows are unpadded");
 
 struct Blk6s {
   static constexpr int T = 16;
@@ -226,7 +235,7 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a, i
   pdl_wait();
   using B = Blk5<T>;
   constexpr int TA = B::TA, TC = B::TC, KS = B::KS, W = B::W, NT = B::NT, SR = B::STRIDE;
-  static_assert(SR == kSlotRow, "staged row = global slot-ordered row");
+  static_assert(SR == slot_row<T>(), "staged row = global slot-ordered row");
   extern __shared__ __align__(16) double smem[];
   double* S = smem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
