@@ -6,8 +6,8 @@ roofline fraction of the dominant kernel).  One step = one application of
 L_s = I - D^-1/2 W D^-1/2 to a block of `nvec` seeded N(0,1) vectors on the
 BASELINE configuration's synthetic point set.  Default workload: config 5
 (`configs[4]`, the largest single-GPU configuration: a block of 16 vectors at
-n = 10M points in 3-D, N = 64, m = 8); configs 2 and 4 are reported under
-"also" with their Lanczos time-to-k.
+n = 10M points in 3-D, N = 64, m = 8); configs 1-4 are reported under
+"also" with their Lanczos time-to-k (k = 10 / 10 / 4 / 20).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--weak]
                   [--impl b200|reference] [--emulate N]
@@ -62,7 +62,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0)
-    p.add_argument("--also", default="2,4", help="comma list of extra configs measured after the main line "
+    p.add_argument("--also", default="1,2,3,4", help="comma list of extra configs measured after the main line "
                    "(device matvecs/s + Lanczos time-to-k), '' to skip")
     p.add_argument("--emulate", type=int, default=0,
                    help="single GPU: time the N-rank sharded path as an emulated shard group (per-rank compute "
