@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import paper_1808_04580_b200 as fgs
-from test_cli import EXE, check_report, run
+from test_cli import EXE, check_report, run, write_spiral_csv
 
 pytestmark = pytest.mark.gpu
 
@@ -59,7 +59,7 @@ def test_nystrom_top_pair_close_to_lanczos():
 
 def test_cli_nystrom_method(tmp_path):
     out = tmp_path / "s.csv"
-    assert run(EXE, "gen", "--spiral", "--per-class", 200, "--out", out, "--seed", 2).returncode == 0
+    write_spiral_csv(out, per_class=200, seed=2)
     rep_path = tmp_path / "ny.json"
     r = run(EXE, "eigs", "--in", out, "--out", rep_path, "--sigma", 3.5, "--k", 4, "--method", "nystrom-gauss-nfft",
             "--L", 40, "--M", 8)
