@@ -54,12 +54,22 @@ constexpr int kSlotRow = slot_row<16>();
 inline int slot_row_of(int T) { return T == 16 ? slot_row<16>() : slot_row<12>(); }
 static_assert(slot_row<12>() == 36, "2m = 12 slot rows are unpadded");
 
+#ifndef FGS_V6S_QS
+#define FGS_V6S_QS 32
+#endif
+#ifndef FGS_V6S_NS
+#define FGS_V6S_NS 4
+#endif
+#ifndef FGS_V6S_MINB
+#define FGS_V6S_MINB 2
+#endif
 struct Blk6s {
   static constexpr int T = 16;
   static constexpr int W = 8;       // warps; warp w owns box c-rows = w (mod 8)
   static constexpr int NT = 32 * W;
-  static constexpr int QS = 32;     // slots per staged chunk (multiple of kSlotAlign)
-  static constexpr int NS = 4;      // ring stages
+  static constexpr int QS = FGS_V6S_QS;  // slots per staged chunk (multiple of kSlotAlign)
+  static constexpr int NS = FGS_V6S_NS;  // ring stages
+  static constexpr int MINB = FGS_V6S_MINB;  // CTAs per SM the registers are budgeted for
   // staged slot row = the global slot-ordered taps row: wa[16] | wc[16] |
   // we[16] | pad; 52 = 4 (mod 16) doubles -> the 4 slots of a K-step sit on
   // distinct bank groups
@@ -90,7 +100,7 @@ __global__ void slot_gather_kernel(PassArgs a, int64_t nslots, double* out) {
   }
 }
 
-__global__ void __launch_bounds__(Blk6s::NT, 2) spread_v6_kernel(PassArgs a, int box_stride_smem) {
+__global__ void __launch_bounds__(Blk6s::NT, Blk6s::MINB) spread_v6_kernel(PassArgs a, int box_stride_smem) {
   pdl_wait();
   using B = Blk6s;
   constexpr int T = B::T, NT = B::NT, QS = B::QS, SR = B::SR, NS = B::NS, W = B::W;
