@@ -221,6 +221,15 @@ constexpr int v5s_w() {
 constexpr int kSpread2dP = 1;
 // d = 3, 2m = 16 dense plans: run-aligned slot layout + kernels_v6.cuh
 // (FGS_V6=0: the v5 kernels over the plain point order)
+// slot-layout interpolation with two batches per B-fragment load
+// (interp_v7_kernel); FGS_INTERP_V7=0 selects interp_v6_kernel
+bool interp_v7_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("FGS_INTERP_V7");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
 bool v6_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("FGS_V6");
@@ -314,7 +323,13 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
   }
   if constexpr (D == 3 && (T == 16 || T == 12)) {
     if (a.slots != nullptr) {  // run-aligned slot layout: v6 interpolation; 2m = 16 v6 spread
-      if (interp) return launch_smem(interp_v6_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+      if (interp) {
+        // two batches per B load: 2m = 16 (C5 interp 48.8 -> 47.8 ms); 2m = 12
+        // loses with it (C4 314 -> 332 us: fewer K-steps per B fragment)
+        if constexpr (T == 16)
+          if (interp_v7_on()) return launch_smem(interp_v7_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+        return launch_smem(interp_v6_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+      }
       if constexpr (T == 16) return launch_smem(spread_v6_kernel, nitems, Blk6s::NT, smem, s, a, box_stride);
       // 2m = 12: the v4 spread below reads the slot rows (stride 3 2m) and the slot-ordered x
     }

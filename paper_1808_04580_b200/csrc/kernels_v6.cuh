@@ -365,4 +365,182 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// interpolation, two batches per B-fragment load (interp_v7_kernel<T>).
+// A warp takes units of two consecutive 8-slot batches (16 slots, one bulk
+// copy).  When both batches belong to the same run they share every B
+// fragment: each grid value read from the box feeds two DMMAs (the A
+// fragments of the two batches), halving the shared-memory loads per DMMA.
+// The unit's taps move to registers right after they land, so one staging
+// buffer per warp suffices (the next unit is copied into it while this one
+// computes).  A unit whose batches straddle two runs runs them one by one.
+// ---------------------------------------------------------------------------
+template <int T>
+struct V7Frag {
+  double aF[Blk5<T>::KS];
+  double wa[Blk5<T>::TA];
+  double wc[Blk5<T>::TC][2];
+};
+
+template <int T>
+__device__ __forceinline__ void v7_load(V7Frag<T>& f, const double* w, int q) {
+#pragma unroll
+  for (int t = 0; t < Blk5<T>::TA; ++t) f.wa[t] = w[2 * t + (q >> 1)];
+#pragma unroll
+  for (int t = 0; t < Blk5<T>::TC; ++t) {
+    f.wc[t][0] = w[T + 4 * t + 2 * (q & 1)];
+    f.wc[t][1] = w[T + 4 * t + 2 * (q & 1) + 1];
+  }
+#pragma unroll
+  for (int ks = 0; ks < Blk5<T>::KS; ++ks) f.aF[ks] = w[2 * T + 4 * ks + q];  // zero on pad slots
+}
+
+// y partial of NB (1 or 2) batches sharing the footprint block gb
+template <int T, int NB>
+__device__ __forceinline__ void v7_compute(const V7Frag<T>* f, const double* gb, int ra, int rc, double* yacc) {
+  constexpr int TA = Blk5<T>::TA, TC = Blk5<T>::TC, KS = Blk5<T>::KS;
+#pragma unroll
+  for (int h = 0; h < NB; ++h) yacc[h] = 0.0;
+#pragma unroll
+  for (int ta = 0; ta < TA; ++ta) {
+    double z[NB][TC][2];
+#pragma unroll
+    for (int h = 0; h < NB; ++h)
+#pragma unroll
+      for (int tc = 0; tc < TC; ++tc) z[h][tc][0] = z[h][tc][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int tc = 0; tc < TC; ++tc) {
+        const double bv = gb[ta * ra + tc * rc + 4 * ks];
+#pragma unroll
+        for (int h = 0; h < NB; ++h) dmma(z[h][tc][0], z[h][tc][1], f[h].aF[ks], bv);
+      }
+#pragma unroll
+    for (int h = 0; h < NB; ++h) {
+      double K = 0.0;
+#pragma unroll
+      for (int tc = 0; tc < TC; ++tc) {
+        K = fma(f[h].wc[tc][0], z[h][tc][0], K);
+        K = fma(f[h].wc[tc][1], z[h][tc][1], K);
+      }
+      yacc[h] = fma(f[h].wa[ta], K, yacc[h]);
+    }
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v7_kernel(PassArgs a, int box_doubles) {
+  pdl_wait();
+  using B = Blk5<T>;
+  constexpr int W = B::W, NT = B::NT, SR = B::STRIDE;
+  static_assert(SR == slot_row<T>(), "staged row = global slot-ordered row");
+  extern __shared__ __align__(16) double smem[];
+  double* S = smem;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, r8 = lane >> 2;
+  double* buf = smem + box_doubles + static_cast<size_t>(warp) * 2 * B::SLOT;  // 16 slot rows
+  unsigned long long* mb =
+      reinterpret_cast<unsigned long long*>(smem + box_doubles + static_cast<size_t>(W) * 2 * B::SLOT) + warp;
+  const DItem it = a.items[blockIdx.x];
+  const int bx1 = it.e1, e2 = it.e2, sp2 = v5_pad(e2);
+  const int rows = it.e0 * it.e1;
+  const int M = a.M;
+  const int s_begin = it.p_begin;
+  const int nb = (it.p_end - s_begin) / 8;  // 8-slot batches of the item
+  const int nu = (nb + 1) / 2;             // units of two batches
+  const int ra = 2 * bx1 * sp2, rc = 4 * sp2;
+  const int bbase = s_begin >> 3;          // global index of the item's first batch
+  if (lane == 0) {
+    mbar_init(mb, 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  auto issue = [&](int u) {  // lane 0: the unit's 8 or 16 taps rows, one bulk copy
+    const int cnt = min(2, nb - 2 * u) * 8;
+    fence_proxy_async();
+    mbar_expect_tx(mb, static_cast<unsigned>(cnt) * SR * 8u);
+    bulk_g2s(buf, a.taps + static_cast<int64_t>(s_begin + 16 * u) * SR, static_cast<unsigned>(cnt) * SR * 8u, mb);
+  };
+  const bool need_s = a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN;
+  unsigned phase = 0;
+
+  for (int vec = 0; vec < a.nvec; ++vec) {
+    const double* gv = a.grid + vec * a.grid_stride;
+    const double* xv = a.x ? a.x + vec * a.ldx : nullptr;
+    double* yv = a.y ? a.y + vec * a.ldy : nullptr;
+    const bool need_x = xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE;
+    if (warp < nu && lane == 0) issue(warp);
+    if (vec > 0) __syncthreads();  // every warp is done with the previous vector's box
+    for (int v = tid; v < rows * e2; v += NT) {
+      const int row = v / e2, x2 = v - row * e2;
+      const int x0 = row / bx1, x1 = row - x0 * bx1;
+      S[row * sp2 + x2] = gv[(static_cast<int64_t>((it.a0 + x0) % M) * M + (it.a1 + x1) % M) * M + (it.a2 + x2) % M];
+    }
+    __syncthreads();
+
+    for (int u = warp; u < nu; u += W) {
+      const int nbat = min(2, nb - 2 * u);
+      int src[2], off[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int b = min(2 * u + h, nb - 1);
+        src[h] = h < nbat ? a.slots[s_begin + 8 * b + r8] : -1;
+        off[h] = a.boff[bbase + b];
+      }
+      double xin[2], sin_[2];
+      int64_t ix[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool mine = q == 0 && src[h] >= 0;
+        ix[h] = mine ? (a.perm ? static_cast<int64_t>(a.perm[src[h]]) : src[h]) : 0;
+        xin[h] = need_x && mine ? xv[ix[h]] : 0.0;
+        sin_[h] = need_s && mine ? a.s[src[h]] : 1.0;
+      }
+      mbar_wait(mb, phase);
+      phase ^= 1u;
+      V7Frag<T> f[2];
+      v7_load<T>(f[0], buf + r8 * SR, q);
+      if (nbat == 2) v7_load<T>(f[1], buf + (8 + r8) * SR, q);
+      __syncwarp();  // every lane has its taps: the buffer takes the next unit
+      if (u + W < nu && lane == 0) issue(u + W);
+      double yacc[2] = {0.0, 0.0};
+      auto footprint = [&](int o) {
+        const int o0 = o & 1023, o1 = (o >> 10) & 1023, o2 = (o >> 20) & 1023;
+        return S + ((o0 + (r8 >> 2)) * bx1 + (o1 + (r8 & 3))) * sp2 + o2 + q;
+      };
+      if (nbat == 2 && off[0] == off[1]) {
+        v7_compute<T, 2>(f, footprint(off[0]), ra, rc, yacc);
+      } else {
+        v7_compute<T, 1>(&f[0], footprint(off[0]), ra, rc, &yacc[0]);
+        if (nbat == 2) v7_compute<T, 1>(&f[1], footprint(off[1]), ra, rc, &yacc[1]);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double yv_ = yacc[h];
+        yv_ += __shfl_xor_sync(0xffffffffu, yv_, 1);
+        yv_ += __shfl_xor_sync(0xffffffffu, yv_, 2);
+        if (q == 0 && src[h] >= 0) {
+          const int sr = src[h];
+          if (a.epilogue == EPI_DEGREE) {
+            const double dg = yv_ - a.k0;  // graphop.cpp:55-56
+            a.degrees[sr] = dg;
+            a.inv_sqrt[sr] = 1.0 / sqrt(dg);
+            if (!(dg > 0.0)) atomicMin(a.bad_flag, static_cast<unsigned long long>(a.caller[sr]));
+          } else {
+            double out;
+            switch (a.epilogue) {
+              case EPI_KERNEL: out = yv_; break;
+              case EPI_WEIGHT: out = yv_ - a.k0 * xin[h]; break;
+              case EPI_NORMALIZED: out = sin_[h] * (yv_ - a.k0 * __dmul_rn(sin_[h], xin[h])); break;
+              default: out = xin[h] - sin_[h] * (yv_ - a.k0 * __dmul_rn(sin_[h], xin[h])); break;
+            }
+            yv[ix[h]] = out;
+          }
+        }
+      }
+    }
+  }
+}
+
 }  // namespace fgsb

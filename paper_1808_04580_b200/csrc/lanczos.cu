@@ -26,8 +26,14 @@ namespace fgsb {
 
 namespace {
 
-constexpr int kRedThreads = 256;
-constexpr int kRowsPerThread = 8;
+#ifndef FGS_LZ_RPT
+#define FGS_LZ_RPT 8
+#endif
+#ifndef FGS_LZ_THREADS
+#define FGS_LZ_THREADS 256
+#endif
+constexpr int kRedThreads = FGS_LZ_THREADS;
+constexpr int kRowsPerThread = FGS_LZ_RPT;  // tuning builds: FGS_NVCC_DEFINES="FGS_LZ_RPT=4" 
 constexpr int kRowsPerBlock = kRedThreads * kRowsPerThread;
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
