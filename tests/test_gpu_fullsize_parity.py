@@ -2,7 +2,7 @@
 
 * Config 5 at its full size (10M points, 2m = 16): the production fp64
   tensor-core spread / interpolation over the run-aligned slot layout
-  (`spread_v6_kernel`, `interp_v6_kernel<16>`) in a multi-vector block, against the CPU
+  (`spread_v6_kernel`, `interp_v7_kernel<16>`) in a multi-vector block, against the CPU
   oracle (pinned bit for bit to the reference binary, tests/test_ref_pin.py)
   at the north-star matvec tolerance rel-l2 <= 1e-10.  The oracle's NFFT loops
   run on all host cores here (orc.threads; per-thread spread grids summed in
