@@ -9,7 +9,7 @@ mkdir -p profiles/${pre}_bench
 for k in spread interp; do
   { python tools/ncu_summary.py gpurun_out/${tag}_$k.ncu-rep;
     echo; echo '## per-instruction stall samples (SASS, `tools/sass_stalls.py`)'; echo; echo '```';
-    python tools/sass_stalls.py gpurun_out/${tag}_$k.ncu-rep "${k}_v6" 30; echo '```'; } > profiles/${pre}_c5_${k}_ncu.md
+    python tools/sass_stalls.py gpurun_out/${tag}_$k.ncu-rep "${k}_v[67]" 30; echo '```'; } > profiles/${pre}_c5_${k}_ncu.md
 done
 cp gpurun_out/${tag}_launches.csv profiles/${pre}_launches_c5.csv
 tail -1 gpurun_out/${tag}_bench.json > profiles/${pre}_bench/default_c5.json
