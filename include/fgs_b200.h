@@ -199,6 +199,13 @@ fgs_status fgs_shard_group_stats(fgs_shard_group_t g, int rank, int64_t* n_local
  * NVLink figure) */
 fgs_status fgs_shard_group_profile(fgs_shard_group_t g, fgs_op op, const double* dx, double* dy, int nvec, int64_t ld,
                                    int reps, double* shard_ms, double* exchange_ms);
+/* per-shard stage times of `reps` applies (CUDA events between the launches,
+ * as fgs_adjacency_profile_read): stage_ms[world][6] = spread (+ slot
+ * gather), assembly, forward plane pass, line passes (+ the exchange and the
+ * other shards' phase-1 work that runs between them on one GPU), inverse
+ * plane pass, interpolation; mean ms per apply */
+fgs_status fgs_shard_group_stage_profile(fgs_shard_group_t g, fgs_op op, const double* dx, double* dy, int nvec,
+                                         int64_t ld, int reps, double* stage_ms);
 void fgs_shard_group_destroy(fgs_shard_group_t g);
 
 /* ---- lanczos_largest (spectral.hpp:68-70, spectral.cpp:141-256) ---------

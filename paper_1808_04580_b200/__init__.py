@@ -481,7 +481,10 @@ class ShardGroup:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().fgs_shard_group_destroy(self._h)
+            try:
+                lib().fgs_shard_group_destroy(self._h)
+            except Exception:  # noqa: BLE001 - interpreter teardown: module globals already gone
+                pass
             self._h = None
 
     def apply_device(self, op, dx_ptr: int, dy_ptr: int, nvec=1, ld=None):
@@ -499,6 +502,16 @@ class ShardGroup:
         _check(lib().fgs_shard_group_profile(self._h, int(op), C.c_void_p(dx_ptr), C.c_void_p(dy_ptr), int(nvec),
                                              C.c_int64(ld), int(reps), _dp(ms), C.byref(ex)))
         return ms, ex.value
+
+    def stage_profile(self, op, dx_ptr: int, dy_ptr: int, nvec=1, ld=None, reps=3):
+        """[world][6] mean ms per apply: spread, assembly, forward planes,
+        lines (+ exchange and the other shards' work between), inverse
+        planes, interpolation."""
+        ld = ld if ld is not None else self._n
+        ms = np.zeros((self.world, 6))
+        _check(lib().fgs_shard_group_stage_profile(self._h, int(op), C.c_void_p(dx_ptr), C.c_void_p(dy_ptr),
+                                                   int(nvec), C.c_int64(ld), int(reps), _dp(ms)))
+        return ms
 
     def stats(self, rank: int) -> dict:
         nl, p0, pn, it = C.c_int64(), C.c_int(), C.c_int(), C.c_int()

@@ -574,6 +574,30 @@ fgs_status fgs_shard_group_profile(fgs_shard_group_t g, fgs_op op, const double*
   });
 }
 
+fgs_status fgs_shard_group_stage_profile(fgs_shard_group_t g, fgs_op op, const double* dx, double* dy, int nvec,
+                                         int64_t ld, int reps, double* stage_ms) {
+  return guard([&] {
+    need(g, "group");
+    need(dx, "x");
+    need(dy, "y");
+    need(stage_ms, "stage_ms");
+    if (nvec < 1 || reps < 1) fail(FGS_ESHAPE, "nvec and reps must be >= 1");
+    bool scale = false;
+    const int epi = epilogue_of(op, &scale);
+    FGS_CUDA(cudaSetDevice(g->group->device));
+    auto& sh = g->group->shards;
+    for (auto& c : sh) c->enable_profile(true);
+    for (int r = 0; r < reps; ++r) g->group->apply(epi, dx, dy, ld, nvec, scale);
+    for (size_t r = 0; r < sh.size(); ++r) {
+      int64_t napp = 0;
+      double ms[Core::ST_COUNT];
+      sh[r]->read_profile(ms, &napp);
+      sh[r]->enable_profile(false);
+      for (int k = 0; k < Core::ST_COUNT; ++k) stage_ms[r * Core::ST_COUNT + k] = napp ? ms[k] / napp : 0.0;
+    }
+  });
+}
+
 void fgs_shard_group_destroy(fgs_shard_group_t g) { delete g; }
 
 // ---- lanczos_largest -------------------------------------------------------

@@ -1464,8 +1464,10 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
   a.caller = perm.p + offset;
   a.defer_epilogue = n_local >= 100000 ? 1 : 0;
 
-  std::vector<cudaEvent_t> evs;
-  if (profile_) mark(evs);
+  // stage events persist across the two phases of a shard-group apply
+  std::vector<cudaEvent_t>& evs = prof_evs_;
+  if (pre) evs.clear();
+  if (profile_ && pre) mark(evs);
   if (pre && use_slots && nitems > 0) {  // the vectors in slot order for the v6 spread (pads 0, s applied)
     const int64_t ns = static_cast<int64_t>(slot_map.n);
     a.xs = w.xs.p;
@@ -1578,7 +1580,8 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
   launch_interp(a);
   if (profile_) {
     mark(evs);
-    ev_pending_.push_back(std::move(evs));
+    ev_pending_.push_back(evs);
+    evs.clear();
   }
 }
 

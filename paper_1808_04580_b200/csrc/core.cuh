@@ -253,6 +253,7 @@ class Core {
   bool profile_ = false;
   std::vector<cudaEvent_t> ev_pool_;
   std::vector<std::vector<cudaEvent_t>> ev_pending_;
+  std::vector<cudaEvent_t> prof_evs_;  // the apply in flight (phase 1 -> phase 2)
   cudaEvent_t stage_event();
   void mark(std::vector<cudaEvent_t>& evs);
   void build_plan(const double* nodes_colmajor);
