@@ -23,6 +23,9 @@
 // the window spectra of the ranks (Core::apply_launches).
 #pragma once
 
+#include <cstdlib>
+#include <string>
+
 #include "conv2d.cuh"
 
 namespace fgsb {
@@ -51,9 +54,9 @@ constexpr int kConv3Lines = 16;  // (l1, k2) lines per CTA of the line pass
 __host__ __device__ inline int conv3_nw(int M, int N) { return M == N ? N : N + 1; }  // M == N: +N/2 aliases -N/2
 
 // shared memory of the plane passes: tw[M] | X[M][H] | buf[S][M] | scratch[S][M + 16]
-inline size_t conv3_plane_smem(int M, int N) {
+inline size_t conv3_plane_smem(int M, int N, int S = 0) {
   const size_t H = static_cast<size_t>(N / 2 + 1);
-  const size_t S = M <= 64 ? 32 : 16;
+  if (S == 0) S = M <= 64 ? 32 : 16;
   return sizeof(double2) * (static_cast<size_t>(M) + static_cast<size_t>(M) * H + S * (2 * M + 16));
 }
 // line pass: tw[M] | buf[L][M] | scratch[L][M + 16]
@@ -61,8 +64,8 @@ inline size_t conv3_line_smem(int M) {
   return sizeof(double2) * (static_cast<size_t>(M) + static_cast<size_t>(kConv3Lines) * (2 * M + 16));
 }
 
-template <int M>
-__global__ void __launch_bounds__(kConv3Threads) conv3_planes_fwd_kernel(Conv3Args a) {
+template <int M, int S = conv3_seq<M>(), int NT = kConv3Threads>
+__global__ void __launch_bounds__(NT) conv3_planes_fwd_kernel(Conv3Args a) {
   extern __shared__ double2 sm3[];
   const int N = a.N, H = N / 2 + 1, hN = N / 2, NW = conv3_nw(M, N);
   const int u0 = (a.plane0 + static_cast<int>(blockIdx.x) % a.planes) & (M - 1);  // cyclic slab
@@ -70,14 +73,14 @@ __global__ void __launch_bounds__(kConv3Threads) conv3_planes_fwd_kernel(Conv3Ar
   double2* tws = sm3;
   double2* X = tws + M;
   double2* buf = X + M * H;
-  double2* scr = buf + conv3_seq<M>() * M;
+  double2* scr = buf + S * M;
   pdl_wait();
   for (int j = threadIdx.x; j < M; j += blockDim.x) tws[j] = a.tw[j];
   __syncthreads();
   const double* g = a.grid_in + v * a.grid_stride + static_cast<int64_t>(u0) * M * M;
-  // rows: 2p and 2p+1 packed as z_p = g[2p] + i g[2p+1], conv3_seq<M>() pairs per round
-  for (int p0 = 0; p0 < M / 2; p0 += conv3_seq<M>()) {
-    const int np = min(conv3_seq<M>(), M / 2 - p0);
+  // rows: 2p and 2p+1 packed as z_p = g[2p] + i g[2p+1], S pairs per round
+  for (int p0 = 0; p0 < M / 2; p0 += S) {
+    const int np = min(S, M / 2 - p0);
     fft_batch<M, false>(
         scr, np, tws,
         [&](int p, int u) {
@@ -98,8 +101,8 @@ __global__ void __launch_bounds__(kConv3Threads) conv3_planes_fwd_kernel(Conv3Ar
   }
   // columns k2: keep |l1| <= N/2, window index i = l1 + N/2
   double2* out = a.win + (static_cast<int64_t>(v) * M + u0) * NW * H;
-  for (int c0 = 0; c0 < H; c0 += conv3_seq<M>()) {
-    const int nc = min(conv3_seq<M>(), H - c0);
+  for (int c0 = 0; c0 < H; c0 += S) {
+    const int nc = min(S, H - c0);
     fft_batch<M, false>(
         scr, nc, tws, [&](int j, int u) { return X[u * H + c0 + j]; },
         [&](int j, int q, double2 f) {
@@ -167,8 +170,8 @@ __global__ void __launch_bounds__(kConv3Threads) conv3_lines_kernel(Conv3Args a,
       });
 }
 
-template <int M>
-__global__ void __launch_bounds__(kConv3Threads) conv3_planes_inv_kernel(Conv3Args a) {
+template <int M, int S = conv3_seq<M>(), int NT = kConv3Threads>
+__global__ void __launch_bounds__(NT) conv3_planes_inv_kernel(Conv3Args a) {
   extern __shared__ double2 sm3[];
   const int N = a.N, H = N / 2 + 1, hN = N / 2, NW = conv3_nw(M, N);
   const int u0 = (a.plane0 + static_cast<int>(blockIdx.x) % a.planes) & (M - 1);  // cyclic slab
@@ -176,14 +179,14 @@ __global__ void __launch_bounds__(kConv3Threads) conv3_planes_inv_kernel(Conv3Ar
   double2* tws = sm3;
   double2* X = tws + M;
   double2* buf = X + M * H;
-  double2* scr = buf + conv3_seq<M>() * M;
+  double2* scr = buf + S * M;
   pdl_wait();
   for (int j = threadIdx.x; j < M; j += blockDim.x) tws[j] = a.tw[j];
   __syncthreads();
   const double2* in = a.win + (static_cast<int64_t>(v) * M + u0) * NW * H;
   // columns k2: inverse along u1 from the kept l1
-  for (int c0 = 0; c0 < H; c0 += conv3_seq<M>()) {
-    const int nc = min(conv3_seq<M>(), H - c0);
+  for (int c0 = 0; c0 < H; c0 += S) {
+    const int nc = min(S, H - c0);
     fft_batch<M, true>(
         scr, nc, tws,
         [&](int j, int q) {
@@ -195,8 +198,8 @@ __global__ void __launch_bounds__(kConv3Threads) conv3_planes_inv_kernel(Conv3Ar
   }
   // rows: Z = S_even + i S_odd, S the Hermitian extension of X' (C2R)
   double* g = a.grid_out + v * a.grid_stride + static_cast<int64_t>(u0) * M * M;
-  for (int p0 = 0; p0 < M / 2; p0 += conv3_seq<M>()) {
-    const int np = min(conv3_seq<M>(), M / 2 - p0);
+  for (int p0 = 0; p0 < M / 2; p0 += S) {
+    const int np = min(S, M / 2 - p0);
     fft_batch<M, true>(
         scr, np, tws,
         [&](int p, int q) {
@@ -224,28 +227,54 @@ __global__ void __launch_bounds__(kConv3Threads) conv3_planes_inv_kernel(Conv3Ar
 
 inline bool conv3_supported(int M) { return M == 32 || M == 64 || M == 128; }
 
+// wide plane passes for 128-point planes: 512 threads, 32 sequences per
+// round (rows in 2 rounds instead of 4, columns in 2 instead of 3; 204 KB of
+// shared memory, one CTA per SM) -- the plane passes are latency-bound
+// rounds of FFTs, and a sharded rank or a single vector has few planes
+inline bool conv3_wide() {
+  static const bool on = [] {
+    const char* e = std::getenv("FGS_CONV3_WIDE");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 template <int M>
 void conv3_launch_t(const Conv3Args& a, int stage, int apply_mult, int inverse_only, cudaStream_t s) {
   const int H = a.N / 2 + 1, L = conv3_nw(M, a.N) * H;
+  constexpr bool kWide = M == 128;
+  constexpr int SW = kWide ? 32 : conv3_seq<M>(), NW_ = kWide ? 512 : kConv3Threads;
   static const bool init = [] {
-    const size_t ps = 200 * 1024;
+    const int ps = 227 * 1024;
     FGS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(conv3_planes_fwd_kernel<M>),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ps)));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, ps));
     FGS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(conv3_planes_inv_kernel<M>),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ps)));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, ps));
+    FGS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(conv3_planes_fwd_kernel<M, SW, NW_>),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, ps));
+    FGS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(conv3_planes_inv_kernel<M, SW, NW_>),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, ps));
     FGS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(conv3_lines_kernel<M>),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ps)));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, ps));
     return true;
   }();
   (void)init;
   const dim3 block(kConv3Threads);
-  if (stage == 0)
-    launch_ex(conv3_planes_fwd_kernel<M>, dim3(a.planes * a.nvec), block, conv3_plane_smem(M, a.N), s, a);
-  else if (stage == 1)
+  const bool wide = kWide && conv3_wide();
+  if (stage == 1) {
     launch_ex(conv3_lines_kernel<M>, dim3(((L + kConv3Lines - 1) / kConv3Lines) * a.nvec), block, conv3_line_smem(M), s,
               a, apply_mult, inverse_only);
-  else
+  } else if (wide) {
+    const size_t sm = conv3_plane_smem(M, a.N, SW);
+    if (stage == 0)
+      launch_ex(conv3_planes_fwd_kernel<M, SW, NW_>, dim3(a.planes * a.nvec), dim3(NW_), sm, s, a);
+    else
+      launch_ex(conv3_planes_inv_kernel<M, SW, NW_>, dim3(a.planes * a.nvec), dim3(NW_), sm, s, a);
+  } else if (stage == 0) {
+    launch_ex(conv3_planes_fwd_kernel<M>, dim3(a.planes * a.nvec), block, conv3_plane_smem(M, a.N), s, a);
+  } else {
     launch_ex(conv3_planes_inv_kernel<M>, dim3(a.planes * a.nvec), block, conv3_plane_smem(M, a.N), s, a);
+  }
 }
 
 // stage 0: planes_fwd, 1: lines, 2: planes_inv
