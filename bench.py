@@ -555,10 +555,11 @@ def run_b200(args, rank, world, local_rank):
     t_hbm = b / (peaks["hbm_gbs"] * 1e9)
     t_fp = f / (fp64_tf * 1e12)
     if t_fp >= t_hbm:
-        roof = {"bound": "fp64", "achieved": f / t / 1e12, "peak": fp64_tf, "unit": "TFLOP/s",
-                "frac": (f / t / 1e12) / fp64_tf, "traffic": None,
+        roof = {"bound": "tensor", "achieved": f / t / 1e12, "peak": fp64_tf, "unit": "TFLOP/s",
+                "frac": (f / t / 1e12) / fp64_tf, "traffic": None, "pipe": "fp64 tensor cores (DMMA m8n8k4)",
                 "peak_source": "fp64 microbenchmarks on this B200 before the run: max(DFMA, DMMA m8n8k4), best of 3 "
-                               "(MEASURED_PEAKS.json has no fp64 entry)"}
+                               "(MEASURED_PEAKS.json has no fp64 entry; its bf16 figure does not apply to an fp64 "
+                               "kernel)"}
     else:
         roof = {"bound": "hbm", "achieved": b / t / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": (b / t / 1e9) / peaks["hbm_gbs"], "traffic": None,
