@@ -182,7 +182,18 @@ void set_smem(const void* func, size_t smem) {
 
 // the tensor-core spread needs runs of >= this many points (K-steps of 4,
 // one block flush per run); sparser plans use the scalar register-blocked one
-constexpr double kDenseRun = 12.0;
+// d = 3, 2m = 16: 4 -- the slot-layout tensor kernels beat the scalar spread from
+// ~4 points per run (config 5 at 1.25M points, ~9 per run: 471 -> 700
+// matvecs/s); other 2m keep 12.  FGS_DENSE_RUN overrides (tuning).
+double dense_run_threshold(int T, int d) {
+  static const double forced = [] {
+    const char* e = std::getenv("FGS_DENSE_RUN");
+    return e ? std::atof(e) : -1.0;
+  }();
+  if (forced >= 0.0) return forced;
+  return T == 16 && d == 3 ? 4.0 : 12.0;
+}
+#define kDenseRun (dense_run_threshold(T, d))
 
 template <int D, int T>
 constexpr bool has_v4_3d() {
