@@ -134,7 +134,6 @@ struct PassArgs {
   double* inv_sqrt;
   unsigned long long* bad_flag;  // EPI_DEGREE: min caller index with d <= 0
   const int* caller;   // internal -> caller index of this shard's slice (always set)
-  int defer_epilogue;  // v4 interp, one warp per footprint: epilogue per staged chunk (large plans)
   const int* slots;    // v6 kernels: slot -> local internal point (-1: pad); items / runs in slots
   const int* boff;     // v6 interp: packed footprint offset of each 8-slot batch's run
   const double* xs;    // v6 spread: the vectors gathered into slot order (pads 0, s applied)

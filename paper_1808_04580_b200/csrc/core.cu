@@ -207,12 +207,8 @@ constexpr bool has_v4_2d() {
 // d = 2 tensor-core kernels: point-stream warps per CTA (interpolation 2:
 // C2 22.8 k vs 22.2 k with 4, 21.7 k with 1; spread 1)
 constexpr int kInterp2dP = 2;
-// d = 3 interpolation: per-warp point batches with B fragments from the box
-// (kernels_v5.cuh); FGS_INTERP_V5=0 builds the v4 register-resident kernel
-#ifndef FGS_INTERP_V5
-#define FGS_INTERP_V5 1
-#endif
-constexpr bool kInterpV5 = FGS_INTERP_V5 != 0;
+// d = 3 interpolation over the point order (plans without the slot layout):
+// per-warp point batches with B fragments from the box (kernels_v5.cuh)
 // d = 3 spread, 2m in {12, 16}: warps own box rows x0 = w (mod W), no
 // barrier per run (kernels_v5.cuh); FGS_SPREAD_V5=0 builds the v4 kernel
 #ifndef FGS_SPREAD_V5
@@ -283,7 +279,7 @@ LaunchShape shape_t(bool dense) {
   size_t interp = base + 2 * static_cast<size_t>(B::NT / 32) * B::QB;
   size_t spread = base;
   if constexpr (has_v4_3d<D, T>()) {
-    interp = kInterpV5 ? v5_extra_doubles<T>() : v4_stage_doubles<T, true>();
+    interp = v5_extra_doubles<T>();
     if (dense) {
       if constexpr (use_spread_v5<T>())
         spread = v5s_extra_doubles<T, v5s_w<T>()>();
@@ -346,15 +342,7 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
     }
   }
   if constexpr (has_v4_3d<D, T>()) {
-    if (interp && kInterpV5)
-      return launch_smem(interp_v5_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
-    if (interp) {
-      // one warp per footprint: partials combined per chunk only on large
-      // plans (C3 +7 %, C1 -5 %); G > 1 always combines per chunk
-      if (a.defer_epilogue)
-        return launch_smem(interp_v4_kernel<T, 0, 0, true>, nitems, Blk4<T, true>::NT, smem, s, a, box_stride);
-      return launch_smem(interp_v4_kernel<T, 0, 0>, nitems, Blk4<T, true>::NT, smem, s, a, box_stride);
-    }
+    if (interp) return launch_smem(interp_v5_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
     if (dense) {
       if constexpr (use_spread_v5<T>()) {
         constexpr int W = v5s_w<T>();
@@ -1172,7 +1160,7 @@ size_t Core::smem_bytes(bool interp) const {
   const bool dense = mean_run >= kDenseRun;
   const LaunchShape sh = d == 3 ? shape_of<3>(T, dense) : (d == 2 ? shape_of<2>(T, dense) : shape_of<1>(T, dense));
   size_t boxes = static_cast<size_t>(box_stride);
-  if (interp && d == 3 && kInterpV5 && (T == 8 || T == 12 || T == 16)) boxes = static_cast<size_t>(box_pad);
+  if (interp && d == 3 && (T == 8 || T == 12 || T == 16)) boxes = static_cast<size_t>(box_pad);
   if (use_slots && interp)
     return (boxes + (T == 16 ? v6i_extra_doubles<16>() : v6i_extra_doubles<12>())) * sizeof(double);
   if (use_slots && !interp && T == 16) return (boxes + v6s_extra_doubles()) * sizeof(double);
@@ -1473,7 +1461,6 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
   a.inv_sqrt = inv_sqrt.p;
   a.bad_flag = flag.p;
   a.caller = perm.p + offset;
-  a.defer_epilogue = n_local >= 100000 ? 1 : 0;
 
   // stage events persist across the two phases of a shard-group apply
   std::vector<cudaEvent_t>& evs = prof_evs_;

@@ -1,5 +1,7 @@
-// kernels_v4.cuh -- fp64 tensor-core (DMMA, mma.sync.m8n8k4.f64) spread and
-// interpolation for d = 3, 2m in {8, 12, 16}: the dense-cell fast path.
+// kernels_v4.cuh -- fp64 tensor-core (DMMA, mma.sync.m8n8k4.f64) spread for
+// d = 3, 2m in {8, 12} (dense cells; 2m = 16 takes kernels_v6.cuh) and the
+// d = 2 spread / interpolation.  The d = 3 interpolation moved to
+// kernels_v5.cuh / kernels_v6.cuh; the pair algebra below is shared.
 //
 // Per run (points sharing one footprint) both passes are small GEMMs over the
 // footprint's (a, c) "pairs":
@@ -81,219 +83,6 @@ __device__ __forceinline__ void v4_issue_chunk(double* buf, const double* taps, 
   for (int k = tid; k < n16; k += nt) {
     const int pt = k / H, r = k - pt * H;
     cp_async16(buf + pt * STRIDE + 2 * r, src + 2 * k);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// interpolation.  smem: box | stage[2][QS*STRIDE] | red[2][QS][G] | x, s, index [2][QS]
-// ---------------------------------------------------------------------------
-// DEFER: combine per-point results once per staged chunk (always when G > 1
-// warps share a point; for G = 1 chosen by plan size, see Core)
-template <int T, int PS, int QSZ, bool DEFER = (Blk4<T, true, PS, QSZ>::G > 1)>
-// 2m = 12: keep 4 CTAs (16 warps) per SM resident (<= 128 registers)
-#ifndef FGS_INTERP12_MINB
-#define FGS_INTERP12_MINB 4
-#endif
-__global__ void __launch_bounds__(Blk4<T, true, PS, QSZ>::NT,
-                                  (T == 12 && Blk4<T, true, PS, QSZ>::NT <= 192) ? FGS_INTERP12_MINB : 1)
-    interp_v4_kernel(PassArgs a, int box_stride_smem) {
-  pdl_wait();
-  using B = Blk4<T, true, PS, QSZ>;
-  constexpr int NT = B::NT, QS = B::QS, TAPS = B::TAPS, G = B::G, P = B::P, SR = B::STRIDE;
-  constexpr int TAW = B::TAW, TC = B::TC, TW = B::TW, KS = B::KS;
-  extern __shared__ __align__(16) double smem[];
-  double* S = smem;
-  double* stg = smem + box_stride_smem;
-  // per staged chunk (double-buffered): partial sums of the G warps per
-  // point and the epilogue operands, reduced after the next chunk barrier
-  double* red = stg + 2 * QS * SR;        // [2][QS][G]
-  double* ex = red + 2 * QS * G;           // [2][QS] x
-  double* es = ex + 2 * QS;                // [2][QS] s
-  long long* eix = reinterpret_cast<long long*>(es + 2 * QS);  // [2][QS] caller index
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int grp = warp / G, wg = warp % G;
-  const int q = lane & 3, r8 = lane >> 2;
-  const int ta0 = wg * TAW;  // first a-tile of this warp
-  // G > 1 warps share a point: their partials are always combined per chunk;
-  // G = 1: deferred only on large plans (measured: C3 +7 %, C1 -5 %)
-  constexpr bool defer = DEFER || G > 1;
-  const DItem it = a.items[blockIdx.x];
-  const int bx1 = it.e1, bx2 = it.e2;
-  const int V = it.e0 * it.e1 * it.e2;
-  const int M = a.M;
-  // point indices: 32-bit for 2m = 16 (C5 interp 73.6 -> 71.9 ms per block;
-  // for 2m = 8 / 12 the 64-bit form schedules better: C3 73 vs 84 us, C4
-  // 427 vs 438 us)
-  using PI = std::conditional_t<T == 16, int, int64_t>;
-  const PI p_begin = it.p_begin, p_end = it.p_end;
-  const int nch = static_cast<int>((p_end - p_begin + QS - 1) / QS);
-
-  for (int vec = 0; vec < a.nvec; ++vec) {
-    const double* gv = a.grid + vec * a.grid_stride;
-    const double* xv = a.x ? a.x + vec * a.ldx : nullptr;
-    double* yv = a.y ? a.y + vec * a.ldy : nullptr;
-    v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
-    cp_async_commit();
-    for (int v = tid; v < V; v += NT) {
-      const int x2 = v % bx2, x1 = (v / bx2) % bx1, x0 = v / (bx2 * bx1);
-      S[v] = gv[(static_cast<int64_t>((it.a0 + x0) % M) * M + (it.a1 + x1) % M) * M + (it.a2 + x2) % M];
-    }
-    int r = it.run_begin;
-    DRun run = a.runs[r];
-    int loaded = -1;
-    double gB[TW][KS];  // B fragments of the run's grid block: g[pair(lane/4)][4 ks + lane%4]
-
-    // y of chunk kk's points: the G partials in warp order, then the epilogue
-    auto finish_chunk = [&](int kk) {
-      const PI f0 = p_begin + static_cast<PI>(kk) * QS;
-      const int cnt = static_cast<int>(pmin<PI>(QS, p_end - f0));
-      const int fb = kk & 1;
-      for (int pt = tid; pt < cnt; pt += NT) {
-        double val = red[(fb * QS + pt) * G];
-#pragma unroll
-        for (int w2 = 1; w2 < G; ++w2) val += red[(fb * QS + pt) * G + w2];
-        const PI ipt = f0 + pt;
-        if (a.epilogue == EPI_DEGREE) {
-          const double dg = val - a.k0;  // graphop.cpp:55-56
-          a.degrees[ipt] = dg;
-          a.inv_sqrt[ipt] = 1.0 / sqrt(dg);
-          if (!(dg > 0.0)) atomicMin(a.bad_flag, static_cast<unsigned long long>(a.caller[ipt]));
-        } else {
-          const double xin = ex[fb * QS + pt], sin_ = es[fb * QS + pt];
-          double out;
-          switch (a.epilogue) {
-            case EPI_KERNEL: out = val; break;
-            case EPI_WEIGHT: out = val - a.k0 * xin; break;
-            case EPI_NORMALIZED: out = sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
-            default: out = xin - sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
-          }
-          yv[eix[fb * QS + pt]] = out;
-        }
-      }
-    };
-
-    for (int k = 0; k < nch; ++k) {
-      const PI c0 = p_begin + static_cast<PI>(k) * QS;
-      const PI c1 = pmin<PI>(c0 + QS, p_end);
-      const int buf = k & 1;
-      cp_async_wait_0();
-      __syncthreads();
-      if (defer && k > 0) finish_chunk(k - 1);
-      if (k + 1 < nch) {
-        v4_issue_chunk<TAPS, SR>(stg + (buf ^ 1) * QS * SR, a.taps, c1, static_cast<int>(lmin(QS, p_end - c1)), tid, NT);
-        cp_async_commit();
-      }
-      const double* sb = stg + buf * QS * SR;
-      for (PI b0 = c0 + 8 * grp; b0 < c1; b0 += 8 * P) {
-        const PI ipt = b0 + r8;  // this lane's point (C rows / A rows)
-        const bool in_chunk = ipt < c1;
-        const double* w = sb + (in_chunk ? (ipt - c0) : 0) * SR;
-        // epilogue operands prefetch (lanes q == 0 of warp 0 of the group)
-        double xin = 0.0, sin_ = 1.0;
-        PI ix = 0;
-        if (wg == 0 && q == 0 && in_chunk) {
-          ix = a.perm ? static_cast<PI>(a.perm[ipt]) : ipt;
-          if (xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE) xin = xv[ix];
-          if (a.epilogue == EPI_NORMALIZED || a.epilogue == EPI_LAPLACIAN) sin_ = a.s[ipt];
-        }
-        // this lane's a- and c-taps (compile-time register indices)
-        double wa[TAW], wc[TC][2];
-#pragma unroll
-        for (int t = 0; t < TAW; ++t) wa[t] = w[2 * (ta0 + t) + (q >> 1)];
-#pragma unroll
-        for (int t = 0; t < TC; ++t) {
-          wc[t][0] = w[T + 4 * t + 2 * (q & 1)];
-          wc[t][1] = w[T + 4 * t + 2 * (q & 1) + 1];
-        }
-        double yacc = 0.0;
-        while (true) {
-          while (static_cast<PI>(run.pstart) + run.pcount <= b0 && r + 1 < it.run_end) run = a.runs[++r];
-          if (loaded != r) {
-            const int o0 = run.off & 1023, o1 = (run.off >> 10) & 1023, o2 = (run.off >> 20) & 1023;
-#pragma unroll
-            for (int t = 0; t < TW; ++t) {
-              const int ta = ta0 + t / TC, tc = t % TC;
-              const int aa = 2 * ta + (r8 >> 2), cc = 4 * tc + (r8 & 3);
-              const double* row = S + ((o0 + aa) * bx1 + (o1 + cc)) * bx2 + o2 + q;
-#pragma unroll
-              for (int ks = 0; ks < KS; ++ks) gB[t][ks] = row[4 * ks];
-            }
-            loaded = r;
-          }
-          const PI rs = run.pstart, re_ = static_cast<PI>(run.pstart) + run.pcount;
-          const bool mine = in_chunk && ipt >= rs && ipt < re_;
-          double aF[KS];  // A fragments: we_{point}[4 ks + q], zero outside this run
-#pragma unroll
-          for (int ks = 0; ks < KS; ++ks) aF[ks] = mine ? w[2 * T + 4 * ks + q] : 0.0;
-          double K[TAW];
-#pragma unroll
-          for (int t = 0; t < TAW; ++t) K[t] = 0.0;
-          // tiles in groups of TG so TG independent accumulator chains interleave
-          constexpr int TG = TW % 4 == 0 ? 4 : (TW % 3 == 0 ? 3 : (TW % 2 == 0 ? 2 : 1));
-#pragma unroll
-          for (int t0 = 0; t0 < TW; t0 += TG) {
-            double z[TG][2];
-#pragma unroll
-            for (int u = 0; u < TG; ++u) z[u][0] = z[u][1] = 0.0;
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-              for (int u = 0; u < TG; ++u) dmma(z[u][0], z[u][1], aF[ks], gB[t0 + u][ks]);
-#pragma unroll
-            for (int u = 0; u < TG; ++u) {
-              const int ta = (t0 + u) / TC, tc = (t0 + u) % TC;
-              K[ta] = fma(wc[tc][0], z[u][0], K[ta]);
-              K[ta] = fma(wc[tc][1], z[u][1], K[ta]);
-            }
-          }
-#pragma unroll
-          for (int t = 0; t < TAW; ++t) yacc = fma(wa[t], K[t], yacc);
-          if (re_ < pmin<PI>(b0 + 8, c1) && r + 1 < it.run_end) {  // batch continues in the next run
-            run = a.runs[++r];
-            continue;
-          }
-          break;
-        }
-        // sum the 4 lanes of each point; the G warps' partials meet in
-        // shared memory (reduced in finish_chunk after the next barrier)
-        yacc += __shfl_xor_sync(0xffffffffu, yacc, 1);
-        yacc += __shfl_xor_sync(0xffffffffu, yacc, 2);
-        if (!defer) {  // one warp per footprint: the epilogue right here
-          if (q == 0 && in_chunk) {
-            const double val = yacc;
-            if (a.epilogue == EPI_DEGREE) {
-              const double dg = val - a.k0;  // graphop.cpp:55-56
-              a.degrees[ipt] = dg;
-              a.inv_sqrt[ipt] = 1.0 / sqrt(dg);
-              if (!(dg > 0.0)) atomicMin(a.bad_flag, static_cast<unsigned long long>(a.caller[ipt]));
-            } else {
-              double out;
-              switch (a.epilogue) {
-                case EPI_KERNEL: out = val; break;
-                case EPI_WEIGHT: out = val - a.k0 * xin; break;
-                case EPI_NORMALIZED: out = sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
-                default: out = xin - sin_ * (val - a.k0 * __dmul_rn(sin_, xin)); break;
-              }
-              yv[ix] = out;
-            }
-          }
-        } else if (q == 0 && in_chunk) {
-          const int pt = static_cast<int>(ipt - c0);
-          red[(buf * QS + pt) * G + wg] = yacc;
-          if (wg == 0) {
-            ex[buf * QS + pt] = xin;
-            es[buf * QS + pt] = sin_;
-            eix[buf * QS + pt] = ix;
-          }
-        }
-      }
-    }
-    cp_async_wait_0();
-    __syncthreads();
-    if (defer) {
-      if (nch > 0) finish_chunk(nch - 1);
-      __syncthreads();
-    }
   }
 }
 
