@@ -136,6 +136,7 @@ struct PassArgs {
   const int* caller;   // internal -> caller index of this shard's slice (always set)
   const int* slots;    // v6 kernels: slot -> local internal point (-1: pad); items / runs in slots
   const int* boff;     // v6 interp: packed footprint offset of each 8-slot batch's run
+  int pair_batches;    // slot layout, 2m = 16: runs long enough for interp_v7's batch pairs
   const double* xs;    // v6 spread: the vectors gathered into slot order (pads 0, s applied)
   int64_t ldxs;
 };

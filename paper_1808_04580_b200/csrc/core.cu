@@ -333,8 +333,11 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
       if (interp) {
         // two batches per B load: 2m = 16 (C5 interp 48.8 -> 47.8 ms); 2m = 12
         // loses with it (C4 314 -> 332 us: fewer K-steps per B fragment)
+        // (from 16 points per run: sparser plans rarely pair two batches of
+        // one run, and v6 is 2 % faster there -- config 5 at 1.25M points)
         if constexpr (T == 16)
-          if (interp_v7_on()) return launch_smem(interp_v7_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+          if (interp_v7_on() && a.pair_batches)
+            return launch_smem(interp_v7_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
         return launch_smem(interp_v6_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
       }
       if constexpr (T == 16) return launch_smem(spread_v6_kernel, nitems, Blk6s::NT, smem, s, a, box_stride);
@@ -1418,6 +1421,7 @@ void Core::pass_layout(PassArgs& a) const {
     a.runs = runs6.p;
     a.slots = slot_map.p;
     a.boff = batch_off.p;
+    a.pair_batches = mean_run >= 16.0 ? 1 : 0;
   } else {
     a.items = items.p;
     a.runs = runs.p;
