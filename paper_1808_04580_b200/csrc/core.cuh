@@ -178,6 +178,10 @@ class Core {
   DBuf<double> lz_vecs, lz_vc, lz_S, lz_pval, lz_psigned;
   DBuf<int64_t> lz_pidx;
   DBuf<int> lz_order;                        // last-block reduction tickets (reset by their kernels)
+  // start vector drawn on the device: mt19937_64 seed state, caller-order
+  // uniforms, sum-of-squares partials
+  DBuf<unsigned long long> lz_mt;
+  DBuf<double> lz_start, lz_sq;
 
   void set_stream(cudaStream_t s);
   Workspace& workspace(int nvec);

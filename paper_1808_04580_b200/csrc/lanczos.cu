@@ -497,6 +497,88 @@ __global__ void ritz_kernel(const double* __restrict__ Q, int64_t ldq, int m, co
     if (c0 + i < k) V[static_cast<int64_t>(c0 + i) * ldv + r] = acc[i];
 }
 
+// ---- start vector on the device (spectral.cpp:152-156) ---------------------
+// std::mt19937_64 as a sequence: w[0..312) is the seeded state, and every
+// later word is w[k + 312] = w[k + 156] ^ twist(w[k], w[k + 1]); output j is
+// temper(w[312 + j]).  The 156 words of one round depend only on earlier
+// rounds, so one CTA produces them in parallel per round from a ring of 1024
+// words (a round reads [k, k + 312) and writes [k + 312, k + 468)).
+constexpr int kMtN = 312, kMtM = 156;
+
+__device__ __forceinline__ unsigned long long mt_next(unsigned long long a, unsigned long long b,
+                                                      unsigned long long c) {
+  const unsigned long long y = (a & 0xFFFFFFFF80000000ull) | (b & 0x7FFFFFFFull);
+  return c ^ (y >> 1) ^ ((y & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
+}
+
+__device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
+  y ^= (y >> 29) & 0x5555555555555555ull;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  return y ^ (y >> 43);
+}
+
+// uniform_real_distribution<double>(-1, 1) over libstdc++'s
+// generate_canonical<double, 53>: one 64-bit draw, (double) r / 2^64 clamped
+// below 1, then u * (b - a) + a
+__device__ __forceinline__ double mt_uniform(unsigned long long r) {
+  double u = __dmul_rn(__ull2double_rn(r), 0x1p-64);
+  if (u >= 1.0) u = 0x1.fffffffffffffp-1;
+  return __dadd_rn(__dmul_rn(u, 2.0), -1.0);
+}
+
+__global__ void __launch_bounds__(kMtM) mt_uniform_kernel(const unsigned long long* __restrict__ seeded, int64_t n,
+                                                          double* __restrict__ out) {
+  __shared__ unsigned long long ring[1024];
+  for (int i = threadIdx.x; i < kMtN; i += blockDim.x) ring[i] = seeded[i];
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += kMtM) {
+    const int64_t k = base + threadIdx.x;
+    const unsigned long long w = mt_next(ring[k & 1023], ring[(k + 1) & 1023], ring[(k + kMtM) & 1023]);
+    ring[(k + kMtN) & 1023] = w;
+    if (k < n) out[k] = mt_uniform(mt_temper(w));
+    __syncthreads();
+  }
+}
+
+constexpr int kSqBlocks = 256, kSqThreads = 256;
+
+// fixed-order sum of squares: block b's rows, then a block tree
+__global__ void __launch_bounds__(kSqThreads) sumsq_partial_kernel(const double* __restrict__ v, int64_t n,
+                                                                   double* __restrict__ partial) {
+  __shared__ double red[kSqThreads];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = lo + per < n ? lo + per : n;
+  double acc = 0.0;
+  for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) acc = fma(v[r], v[r], acc);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kSqThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// basis[:, 0][p] = start[perm[offset + p]] / |start| (every block sums the
+// partials in the same order)
+__global__ void __launch_bounds__(kSqThreads) start_scatter_kernel(const double* __restrict__ start,
+                                                                   const double* __restrict__ partial,
+                                                                   const int* __restrict__ perm, int64_t offset,
+                                                                   int64_t nl, double* __restrict__ q) {
+  __shared__ double red[kSqBlocks];
+  for (int i = threadIdx.x; i < kSqBlocks; i += blockDim.x) red[i] = partial[i];
+  __syncthreads();
+  for (int s = kSqBlocks / 2; s > 0; s >>= 1) {
+    for (int i = threadIdx.x; i < s; i += blockDim.x) red[i] += red[i + s];
+    __syncthreads();
+  }
+  const double sn = sqrt(red[0]);
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nl;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    q[p] = start[perm[offset + p]] / sn;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -579,16 +661,25 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
   const auto entry = std::chrono::steady_clock::now();
 
   // start vector: mt19937_64(seed) uniform(-1, 1) over the caller order,
-  // normalised (spectral.cpp:152-156); moved to the internal order
+  // normalised (spectral.cpp:152-156), drawn on the device (the host draw +
+  // permutation cost 27 ms of a 137 ms C4 solve); the host generator is
+  // advanced past those n draws only if a breakdown restart needs it
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> unif(-1.0, 1.0);
-  std::vector<double> start(static_cast<size_t>(n));
-  for (int64_t i = 0; i < n; ++i) start[static_cast<size_t>(i)] = unif(rng);
-  double sn = 0.0;
-  for (double v : start) sn += v * v;
-  sn = std::sqrt(sn);
-  std::vector<double> local(static_cast<size_t>(std::max<int64_t>(nl, 1)));
-  for (int64_t p = 0; p < nl; ++p) local[static_cast<size_t>(p)] = start[static_cast<size_t>(c.host_perm[static_cast<size_t>(c.offset + p)])] / sn;
+  bool rng_at_restart = false;
+  std::vector<double> local;
+  {
+    unsigned long long seeded[kMtN];
+    seeded[0] = seed;
+    for (int i = 1; i < kMtN; ++i)  // the standard's seeding (mersenne_twister_engine::seed)
+      seeded[i] = 6364136223846793005ull * (seeded[i - 1] ^ (seeded[i - 1] >> 62)) + static_cast<unsigned long long>(i);
+    c.lz_mt.upload(seeded, kMtN, st);
+    c.lz_start.alloc(static_cast<size_t>(n));
+    c.lz_sq.alloc(kSqBlocks);
+    mt_uniform_kernel<<<1, kMtM, 0, st>>>(c.lz_mt.p, n, c.lz_start.p);
+    sumsq_partial_kernel<<<kSqBlocks, kSqThreads, 0, st>>>(c.lz_start.p, n, c.lz_sq.p);
+    c.launches += 2;
+  }
 
   // initial basis width: the reference grows from 64 columns geometrically
   // (conservativeResize); k-dependent pre-sizing (4k + 8, C4's k = 20
@@ -626,7 +717,9 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
     }
   }
   scal.alloc(4);
-  FGS_CUDA(cudaMemcpyAsync(basis.p, local.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, st));
+  start_scatter_kernel<<<std::max(1, std::min(ceil_div(std::max<int64_t>(nl, 1), kSqThreads), 1184)), kSqThreads, 0,
+                         st>>>(c.lz_start.p, c.lz_sq.p, c.perm.p, c.offset, nl, basis.p);
+  ++c.launches;
 
   auto allreduce = [&](double* v, int count) {
     if (c.sharded)
@@ -895,6 +988,11 @@ LanczosResult lanczos_device(Core& c, int which, int k, int max_iter, double tol
       // breakdown: fresh random direction orthogonal to the basis
       // (spectral.cpp:59-75, 225-238), same RNG stream as the start vector
       qin_holds = 0;  // the host forms q_{m+1}
+      if (!rng_at_restart) {  // the start vector's n draws happened on the device
+        rng.discard(static_cast<unsigned long long>(n));
+        local.resize(static_cast<size_t>(std::max<int64_t>(nl, 1)));
+        rng_at_restart = true;
+      }
       bool found = false;
       for (int attempt = 0; attempt < 8 && !found; ++attempt) {
         std::vector<double> v(static_cast<size_t>(n));

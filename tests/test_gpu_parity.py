@@ -240,6 +240,24 @@ def test_lanczos_matches_oracle_on_config1(orc):
     assert np.array_equal(lap.vectors[:, 0], pairs.vectors[:, -1])
 
 
+@pytest.mark.parametrize("n,seed", [(155, 1), (157, 7), (20000, 1), (20000, 12345678901234)])
+def test_lanczos_start_vector_drawn_on_device(orc, n, seed):
+    # one step, one pair: the Ritz vector is the normalised start vector
+    # (spectral.cpp:152-156: mt19937_64(seed), uniform(-1, 1)), which the
+    # device draws itself -- it must be the reference's draw sequence
+    X, info, params = _config_case(1, n)
+    op = fgs.AdjacencyOperator(X, fgs.KernelSpec.gaussian(info["sigma"]), params)
+    ref = orc.AdjacencyOperator(X, 0, info["sigma"], N=info["N"], m=info["m"], p=info["p"])
+    li = fgs.LanczosInfo()
+    pairs = fgs.lanczos_largest(op, 1, fgs.LanczosOptions(max_iter=1, tol=1e-8, seed=seed), li)
+    rv, rV, rit, _ = ref.lanczos_largest(1, max_iter=1, tol=1e-8, seed=seed)
+    assert li.iterations == rit == 1
+    # same draws; the norm is summed in another order (a tree on the device,
+    # the reference's serial loop: ~sqrt(n) ulps apart)
+    assert np.max(np.abs(pairs.vectors[:, 0] - rV[:, 0])) <= 1e-14 * np.max(np.abs(rV[:, 0]))
+    assert abs(pairs.values[0] - rv[0]) <= 1e-12 * abs(rv[0])
+
+
 def test_lanczos_laplacian_handle_and_reproducibility(orc):
     X, info, params = _config_case(2, 20000)
     op = fgs.AdjacencyOperator(X, fgs.KernelSpec.gaussian(info["sigma"]), params)
