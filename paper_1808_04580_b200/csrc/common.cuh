@@ -139,6 +139,33 @@ struct PassArgs {
   int pair_batches;    // slot layout, 2m = 16: runs long enough for interp_v7's batch pairs
   const double* xs;    // v6 spread: the vectors gathered into slot order (pads 0, s applied)
   int64_t ldxs;
+  int vsplit;          // slot-layout kernels: CTAs per item, each a share of the block's vectors (0/1: one)
 };
+
+// Vector split of the slot-layout kernels.  A block of nvec vectors re-reads
+// every item's taps once per vector; with `vsplit` CTAs per item (consecutive
+// block indices, so they are resident at the same time) each CTA takes a
+// share of the vectors and the CTAs of one item stream the same taps rows
+// within microseconds of one another: all but the first read hit L2 instead
+// of HBM.  Narrows `a` to this CTA's vectors; returns (item, number of items).
+struct ItemOfBlock {
+  int item, nitems;
+};
+__device__ __forceinline__ ItemOfBlock vsplit_narrow(PassArgs& a) {
+  const int vs = a.vsplit > 1 ? a.vsplit : 1;
+  ItemOfBlock r{static_cast<int>(blockIdx.x) / vs, static_cast<int>(gridDim.x) / vs};
+  if (vs > 1) {
+    const int part = static_cast<int>(blockIdx.x) - r.item * vs;
+    const int vper = (a.nvec + vs - 1) / vs;
+    const int v0 = min(part * vper, a.nvec), v1 = min(v0 + vper, a.nvec);
+    if (a.x) a.x += v0 * a.ldx;
+    if (a.xs) a.xs += v0 * a.ldxs;
+    if (a.y) a.y += v0 * a.ldy;
+    if (a.grid) a.grid += v0 * a.grid_stride;
+    if (a.priv) a.priv += static_cast<int64_t>(v0) * r.nitems * a.box_stride;
+    a.nvec = v1 - v0;
+  }
+  return r;
+}
 
 }  // namespace fgsb

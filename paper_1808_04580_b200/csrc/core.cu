@@ -18,6 +18,7 @@
 #include "kernels_v2.cuh"
 #include "kernels_v4.cuh"
 #include "kernels_v6.cuh"
+#include "kernels_v8.cuh"
 #include "conv2d.cuh"
 #include "conv3d.cuh"
 #include "direct.cuh"
@@ -226,6 +227,7 @@ constexpr int v5s_w() {
   return T == 16 ? FGS_V5S_W16 : T / 2;
 }
 constexpr int kSpread2dP = 1;
+constexpr int kVSplitDefault = 16;  // one vector per CTA: C5 taps traffic 68.7 -> ~8 GB per block (L2 hits), 98.8 -> 97.9 ms
 // d = 3, 2m = 16 dense plans: run-aligned slot layout + kernels_v6.cuh
 // (FGS_V6=0: the v5 kernels over the plain point order)
 // slot-layout interpolation with two batches per B-fragment load
@@ -236,6 +238,23 @@ bool interp_v7_on() {
     return !(e && std::string(e) == "0");
   }();
   return on;
+}
+bool spread_v8_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("FGS_SPREAD_V8");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+// slot-layout kernels: CTAs per item of a vector block (vsplit_narrow,
+// common.cuh); FGS_VSPLIT overrides (tuning)
+int vsplit_for(int nvec) {
+  static const int forced = [] {
+    const char* e = std::getenv("FGS_VSPLIT");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int vs = forced > 0 ? forced : kVSplitDefault;
+  return std::max(1, std::min(vs, nvec));
 }
 bool v6_enabled() {
   static const bool on = [] {
@@ -341,7 +360,9 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
         return launch_smem(interp_v6_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
       }
       if constexpr (T == 16) return launch_smem(spread_v6_kernel, nitems, Blk6s::NT, smem, s, a, box_stride);
-      // 2m = 12: the v4 spread below reads the slot rows (stride 3 2m) and the slot-ordered x
+      // 2m = 12: e split 8 (DMMA) + 4 (DFMA), warps own box c-rows (kernels_v8.cuh);
+      // FGS_SPREAD_V8=0: the v4 spread below reads the slot rows (stride 3 2m) and the slot-ordered x
+      if (spread_v8_on()) return launch_smem(spread_v8_kernel<Blk8::H>, nitems, Blk8::NT, smem, s, a, box_stride);
     }
   }
   if constexpr (has_v4_3d<D, T>()) {
@@ -1167,6 +1188,7 @@ size_t Core::smem_bytes(bool interp) const {
   if (use_slots && interp)
     return (boxes + (T == 16 ? v6i_extra_doubles<16>() : v6i_extra_doubles<12>())) * sizeof(double);
   if (use_slots && !interp && T == 16) return (boxes + v6s_extra_doubles()) * sizeof(double);
+  if (use_slots && !interp && T == 12 && spread_v8_on()) return (boxes + v8s_extra_doubles()) * sizeof(double);
   if (d == 3 && !interp && dense) boxes *= static_cast<size_t>(v4_spread_groups(T));  // per-group boxes
   if (d == 2 && !interp && dense && (T == 8 || T == 12 || T == 16))
     boxes *= static_cast<size_t>(kSpread2dP);  // per-stream boxes
@@ -1186,6 +1208,14 @@ void Core::launch_spread(const PassArgs& a) {
   if (smem > 227 * 1024) fail(FGS_ERESOURCE, "tile box exceeds shared memory (cutoff too large for d = 3)");
   const bool dense = mean_run >= kDenseRun;
   const int bs = static_cast<int>(box_stride), bp = static_cast<int>(box_pad);
+  if (use_slots && (T == 16 || spread_v8_on()) && a.nvec > 1) {  // spread_v6 / spread_v8: vector split
+    PassArgs b = a;
+    b.vsplit = vsplit_for(a.nvec);
+    dispatch<3>(false, dense, T, b, nitems * b.vsplit, smem, bs, bp, stream);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+    return;
+  }
   if (d == 3) dispatch<3>(false, dense, T, a, nitems, smem, bs, bp, stream);
   if (d == 2) dispatch<2>(false, dense, T, a, nitems, smem, bs, bp, stream);
   if (d == 1) dispatch<1>(false, dense, T, a, nitems, smem, bs, bp, stream);
@@ -1198,6 +1228,14 @@ void Core::launch_interp(const PassArgs& a) {
   const size_t smem = smem_bytes(true);
   if (smem > 227 * 1024) fail(FGS_ERESOURCE, "tile box exceeds shared memory (cutoff too large for d = 3)");
   const int bs = static_cast<int>(box_stride), bp = static_cast<int>(box_pad);
+  if (use_slots && a.nvec > 1) {  // interp_v6 / interp_v7: vector split
+    PassArgs b = a;
+    b.vsplit = vsplit_for(a.nvec);
+    dispatch<3>(true, true, T, b, nitems * b.vsplit, smem, bs, bp, stream);
+    ++launches;
+    FGS_CUDA(cudaGetLastError());
+    return;
+  }
   if (d == 3) dispatch<3>(true, true, T, a, nitems, smem, bs, bp, stream);
   if (d == 2) dispatch<2>(true, true, T, a, nitems, smem, bs, bp, stream);
   if (d == 1) dispatch<1>(true, true, T, a, nitems, smem, bs, bp, stream);

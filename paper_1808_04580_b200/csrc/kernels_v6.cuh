@@ -100,8 +100,10 @@ __global__ void slot_gather_kernel(PassArgs a, int64_t nslots, double* out) {
   }
 }
 
-__global__ void __launch_bounds__(Blk6s::NT, Blk6s::MINB) spread_v6_kernel(PassArgs a, int box_stride_smem) {
+__global__ void __launch_bounds__(Blk6s::NT, Blk6s::MINB) spread_v6_kernel(PassArgs a_, int box_stride_smem) {
   pdl_wait();
+  PassArgs a = a_;
+  const ItemOfBlock ib = vsplit_narrow(a);
   using B = Blk6s;
   constexpr int T = B::T, NT = B::NT, QS = B::QS, SR = B::SR, NS = B::NS, W = B::W;
   extern __shared__ __align__(16) double smem[];
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(Blk6s::NT, Blk6s::MINB) spread_v6_kernel(PassA
   unsigned long long* empty = full + NS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = lane & 3, r8 = lane >> 2;
-  const DItem it = a.items[blockIdx.x];
+  const DItem it = a.items[ib.item];
   const int bx1 = it.e1, bx2 = it.e2;
   const int V = it.e0 * bx1 * bx2;
   const int s_begin = it.p_begin, s_end = it.p_end;  // slots, multiples of kSlotAlign
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(Blk6s::NT, Blk6s::MINB) spread_v6_kernel(PassA
       if (lane == 0) mbar_arrive(&empty[st]);
     }
     __syncthreads();  // every warp's flushes are in the box
-    double* out = a.priv + (static_cast<int64_t>(vec) * gridDim.x + blockIdx.x) * a.box_stride;
+    double* out = a.priv + (static_cast<int64_t>(vec) * ib.nitems + ib.item) * a.box_stride;
     for (int v = tid; v < V; v += NT) out[v] = S[v];
   }
 }
@@ -241,8 +243,10 @@ constexpr size_t v6i_extra_doubles() {
 }
 
 template <int T>
-__global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a, int box_doubles) {
+__global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a_, int box_doubles) {
   pdl_wait();
+  PassArgs a = a_;
+  const ItemOfBlock ib = vsplit_narrow(a);
   using B = Blk5<T>;
   constexpr int TA = B::TA, TC = B::TC, KS = B::KS, W = B::W, NT = B::NT, SR = B::STRIDE;
   static_assert(SR == slot_row<T>(), "staged row = global slot-ordered row");
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a, i
   double* slots = smem + box_doubles + static_cast<size_t>(warp) * 2 * B::SLOT;
   unsigned long long* mb =
       reinterpret_cast<unsigned long long*>(smem + box_doubles + static_cast<size_t>(W) * 2 * B::SLOT) + 2 * warp;
-  const DItem it = a.items[blockIdx.x];
+  const DItem it = a.items[ib.item];
   const int bx1 = it.e1, e2 = it.e2, sp2 = v5_pad(e2);
   const int rows = it.e0 * it.e1;
   const int M = a.M;
@@ -430,8 +434,10 @@ __device__ __forceinline__ void v7_compute(const V7Frag<T>* f, const double* gb,
 }
 
 template <int T>
-__global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v7_kernel(PassArgs a, int box_doubles) {
+__global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v7_kernel(PassArgs a_, int box_doubles) {
   pdl_wait();
+  PassArgs a = a_;
+  const ItemOfBlock ib = vsplit_narrow(a);
   using B = Blk5<T>;
   constexpr int W = B::W, NT = B::NT, SR = B::STRIDE;
   static_assert(SR == slot_row<T>(), "staged row = global slot-ordered row");
@@ -442,7 +448,7 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v7_kernel(PassArgs a, i
   double* buf = smem + box_doubles + static_cast<size_t>(warp) * 2 * B::SLOT;  // 16 slot rows
   unsigned long long* mb =
       reinterpret_cast<unsigned long long*>(smem + box_doubles + static_cast<size_t>(W) * 2 * B::SLOT) + warp;
-  const DItem it = a.items[blockIdx.x];
+  const DItem it = a.items[ib.item];
   const int bx1 = it.e1, e2 = it.e2, sp2 = v5_pad(e2);
   const int rows = it.e0 * it.e1;
   const int M = a.M;
