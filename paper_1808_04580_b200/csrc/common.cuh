@@ -139,6 +139,7 @@ struct PassArgs {
   int pair_batches;    // slot layout, 2m = 16: runs long enough for interp_v7's batch pairs
   const double* xs;    // v6 spread: the vectors gathered into slot order (pads 0, s applied)
   int64_t ldxs;
+  int box_ext;         // slot-layout interpolation: fixed box extent (tile B + 2m - 1), 0 = per-item strides
   int vsplit;          // slot-layout kernels: CTAs per item, each a share of the block's vectors (0/1: one)
 };
 

@@ -354,10 +354,20 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
         // loses with it (C4 314 -> 332 us: fewer K-steps per B fragment)
         // (from 16 points per run: sparser plans rarely pair two batches of
         // one run, and v6 is 2 % faster there -- config 5 at 1.25M points)
+        // fixed box strides for the plan's tile size (B = 2: 2m + 1, B = 4: 2m + 3)
         if constexpr (T == 16)
-          if (interp_v7_on() && a.pair_batches)
-            return launch_smem(interp_v7_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
-        return launch_smem(interp_v6_kernel<T>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+          if (interp_v7_on() && a.pair_batches) {
+            if (a.box_ext == T + 1)
+              return launch_smem(interp_v7_kernel<T, T + 1>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+            if (a.box_ext == T + 3)
+              return launch_smem(interp_v7_kernel<T, T + 3>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+            return launch_smem(interp_v7_kernel<T, 0>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+          }
+        if (a.box_ext == T + 1)
+          return launch_smem(interp_v6_kernel<T, T + 1>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+        if (a.box_ext == T + 3)
+          return launch_smem(interp_v6_kernel<T, T + 3>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
+        return launch_smem(interp_v6_kernel<T, 0>, nitems, Blk5<T>::NT, smem, s, a, box_pad_arg);
       }
       if constexpr (T == 16) return launch_smem(spread_v6_kernel, nitems, Blk6s::NT, smem, s, a, box_stride);
       // 2m = 12: e split 8 (DMMA) + 4 (DFMA), warps own box c-rows (kernels_v8.cuh);
@@ -1019,6 +1029,10 @@ void Core::build_plan(const double* nodes_colmajor) {
       }
     batch_off.upload(boff.data(), boff.size(), stream);
     use_slots = true;
+    // fixed box strides for the slot-layout interpolation (tile B in {2, 4}):
+    // every item's box laid out with the maximal extent B + 2m - 1
+    box_ext = (B == 2 || B == 4) && !std::getenv("FGS_BOX_EXT0") ? B + T - 1 : 0;
+    if (box_ext) box_pad = std::max<int64_t>(box_pad, static_cast<int64_t>(box_ext) * box_ext * v5_pad(box_ext));
   }
   items.upload(ditems.data(), ditems.size(), stream);
   if (druns.empty()) druns.push_back(DRun{0, 0, 0});
@@ -1460,6 +1474,7 @@ void Core::pass_layout(PassArgs& a) const {
     a.slots = slot_map.p;
     a.boff = batch_off.p;
     a.pair_batches = mean_run >= 16.0 ? 1 : 0;
+    a.box_ext = box_ext;
   } else {
     a.items = items.p;
     a.runs = runs.p;

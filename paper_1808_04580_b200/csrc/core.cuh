@@ -152,6 +152,7 @@ class Core {
   bool tensor_spread() const;  // the DMMA spread runs (dense runs, 2m in {8, 12, 16}, d in {2, 3})
   bool tensor_interp() const;
   int64_t box_stride = 0;
+  int box_ext = 0;      // slot layout: fixed interpolation box extent (tile B + 2m - 1), 0 = per-item
   int64_t box_pad = 0;  // largest item box with rows padded for the d = 3 interpolation (kernels_v5.cuh)
   int64_t grid_elems = 0, spec_elems = 0, window_elems = 0;
   std::vector<int> host_perm;

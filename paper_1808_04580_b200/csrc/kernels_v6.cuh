@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(Blk6s::NT, Blk6s::MINB) spread_v6_kernel(PassA
     __syncthreads();  // flushes of this vector may start as soon as a warp finishes its first run
     int r = it.run_begin;
     DRun run = a.runs[r];
+    DRun nxt = a.runs[min(r + 1, it.run_end - 1)];    // one run ahead: the load is off the flush path
     int cur = run.pstart;                             // K-step cursor (slots)
     int kend = run.pstart + ((run.pcount + 3) & ~3);  // the run's last K-step end
     int cw = (warp - ((run.off >> 10) & 1023)) & 7;   // this warp's first c in the run
@@ -216,7 +217,8 @@ __global__ void __launch_bounds__(Blk6s::NT, Blk6s::MINB) spread_v6_kernel(PassA
             done = true;
             break;
           }
-          run = a.runs[r];
+          run = nxt;
+          nxt = a.runs[min(r + 1, it.run_end - 1)];
           cur = run.pstart;
           kend = run.pstart + ((run.pcount + 3) & ~3);
           cw = (warp - ((run.off >> 10) & 1023)) & 7;
@@ -242,7 +244,11 @@ constexpr size_t v6i_extra_doubles() {
   return v5_extra_doubles<T>() + 2 * static_cast<size_t>(Blk5<T>::W);
 }
 
-template <int T>
+// EXT > 0: the box is laid out with the plan's maximal extent (tile B + 2m - 1)
+// in every item, so the B-fragment offsets ta ra + tc rc + 4 ks are immediates
+// (runtime strides cost ~2 IMADs per DMMA at 2m = 12, and a DMMA's issue slot
+// is the kernel's limit); EXT = 0: per-item strides.
+template <int T, int EXT>
 __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a_, int box_doubles) {
   pdl_wait();
   PassArgs a = a_;
@@ -258,8 +264,9 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a_, 
   unsigned long long* mb =
       reinterpret_cast<unsigned long long*>(smem + box_doubles + static_cast<size_t>(W) * 2 * B::SLOT) + 2 * warp;
   const DItem it = a.items[ib.item];
-  const int bx1 = it.e1, e2 = it.e2, sp2 = v5_pad(e2);
-  const int rows = it.e0 * it.e1;
+  const int e1 = it.e1, e2 = it.e2;
+  const int bx1 = EXT > 0 ? EXT : e1, sp2 = EXT > 0 ? v5_pad(EXT) : v5_pad(e2);  // box strides
+  const int rows = it.e0 * e1;
   const int M = a.M;
   const int s_begin = it.p_begin;
   const int nb = (it.p_end - s_begin) / 8;  // 8-slot batches of the item
@@ -284,11 +291,7 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v6_kernel(PassArgs a_, 
     double* yv = a.y ? a.y + vec * a.ldy : nullptr;
     if (warp < nb && lane == 0) issue(g, warp);
     if (vec > 0) __syncthreads();  // every warp is done with the previous vector's box
-    for (int v = tid; v < rows * e2; v += NT) {
-      const int row = v / e2, x2 = v - row * e2;
-      const int x0 = row / bx1, x1 = row - x0 * bx1;
-      S[row * sp2 + x2] = gv[(static_cast<int64_t>((it.a0 + x0) % M) * M + (it.a1 + x1) % M) * M + (it.a2 + x2) % M];
-    }
+    v5_load_box<NT>(S, gv, it, M, bx1, sp2, tid);
     __syncthreads();
 
     // per batch: its run's footprint offset (plan array, one per 8 slots) and
@@ -433,7 +436,7 @@ __device__ __forceinline__ void v7_compute(const V7Frag<T>* f, const double* gb,
   }
 }
 
-template <int T>
+template <int T, int EXT>
 __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v7_kernel(PassArgs a_, int box_doubles) {
   pdl_wait();
   PassArgs a = a_;
@@ -449,8 +452,9 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v7_kernel(PassArgs a_, 
   unsigned long long* mb =
       reinterpret_cast<unsigned long long*>(smem + box_doubles + static_cast<size_t>(W) * 2 * B::SLOT) + warp;
   const DItem it = a.items[ib.item];
-  const int bx1 = it.e1, e2 = it.e2, sp2 = v5_pad(e2);
-  const int rows = it.e0 * it.e1;
+  const int e1 = it.e1, e2 = it.e2;
+  const int bx1 = EXT > 0 ? EXT : e1, sp2 = EXT > 0 ? v5_pad(EXT) : v5_pad(e2);  // box strides
+  const int rows = it.e0 * e1;
   const int M = a.M;
   const int s_begin = it.p_begin;
   const int nb = (it.p_end - s_begin) / 8;  // 8-slot batches of the item
@@ -478,11 +482,7 @@ __global__ void __launch_bounds__(Blk5<T>::NT, 2) interp_v7_kernel(PassArgs a_, 
     const bool need_x = xv && a.epilogue != EPI_KERNEL && a.epilogue != EPI_DEGREE;
     if (warp < nu && lane == 0) issue(warp);
     if (vec > 0) __syncthreads();  // every warp is done with the previous vector's box
-    for (int v = tid; v < rows * e2; v += NT) {
-      const int row = v / e2, x2 = v - row * e2;
-      const int x0 = row / bx1, x1 = row - x0 * bx1;
-      S[row * sp2 + x2] = gv[(static_cast<int64_t>((it.a0 + x0) % M) * M + (it.a1 + x1) % M) * M + (it.a2 + x2) % M];
-    }
+    v5_load_box<NT>(S, gv, it, M, bx1, sp2, tid);
     __syncthreads();
 
     for (int u = warp; u < nu; u += W) {

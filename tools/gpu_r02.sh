@@ -15,7 +15,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file
   > gpurun_out/${tag}_ncu_launch.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"spread_v6_kernel" -s 1 -c 1 \
   -o gpurun_out/${tag}_spread -f $short > gpurun_out/${tag}_ncu_spread.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"interp_v7_kernel" -s 1 -c 1 \
+ncu --set full --import-source on --clock-control none -k regex:"interp_v7_kernel" -s 1 -c 1 --replay-mode application \
   -o gpurun_out/${tag}_interp -f $short > gpurun_out/${tag}_ncu_interp.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${tag}_smoke.txt 2>&1
 echo done
