@@ -61,39 +61,45 @@ __device__ __forceinline__ void v5_stage_batch(double* slot, const double* taps,
   cp_async_commit();
 }
 
-// The item's grid block -> the (padded) box: one warp per (x0, x1) row, lanes
-// over x2, the wrapped indices by compare-and-subtract.  (The flat loop it
+// The item's grid block -> the (padded) box: flat element loop, nine loads
+// in flight per thread, indices by multiply-shift division and
+// compare-and-subtract wrap.  (The flat loop it
 // replaces did two integer divisions and three modulos per element -- ~100
 // instructions each, 12-17 % of the interpolation's instruction stream at
 // configs 5 / 4, in kernels whose limit is the issue slot.)
+__device__ __forceinline__ int v5_wrap(int g, int M) {  // g in [0, M + ext): g mod M
+  if (g >= M) {
+    g -= M;
+    if (g >= M) g %= M;
+  }
+  return g;
+}
+
 template <int NT>
 __device__ __forceinline__ void v5_load_box(double* S, const double* gv, const DItem& it, int M, int bx1, int sp2,
                                             int tid) {
-  constexpr int W = NT / 32;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int e1 = it.e1, e2 = it.e2, rows = it.e0 * e1;
-  int x0 = 0, x1 = warp;
-  while (x1 >= e1) {
-    x1 -= e1;
-    ++x0;
-  }
-#pragma unroll 4
-  for (int row = warp; row < rows; row += W) {
-    int g0 = it.a0 + x0, g1 = it.a1 + x1;
-    while (g0 >= M) g0 -= M;
-    while (g1 >= M) g1 -= M;
-    const double* src = gv + (static_cast<int64_t>(g0) * M + g1) * M;
-    double* dst = S + (x0 * bx1 + x1) * sp2;
-    for (int x2 = lane; x2 < e2; x2 += 32) {
-      int g2 = it.a2 + x2;
-      while (g2 >= M) g2 -= M;
-      dst[x2] = src[g2];
+  constexpr int U = 9;  // loads in flight per thread (a 13^3 box is one round trip, 19^3 three)
+  const int e1 = it.e1, e2 = it.e2, total = it.e0 * e1 * e2;
+  // floor(v / e) = (v m) >> 20, m = floor(2^20 / e) + 1, exact while v e < 2^20:
+  // a box that fits shared memory has extents <= 30, 30^4 < 2^20
+  const unsigned m1 = (1u << 20) / static_cast<unsigned>(e1) + 1u, m2 = (1u << 20) / static_cast<unsigned>(e2) + 1u;
+  for (int v0 = tid; v0 < total; v0 += NT * U) {
+    double val[U];
+    int so[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = v0 + u * NT;
+      const bool ok = v < total;
+      const int row = static_cast<int>((static_cast<unsigned>(v) * m2) >> 20);
+      const int x0 = static_cast<int>((static_cast<unsigned>(row) * m1) >> 20);
+      const int x2 = v - row * e2, x1 = row - x0 * e1;
+      const int g0 = v5_wrap(it.a0 + x0, M), g1 = v5_wrap(it.a1 + x1, M), g2 = v5_wrap(it.a2 + x2, M);
+      so[u] = ok ? (x0 * bx1 + x1) * sp2 + x2 : -1;
+      val[u] = ok ? gv[(static_cast<int64_t>(g0) * M + g1) * M + g2] : 0.0;
     }
-    x1 += W;
-    while (x1 >= e1) {
-      x1 -= e1;
-      ++x0;
-    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (so[u] >= 0) S[so[u]] = val[u];
   }
 }
 

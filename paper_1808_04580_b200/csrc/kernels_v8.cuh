@@ -36,10 +36,10 @@
 namespace fgsb {
 
 #ifndef FGS_V8S_QS
-#define FGS_V8S_QS 32
+#define FGS_V8S_QS 64
 #endif
 #ifndef FGS_V8S_NS
-#define FGS_V8S_NS 3
+#define FGS_V8S_NS 2
 #endif
 #ifndef FGS_V8S_H
 #define FGS_V8S_H 2
