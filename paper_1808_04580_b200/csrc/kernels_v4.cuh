@@ -337,9 +337,15 @@ __global__ void __launch_bounds__(Blk4d2<T, PS>::NT) interp_v4_2d_kernel(PassArg
     v4_issue_chunk<TAPS, SR>(stg, a.taps, p_begin, static_cast<int>(lmin(QS, p_end - p_begin)), tid, NT);
     cp_async_commit();
     v4_stage_interp_x<NT, XW>(a, xv, p_begin, p_end, xs, ixs, tid);
-    for (int v = tid; v < V; v += NT) {
-      const int x2 = v % bx2, x1 = v / bx2;
-      S[v] = gv[static_cast<int64_t>((it.a1 + x1) % M) * M + (it.a2 + x2) % M];
+    {  // floor(v / bx2) by multiply-shift (exact while v bx2 < 2^20), wraps by compare-and-subtract
+      const unsigned mdiv = (1u << 20) / static_cast<unsigned>(bx2) + 1u;
+      for (int v = tid; v < V; v += NT) {
+        const int x1 = static_cast<int>((static_cast<unsigned>(v) * mdiv) >> 20), x2 = v - x1 * bx2;
+        int g1 = it.a1 + x1, g2 = it.a2 + x2;
+        if (g1 >= M) g1 = g1 - M < M ? g1 - M : g1 % M;
+        if (g2 >= M) g2 = g2 - M < M ? g2 - M : g2 % M;
+        S[v] = gv[static_cast<int64_t>(g1) * M + g2];
+      }
     }
     int r = it.run_begin;
     DRun run = a.runs[r];
