@@ -351,7 +351,8 @@ void launch_t(bool interp, bool dense, const PassArgs& a, int nitems, size_t sme
     if (a.slots != nullptr) {  // run-aligned slot layout: v6 interpolation; 2m = 16 v6 spread
       if (interp) {
         // two batches per B load: 2m = 16 (C5 interp 48.8 -> 47.8 ms); 2m = 12
-        // loses with it (C4 314 -> 332 us: fewer K-steps per B fragment)
+        // does not gain (C4 314 -> 332 us with per-item strides, 313 = 313 us
+        // with the fixed ones: fewer K-steps per B fragment)
         // (from 16 points per run: sparser plans rarely pair two batches of
         // one run, and v6 is 2 % faster there -- config 5 at 1.25M points)
         // fixed box strides for the plan's tile size (B = 2: 2m + 1, B = 4: 2m + 3)
