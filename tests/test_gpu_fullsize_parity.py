@@ -85,6 +85,29 @@ def test_dense_cells_block_matches_oracle(orc, m, N):
         assert rel_l2(op.apply_weight(xs[:, 1]), ref.apply_weight(xs[:, 1])) <= 1e-10
 
 
+@pytest.mark.parametrize("m,N,nvec", [(8, 64, 17), (6, 64, 5), (8, 64, 33)])
+def test_vector_split_ragged_blocks(orc, m, N, nvec):
+    # the slot-layout kernels launch one CTA per (item, share of the block's
+    # vectors) -- vsplit_narrow, csrc/common.cuh: blocks that do not divide
+    # into 16 shares (ragged shares, idle CTAs, two vectors per CTA) equal
+    # their column-wise applies bit for bit, and a column the oracle
+    rng = np.random.default_rng(40 + nvec)
+    n = 60_000
+    d = rng.standard_normal((n, 3))
+    X = 0.06 * d / np.linalg.norm(d, axis=1)[:, None] * rng.uniform(0, 1, (n, 1)) ** (1 / 3)
+    info = {"sigma": 0.3, "N": N, "m": m, "p": m}
+    op = _op(X, info)
+    st = op.plan_stats()
+    assert st["slot_layout"] and st["tensor_spread"] and st["tensor_interp"], st
+    xs = np.asfortranarray(rng.standard_normal((n, nvec)))
+    Y = op.apply_sym_laplacian(xs)
+    for j in (0, nvec // 2, nvec - 1):
+        assert np.array_equal(Y[:, j], op.apply_sym_laplacian(xs[:, j])), j
+    with orc.threads(THREADS):
+        ref = _ref(orc, X, info)
+        assert rel_l2(Y[:, nvec - 1], ref.apply_sym_laplacian(xs[:, nvec - 1])) <= 1e-10
+
+
 def _subspace_sin(U, V):
     Qu, _ = np.linalg.qr(U)
     Qv, _ = np.linalg.qr(V)
