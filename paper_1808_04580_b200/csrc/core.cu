@@ -1343,21 +1343,55 @@ static bool is_pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
-// sub-blocks of a host-vector block: the largest divisor of nvec with at
-// most nvec / 16 vectors (16 -> 1: the exposed copies are one sub-block's
-// H2D + D2H, 2 x 80 MB at config 5, instead of the whole 2 x 1.28 GB; C5 e2e
-// 141 / 148 / 153 matvecs/s with 4 / 2 / 1-vector sub-blocks, the kernels
-// cost the same per vector); FGS_PIPE_BLOCK=k forces k vectors per sub-block
-static int pipe_sub_block(int nvec) {
-  static const int forced = [] {
-    const char* e = std::getenv("FGS_PIPE_BLOCK");
-    return e ? std::atoi(e) : 0;
+// Sub-blocks of a host-vector block.  The copy streams move one sub-block
+// while the compute stream applies another, so the exposed copies are the
+// first sub-block's upload and the last one's download: both one vector.
+// Sub-blocks in between grow (and shrink again towards the end) as fast as
+// the copies allow -- a multi-vector apply is cheaper per vector than
+// single-vector ones (shared taps reads, fewer wave tails, one convolution
+// launch), and the upload of sub-blocks 1..k+1 only has to finish while
+// 1..k compute: S_{k+1} <= 1 + rho S_k, rho = compute / copy time per vector
+// (d = 3: ~2.7e-3 (2m)^3 / 3 with PCIe at ~50 GB/s; config 5: 16 vectors ->
+// 1 2 5 5 2 1).  Copy-bound plans (rho < 1) keep single-vector sub-blocks.
+// FGS_PIPE_PARTS="1,3,8,3,1" forces a partition (tuning).
+static std::vector<int> pipe_partition(int nvec, int d, int T) {
+  static const std::vector<int> forced = [] {
+    std::vector<int> v;
+    if (const char* e = std::getenv("FGS_PIPE_PARTS")) {
+      const std::string str(e);
+      size_t pos = 0;
+      while (pos < str.size()) {
+        const size_t c = str.find(',', pos);
+        v.push_back(std::atoi(str.substr(pos, c == std::string::npos ? std::string::npos : c - pos).c_str()));
+        if (c == std::string::npos) break;
+        pos = c + 1;
+      }
+    }
+    return v;
   }();
-  if (forced > 0 && nvec % forced == 0) return forced;
-  const int target = std::max(1, nvec / 16);
-  for (int b = target; b >= 1; --b)
-    if (nvec % b == 0) return b;
-  return 1;
+  if (!forced.empty() && std::accumulate(forced.begin(), forced.end(), 0) == nvec &&
+      *std::min_element(forced.begin(), forced.end()) > 0)
+    return forced;
+  const double rho = d == 3 ? 0.8 * 9.1e-4 * T * T * T : 0.0;
+  constexpr int kCap = 8;  // largest sub-block (bounds the extra workspaces)
+  std::vector<int> head;
+  int S = 0, b = 1;
+  while (rho > 1.0 && 2 * (S + b) <= nvec) {
+    head.push_back(b);
+    S += b;
+    b = std::max(1, std::min(kCap, static_cast<int>(1.0 + rho * S) - S));
+  }
+  if (head.empty()) return std::vector<int>(static_cast<size_t>(nvec), 1);
+  std::vector<int> parts(head);
+  int mid = nvec - 2 * S;
+  while (mid > 0) {  // the middle in near-equal sub-blocks of <= kCap vectors
+    const int pieces = (mid + kCap - 1) / kCap;
+    const int take = (mid + pieces - 1) / pieces;
+    parts.push_back(take);
+    mid -= take;
+  }
+  parts.insert(parts.end(), head.rbegin(), head.rend());
+  return parts;
 }
 
 bool Core::apply_host_graph(int epilogue, const double* hx, double* hy, int64_t ld, int nvec, bool scale_input) {
@@ -1381,9 +1415,9 @@ bool Core::apply_host_graph(int epilogue, const double* hx, double* hy, int64_t 
       return true;
     }
   }
-  const int nb = pipe_sub_block(nvec);
-  const int nsub = nvec / nb;
-  workspace(nb);
+  const std::vector<int> parts = pipe_partition(nvec, d, T);
+  const int nsub = static_cast<int>(parts.size());
+  for (int b : parts) workspace(b);
   if (nsub > 1) {
     if (!cp_in) FGS_CUDA(cudaStreamCreateWithFlags(&cp_in, cudaStreamNonBlocking));
     if (!cp_out) FGS_CUDA(cudaStreamCreateWithFlags(&cp_out, cudaStreamNonBlocking));
@@ -1428,17 +1462,18 @@ bool Core::apply_host_graph(int epilogue, const double* hx, double* hy, int64_t 
       FGS_CUDA(cudaEventRecord(fork, stream));
       FGS_CUDA(cudaStreamWaitEvent(cp_in, fork, 0));
       FGS_CUDA(cudaStreamWaitEvent(cp_out, fork, 0));
-      for (int k = 0; k < nsub; ++k) {
+      for (int k = 0, v0 = 0; k < nsub; v0 += parts[static_cast<size_t>(k)], ++k) {
+        const int nb = parts[static_cast<size_t>(k)];
         cudaEvent_t in_done = pipe_ev[static_cast<size_t>(3 + 2 * k)];
         cudaEvent_t ap_done = pipe_ev[static_cast<size_t>(4 + 2 * k)];
-        h2d(k * nb, nb, cp_in);
+        h2d(v0, nb, cp_in);
         FGS_CUDA(cudaEventRecord(in_done, cp_in));
         FGS_CUDA(cudaStreamWaitEvent(stream, in_done, 0));
-        apply_launches(epilogue, xbuf.p + static_cast<int64_t>(k) * nb * n, n,
-                       ybuf.p + static_cast<int64_t>(k) * nb * n, n, nb, true, scale_input);
+        apply_launches(epilogue, xbuf.p + static_cast<int64_t>(v0) * n, n, ybuf.p + static_cast<int64_t>(v0) * n, n,
+                       nb, true, scale_input);
         FGS_CUDA(cudaEventRecord(ap_done, stream));
         FGS_CUDA(cudaStreamWaitEvent(cp_out, ap_done, 0));
-        d2h(k * nb, nb, cp_out);
+        d2h(v0, nb, cp_out);
       }
       // join both copy streams back into the capture stream
       FGS_CUDA(cudaEventRecord(pipe_ev[1], cp_in));
