@@ -187,7 +187,10 @@ class NfftPlan:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().fgs_nfft_destroy(self._h)
+            try:
+                lib().fgs_nfft_destroy(self._h)
+            except Exception:  # noqa: BLE001 - interpreter teardown: module globals already gone
+                pass
             self._h = None
 
     def dims(self):
@@ -248,7 +251,10 @@ class FastsumPlan:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().fgs_fastsum_destroy(self._h)
+            try:
+                lib().fgs_fastsum_destroy(self._h)
+            except Exception:  # noqa: BLE001 - interpreter teardown: module globals already gone
+                pass
             self._h = None
 
     def size(self):
@@ -338,7 +344,10 @@ class AdjacencyOperator:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().fgs_adjacency_destroy(self._h)
+            try:
+                lib().fgs_adjacency_destroy(self._h)
+            except Exception:  # noqa: BLE001 - interpreter teardown: module globals already gone
+                pass
             self._h = None
 
     @property
