@@ -10,10 +10,10 @@
 //                 accumulates its own point's 4 tail columns
 //                 D[t][e'] += af[t] * we_q[8 + e'] and the 4 q-lanes are summed
 //                 once per run (a 4 x 4 transpose-reduce: 3 shuffles).
-// On this B200 a DFMA costs the fp64 pipe 2 cycles for 32 FMAs, a DMMA 16 for
-// 256 -- the same rate -- so the tail costs 4/8 of a DMMA's pipe time instead
-// of a whole padded one: per warp K-step 3 DMMA + 12 DFMA + 4 DMUL = 80 pipe
-// cycles for 72 cycles of useful FMAs (v4: 18 DMMA + 11 DMUL = 310 for 216).
+// On this B200 a DFMA costs the fp64 pipe ~2.25 cycles for 32 FMAs, a DMMA 16
+// for 256 -- nearly the same rate, and mixing them is free
+// (tools/dmma_dfma_probe.cu: 3 DMMA + 12 DFMA = 81 cycles, ideal 72) -- so the
+// tail costs about half a padded DMMA's pipe time.
 //
 // W = 6 / H warps; warp w owns the box c-rows = w (mod W) -- in a run with
 // origin o1 its 2 H c values are cw + W j, cw = (w - o1) mod W -- and all 12
@@ -22,10 +22,12 @@
 // Flushes of consecutive runs never touch another warp's rows, so there is
 // no barrier per run (the v4 kernel's two point streams flushed in turn
 // through two CTA barriers per run).  x is folded into wc once per K-step.
-// The kernel is shared-memory-bandwidth bound next to the fp64 pipe: a lane
-// loads 80 B of operands per K-step at H = 1 (ncu: 73 % of the LSU wavefront
-// peak at 65 % fp64 pipe), all but wc shared by the H tile rows, so H = 2
-// halves the operand wavefronts per FMA.
+// Measured (config 4): 0.356 ms with 2, 4 or 6 c-rows per warp (H = 1, 2, 3)
+// and 12-24 warps per SM alike -- neither shared-memory bandwidth (73 % of the
+// LSU wavefront peak at H = 1, 40 % at H = 2) nor occupancy binds; what does
+// is issue slots: a DMMA holds its scheduler's issue port for 16 cycles and
+// every other instruction adds its own.  H = 2 issues the
+// fewest instructions per FMA that still fit 4 CTAs per SM.
 // Staging is the v6 spread's ring of bulk-copied chunks on full/empty
 // mbarriers.  The slot rows are 36 doubles (wa | wc | we), = 4 (mod 16), so
 // the 4 slots of a K-step sit on distinct bank groups.
