@@ -699,6 +699,9 @@ def run_b200(args, rank, world, local_rank):
             "data": "synthetic (seeded stand-in for the paper's datasets)", "config": cfg,
             "parallelism": f"points sharded x{world} (NCCL)" if sharded else "single GPU",
             "l2": "flushed (256 MB write) between timed steps, outside the events",
+            "vectors": ("value: device-resident block in the handle's internal (spatially sorted) order, the "
+                        "order the Lanczos basis is kept in (fgs_adjacency_apply_device); e2e: host vectors in "
+                        "the caller's order, permuted inside the handle"),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(w0, w1), "lanczos": lanczos, "setup_s": setup_s, "also": also,
         }
