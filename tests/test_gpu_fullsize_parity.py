@@ -85,6 +85,30 @@ def test_dense_cells_block_matches_oracle(orc, m, N):
         assert rel_l2(op.apply_weight(xs[:, 1]), ref.apply_weight(xs[:, 1])) <= 1e-10
 
 
+@pytest.mark.parametrize("m", [8, 6])
+def test_very_dense_cells_small_tiles(orc, m):
+    # >= 100 points per nonempty cell: the plan takes 2-cell tiles, so the
+    # slot-layout interpolation runs its fixed-extent box of 2m + 1 cells per
+    # dimension (interp_v7<16, 17> / interp_v6<12, 13>; the other dense cases
+    # have 4-cell tiles, extent 2m + 3)
+    rng = np.random.default_rng(70 + m)
+    n = 100_000
+    d = rng.standard_normal((n, 3))
+    X = 0.03 * d / np.linalg.norm(d, axis=1)[:, None] * rng.uniform(0, 1, (n, 1)) ** (1 / 3)
+    info = {"sigma": 0.3, "N": 32, "m": m, "p": m}
+    op = _op(X, info)
+    st = op.plan_stats()
+    assert st["slot_layout"] and st["mean_run"] >= 32.0, st  # runs are cut at the item size (64 points)
+    xs = np.asfortranarray(rng.standard_normal((n, 3)))
+    Y = op.apply_sym_laplacian(xs)
+    assert np.array_equal(Y[:, 2], op.apply_sym_laplacian(xs[:, 2]))
+    with orc.threads(THREADS):
+        ref = _ref(orc, X, info)
+        assert rel_l2(op.degrees(), ref.degrees()) <= 1e-10
+        for j in range(3):
+            assert rel_l2(Y[:, j], ref.apply_sym_laplacian(xs[:, j])) <= 1e-10
+
+
 @pytest.mark.parametrize("m,N,nvec", [(8, 64, 17), (6, 64, 5), (8, 64, 33)])
 def test_vector_split_ragged_blocks(orc, m, N, nvec):
     # the slot-layout kernels launch one CTA per (item, share of the block's
