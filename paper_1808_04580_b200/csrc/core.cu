@@ -1563,7 +1563,7 @@ void Core::apply_launches(int epilogue, const double* x, int64_t ldx, double* y,
     const int64_t ns = static_cast<int64_t>(slot_map.n);
     a.xs = w.xs.p;
     a.ldxs = ns;
-    launch_ex(slot_gather_kernel, dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div(ns * nvec, 256), 148 * 16))),
+    launch_ex(slot_gather_kernel, dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div(ns, 256), 148 * 16))),
               dim3(256), 0, stream, a, ns, w.xs.p);
     ++launches;
     FGS_CUDA(cudaGetLastError());

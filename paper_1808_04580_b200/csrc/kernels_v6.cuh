@@ -88,18 +88,49 @@ constexpr size_t v6s_extra_doubles() {
 // (scale_input) or x[src], 0 on pad slots (v2_x over the slot map)
 __global__ void slot_gather_kernel(PassArgs a, int64_t nslots, double* out) {
   pdl_wait();
-  const int64_t total = nslots * a.nvec;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t v = i / nslots, sl = i - v * nslots;
-    const int src = a.slots[sl];
-    double val = 0.0;
-    if (src >= 0) {
-      const int64_t ix = a.perm ? static_cast<int64_t>(a.perm[src]) : src;
-      val = a.x[v * a.ldx + ix];
-      if (a.scale_input) val = __dmul_rn(a.s[src], val);
+  if (a.perm != nullptr) {
+    // caller order: x[perm[src]] is a random gather, so one vector at a time
+    // (an 80 MB vector stays in L2; all vectors of a slot at once measured
+    // 98.7 -> 99.9 ms on the caller-order config-5 block)
+    const int64_t total = nslots * a.nvec;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t v = i / nslots, sl = i - v * nslots;
+      const int src = a.slots[sl];
+      double val = 0.0;
+      if (src >= 0) {
+        val = a.x[v * a.ldx + a.perm[src]];
+        if (a.scale_input) val = __dmul_rn(a.s[src], val);
+      }
+      out[v * nslots + sl] = val;
     }
-    out[v * nslots + sl] = val;
+    return;
+  }
+  // internal order: one thread per slot, all vectors of the block -- the slot
+  // map and s are read once per slot instead of once per (slot, vector)
+  // (config 5, 16 vectors: 1.13 -> 0.5 ms)
+  for (int64_t sl = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; sl < nslots;
+       sl += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int src = a.slots[sl];
+    if (src < 0) {
+      for (int v = 0; v < a.nvec; ++v) out[v * nslots + sl] = 0.0;
+      continue;
+    }
+    const double sc = a.scale_input ? a.s[src] : 1.0;
+    const double* xp = a.x + src;
+    double* op = out + sl;
+    int v = 0;
+    for (; v + 4 <= a.nvec; v += 4) {
+      double val[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) val[u] = xp[(v + u) * a.ldx];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) op[(v + u) * nslots] = a.scale_input ? __dmul_rn(sc, val[u]) : val[u];
+    }
+    for (; v < a.nvec; ++v) {
+      const double val = xp[v * a.ldx];
+      op[v * nslots] = a.scale_input ? __dmul_rn(sc, val) : val;
+    }
   }
 }
 
